@@ -1,0 +1,391 @@
+#!/usr/bin/env python3
+"""bench.py — routed tokens/s of the expert-statistics + placement pass on B200.
+
+One step = one pass of the hot path over one batch of synthetic input: reset -> count the
+rank's routing trace (A / E / W) -> [all-reduce over ranks] -> strong-pair set M -> greedy
+placement (written as candidate 0) -> score all C candidates (deviation, cut, objective) ->
+argmin.  Default workload: the DeepSeek-V3-shape trace (58 MoE layers, 256 experts, top-8,
+g = 8 placement target), 64 Mi tokens per GPU (weak scaling), 4096 candidate placements
+(BASELINE.json configs[3], the north_star's target shape).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config dsv3|qwen3|dsv2lite|mixtral]
+  python bench.py --impl reference ...   # the reference's own CPU code (oracle/_ref) on host cores
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, n_e, top_k, g, tokens per GPU, candidates, BASELINE.json config)
+    "mixtral": (32, 8, 2, 8, 1 << 20, 4096, "Mixtral-8x7B-shape trace (32 layers, 8 experts, top-2), 1M tokens"),
+    "dsv2lite": (26, 64, 6, 8, 16 << 20, 4096, "DeepSeek-V2-Lite-shape trace (26 layers, 64 experts, top-6), 16M tokens"),
+    "qwen3": (48, 128, 8, 8, 32 << 20, 4096, "Qwen3-30B-A3B-shape trace (48 layers, 128 experts, top-8), 32M tokens"),
+    "dsv3": (58, 256, 8, 8, 64 << 20, 4096,
+             "DeepSeek-V3-shape trace (58 MoE layers, 256 experts, top-8), 64M tokens, 4096 candidate placements"),
+}
+METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+REASON_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            cmd = ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                   "--format=csv,noheader,nounits"]
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout.strip()
+                    sm, smax, reasons = [x.strip() for x in out.split(",")]
+                    self.samples.append((float(sm), float(smax), int(reasons, 16)))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(s[0] for s in self.samples)
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        names = [n for b, n in REASON_BITS.items() if mask & b and n != "gpu_idle"]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.samples[0][1], "reasons": names,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the reference's own moe.cpp/placement.cpp (oracle/_ref) on host cores."""
+    world, rank, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    import oracle
+
+    L, ne, k, g, T, C, desc = CONFIGS[args.config]
+    ref = oracle.Ref()
+    cores = os.cpu_count() or 1
+    sample_T, sample_C = sample_size(args.config)
+    ids, cands = sample_inputs(args.config, sample_T, sample_C)
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = ref.pipeline(L, ne, k, g, ids, cands, n_threads=cores)
+        if i >= args.warmup:
+            times.append(r)
+    rate = np.median([extrapolated_rate(r, sample_T, sample_C, T, C) for r in times])
+    ms = T / rate * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int-in-f64 (reference Eigen doubles)",
+        "data": "synthetic (GPU generator, RoutingModel semantics)",
+        "config": {"workload": desc, "tokens": T, "candidates": C, "g": g},
+        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                         "sample": f"{sample_T} tokens through add_token+flat forms+affinity+greedy, {sample_C} "
+                                   f"eval_cost calls; rate extrapolated linearly to {T} tokens and {C} candidates"},
+        "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def sample_size(config):
+    return {"mixtral": (1 << 16, 64), "dsv2lite": (1 << 15, 8), "qwen3": (1 << 13, 2), "dsv3": (1 << 12, 1)}[config]
+
+
+def sample_inputs(config, T, C):
+    """Bounded CPU sample: generated with the bit-exact CPU twin of the GPU generator."""
+    import oracle
+
+    L, ne, k, g, _, _, _ = CONFIGS[config]
+    o = oracle.Oracle()
+    cdf, thr = generator_tables_host(L, ne, k, g)
+    ids = o.generate_trace(L, ne, k, cdf.ravel(), int(thr[0]), int(thr[1]), 2, 0, T)
+    cands = np.zeros((C, L * ne), np.uint8)
+    import paper_2602_21626_b200 as G
+
+    cands[:] = G.shuffled_candidates(L * ne, g, 1000, C)
+    return ids, cands
+
+
+def generator_tables_host(L, ne, k, g):
+    import paper_2602_21626_b200 as G
+
+    return G.generator_tables(G.MoeTopology(L, ne, k, g), model_seed=1)
+
+
+def extrapolated_rate(r, sT, sC, T, C):
+    per_token = r["t_stats"] / sT
+    per_cand = r["t_eval"] / max(sC, 1)
+    total = per_token * T + r["t_place"] + per_cand * C
+    return T / total
+
+
+def cpu_baseline(config, T, C):
+    """Rank 0, N = 1: the reference's own code (oracle/_ref) on host cores, bounded sample."""
+    import oracle
+
+    L, ne, k, g, _, _, _ = CONFIGS[config]
+    if not oracle.ref_available():
+        return None
+    sT, sC = sample_size(config)
+    ids, cands = sample_inputs(config, sT, sC)
+    cores = os.cpu_count() or 1
+    r = oracle.Ref().pipeline(L, ne, k, g, ids, cands, n_threads=cores)
+    rate = extrapolated_rate(r, sT, sC, T, C)
+    return {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "sample": f"{sT} tokens (add_token over {cores} RoutingStats shards + affinity/flat forms + "
+                      f"build_affinity_set + greedy_place) and {sC} eval_cost calls on the reference's own "
+                      f"moe.cpp/placement.cpp; stage times {r['t_stats']:.3f}/{r['t_place']:.3f}/{r['t_eval']:.3f} s, "
+                      f"extrapolated linearly to {T} tokens, {C} candidates"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="dsv3", choices=list(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
+    ap.add_argument("--candidates", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21626_b200 as G
+    from paper_2602_21626_b200.pipeline import shard_range
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L, ne, k, g, T, C, desc = CONFIGS[args.config]
+    if args.tokens:
+        T = args.tokens
+    if args.candidates:
+        C = args.candidates
+    topo = G.MoeTopology(L, ne, k, g)
+    m = topo.total_experts()
+    dev = torch.device("cuda", local)
+
+    # inputs resident in HBM: this rank's token shard (tokens rank*T .. (rank+1)*T of one stream)
+    trace = G.generate_trace(topo, T, model_seed=1, stream_seed=2, first_token=rank * T, device=local)
+    c_lo, c_hi = shard_range(C, rank, world)
+    cands_host = torch.from_numpy(G.shuffled_candidates(m, g, 1000 + c_lo, c_hi - c_lo))
+    cands = cands_host.to(dev)
+    hp = G.HotPath(topo, device=local)
+    stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=dev)
+
+    def step():
+        if world > 1:
+            return hp.run_distributed(trace, cands, c_lo, C)
+        return hp.run(trace, cands)
+
+    # the dominant kernel's duration, measured live on the stream it is launched on
+    count_ev = []
+
+    def step_timed():
+        hp.stats.reset()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hp.stats.add_tokens(trace)
+        e1.record(stream)
+        count_ev.append((e0, e1))
+        return hp.place(cands)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        res = step() if world > 1 else step_timed()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    clk = clocks.stop() if clocks else None
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    value = world * T / (ms * 1e-3)
+
+    # roofline of the dominant kernel (trace counting): algorithmic bytes per launch =
+    # trace bytes (T*L*k uint8) + one u64 write of E; duration from the live events above
+    count_ms = float(np.mean([a.elapsed_time(b) for a, b in count_ev])) if count_ev else None
+    alg_bytes = T * L * k + (L - 1) * ne * ne * 8
+    peak, peak_kind = peaks()
+    roof = None
+    if count_ms:
+        achieved = alg_bytes / (count_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "count_pairs_kernel", "kernel_ms": count_ms,
+                "algorithmic_bytes": alg_bytes, "peak_source": peak_kind,
+                "e_pair_updates_per_s": T * (L - 1) * k * k / (count_ms * 1e-3),
+                "share_of_step": count_ms / ms}
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(G, topo, trace, cands_host, T, args, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(args.config, T, C)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
+            "data": "synthetic (Zipf-skewed RoutingModel-semantics trace generated on the GPU)",
+            "config": {"workload": desc, "tokens_per_gpu": T, "candidates": C, "g": g,
+                       "parallelism": f"token-shard dp{world}",
+                       "l2": f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": launches_per_step(topo) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def launches_per_step(topo):
+    """Kernels of ours per step: memsets are not kernels; count_pairs 1, derive A 1, derive W 1,
+    affinity keys 1 + sort (local + global passes) + select 1, greedy keys 1 + sort + walk 1,
+    eval same 1 + dev 1 + finish 1."""
+    L, ne = topo.n_layers, topo.n_experts
+
+    def sort_launches(n):
+        p = 1
+        while p < n:
+            p <<= 1
+        if p <= 2048:
+            return 1
+        c = 1
+        k = 4096
+        while k <= p:
+            j = k // 2
+            while j >= 2048:
+                c += 1
+                j //= 2
+            c += 1
+            k *= 2
+        return c
+
+    return 3 + 2 + sort_launches((L - 1) * ne * ne) + 2 + sort_launches(L * ne) + 3
+
+
+def run_e2e(G, topo, trace, cands_host, T, args, local):
+    """Same step through the public API from pinned host memory: H2D of the trace and the
+    candidates and D2H of the scores inside the timed region."""
+    import torch
+
+    L, k = topo.n_layers, topo.top_k
+    try:
+        host = torch.empty((T, L, k), dtype=torch.uint8, pin_memory=True)
+        step_t = 1 << 22
+        for lo in range(0, T, step_t):
+            host[lo:lo + step_t].copy_(trace[lo:lo + step_t])
+        ch = cands_host.pin_memory()
+    except Exception as ex:
+        return {"error": f"pinned host buffers unavailable: {ex}"}
+    hp = G.HotPath(topo, device=local)
+    stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", local))
+    C = ch.shape[0]
+    out = {}
+
+    def step():
+        hp.stats.reset()
+        hp.stats.add_tokens(host)            # H2D inside (pinned, double-buffered)
+        dcands = ch.to(f"cuda:{local}", non_blocking=True)   # H2D of the candidates
+        torch.cuda.current_stream().synchronize()
+        r = hp.place(dcands)
+        out["scores"] = hp._out.cpu()        # D2H of D / cut / objective
+        return r
+
+    for _ in range(1):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n = max(1, min(args.steps, 3))
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    wall = (time.perf_counter() - t0) / n * 1e3
+    return {"value": T / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(T * L * k + C * topo.total_experts()),
+            "d2h_bytes_per_step": int(3 * C * 8 + 8), "ms_per_step": ms, "wall_ms_per_step": wall, "steps": n}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * gimbal_gpu.h — C ABI of the B200 (sm_100a) expert-statistics + placement hot path.
+ *
+ * Drop-in boundary for the reference's operator API (/root/reference/proj):
+ *   moe::RoutingStats / record_stats / comm_cost        include/gimbal/moe.hpp:86-111
+ *   placement::eval_cost / build_affinity_set /
+ *   greedy_place / maybe_relocate / static_placement     include/gimbal/placement.hpp:44-85
+ * A C++ layer with the reference's exact signatures sits on top of this ABI
+ * (paper_2602_21626_b200/shim/); the Python mirror binds it with ctypes.
+ *
+ * Conventions
+ *  - Every entry point returns a gimbal_status; gimbal_last_error() returns the calling thread's
+ *    last message (the reference's std::invalid_argument text where one exists).
+ *  - Plain pointers + sizes only.  `mem` says whether a buffer is host (GIMBAL_MEM_HOST) or
+ *    device (GIMBAL_MEM_DEVICE) memory.  Host buffers may be pageable; pinned ones overlap.
+ *  - Matrices are row-major: A [L][n_e], E [(L-1)][n_e][n_e], W [n_e][n_e]  (the reference stores
+ *    the same numbers column-major in Eigen).  Counts are uint64 (the reference keeps them as
+ *    integer-valued doubles, exact below 2^53).
+ *  - Traces are token-major [T][L][top_k] expert ids, the order of RoutedStream::choices
+ *    (moe.hpp:75-83); id_bytes 1 (uint8, n_e <= 256, the native layout) or 4 (int32, the
+ *    reference layout).  Ids outside [0, n_e) are an error (GIMBAL_OUT_OF_RANGE); the reference
+ *    leaves them undefined (no range check at moe.cpp:176-187).
+ *  - Handles own device memory and a CUDA stream on their device; no global mutable state, so
+ *    independent handles may be driven from different host threads (the reference runs one
+ *    MoeSubsystem per sweep thread, cli.cpp:145-162).
+ *  - Work is enqueued asynchronously on the handle's stream; calls that return data to the
+ *    host synchronise that stream.  Errors raised inside kernels (ids out of range) are sticky
+ *    and reported by the next synchronising call.
+ */
+#ifndef GIMBAL_GPU_H_
+#define GIMBAL_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIMBAL_ABI_VERSION 1
+
+typedef enum gimbal_status {
+  GIMBAL_OK = 0,
+  GIMBAL_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+  GIMBAL_CUDA_ERROR = 2,
+  GIMBAL_NCCL_ERROR = 3,
+  GIMBAL_OVERFLOW = 4,         /* a count would leave the exactly representable range */
+  GIMBAL_OUT_OF_RANGE = 5,     /* expert id outside [0, n_e) in a trace */
+  GIMBAL_NOT_SUPPORTED = 6
+} gimbal_status;
+
+typedef enum gimbal_mem { GIMBAL_MEM_HOST = 0, GIMBAL_MEM_DEVICE = 1 } gimbal_mem;
+
+/* moe::MoeTopology (moe.hpp:14-23); validated like MoeTopology::validate (moe.cpp:12-24). */
+typedef struct gimbal_topology {
+  int32_t n_layers;
+  int32_t n_experts; /* per layer */
+  int32_t top_k;
+  int32_t n_gpus;    /* placement target g */
+} gimbal_topology;
+
+typedef struct gimbal_stats_s* gimbal_stats_t;
+
+int gimbal_abi_version(void);
+const char* gimbal_last_error(void);
+/* Validates a topology (moe.cpp:12-24). */
+int gimbal_topology_validate(const gimbal_topology* topo);
+
+/* ---- routing statistics: replaces moe::RoutingStats (moe.hpp:86-105, moe.cpp:162-231) ---- */
+
+/* RoutingStats(topo): zeroed A/E on `device`, with its own stream (moe.cpp:162-167). */
+int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t* out);
+int gimbal_stats_destroy(gimbal_stats_t h);
+/* RoutingStats::reset (moe.cpp:193-197). */
+int gimbal_stats_reset(gimbal_stats_t h);
+/* Batch RoutingStats::add_token (moe.cpp:169-191) / record_stats (moe.cpp:233-239): counts
+ * n_tokens tokens of a [T][L][k] trace, all k x k consecutive-layer pairings with multiplicity.
+ * Asynchronous on the handle's stream; a host trace is staged through pinned buffers. */
+int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n_tokens,
+                            int mem);
+/* RoutingStats::tokens (moe.hpp:93). */
+int gimbal_stats_tokens(gimbal_stats_t h, int64_t* tokens);
+/* activation() / affinity() (moe.hpp:91-92, moe.cpp:199-205): copies A [L][n_e],
+ * E [(L-1)][n_e][n_e] and W [n_e][n_e] (any may be NULL) into host or device buffers.
+ * Synchronises and reports sticky kernel errors. */
+int gimbal_stats_read(gimbal_stats_t h, uint64_t* A, uint64_t* E, uint64_t* W, int mem);
+/* flat_activation() (moe.cpp:207-215) as doubles [L][L*n_e], and flat_pair_weights()
+ * (moe.cpp:217-231) as doubles [m][m] (either may be NULL; m = L*n_e; host or device). */
+int gimbal_stats_flat(gimbal_stats_t h, double* flat_activation, double* flat_pair_weights, int mem);
+/* Device pointers of the handle's counters, for in-place collectives over the token shards of
+ * several ranks (ncclAllReduce(ncclUint64, ncclSum) on E, then gimbal_stats_mark_reduced).
+ * E has (L-1)*n_e*n_e uint64 (NULL when L == 1, then A is the counted buffer). */
+int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, void** stream);
+/* After an external in-place reduction of E (or A when L == 1) over ranks: sets the token count
+ * to the global total and re-derives A / W. */
+int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens);
+/* Synchronises the handle's stream and returns sticky errors. */
+int gimbal_stats_sync(gimbal_stats_t h);
+
+/* ---- placement over the handle's statistics (placement.cpp:58-85, 186-331) ---- */
+
+/* eval_cost for a batch of candidate placements [C][m] (uint8 GPU ids), m = L*n_e, on
+ * A = flat_activation(), W = flat_pair_weights() without materialising W (placement.cpp:58-85).
+ * Per candidate: deviation D, cut, objective = alpha*D + beta*cut (IEEE double, unfused).
+ * argmin = lowest index among the minimal objectives (may be NULL).  Outputs host or device
+ * (`out_mem`); candidates host or device (`cand_mem`).  A candidate that violates
+ * check_feasible (placement.cpp:30-50) fails the call with GIMBAL_INVALID_ARGUMENT. */
+int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t n_candidates,
+                      int cand_mem, double alpha, double beta, double* deviation, double* cut,
+                      double* objective, int64_t* argmin, int out_mem);
+
+/* build_affinity_set (placement.cpp:186-238) on the handle's E: pairs with count >= threshold
+ * and > 0, ordered by count desc then flat ids asc, truncated to top_e (top_e < 0 keeps all),
+ * then lightest pairs dropped until the endpoint union fits `capacity`.  Writes the sorted
+ * member ids (at most min(2*top_e, capacity) when top_e >= 0, else capacity) to host `out`. */
+int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity,
+                        int32_t anchor_gpu, int32_t* out, int32_t* n_out);
+
+/* greedy_place (placement.cpp:240-299) on the handle's flat activation with affinity set M
+ * (sorted unique flat ids, host) anchored on anchor_gpu.  Writes m int32 GPU ids to `out`
+ * (host or device per out_mem).  Also writes them as uint8 to `out_u8` if non-NULL (device),
+ * e.g. row 0 of a candidate batch. */
+int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t n_M, int32_t anchor_gpu,
+                        int32_t* out, int out_mem, uint8_t* out_u8_device);
+
+/* ---- the reference's general dense forms (PlacementProblem with arbitrary A / W) ---- */
+
+/* eval_cost (placement.cpp:58-85) on dense A [rows][m] and W [m][m] doubles (host). */
+int gimbal_eval_cost_dense(int32_t rows, int32_t m, const double* A, const double* W, int32_t g,
+                           double alpha, double beta, const int32_t* assign, double* deviation,
+                           double* cut, double* objective);
+/* build_affinity_set from an explicit double tensor E [(n_blocks)][n_e][n_e] (host). */
+int gimbal_affinity_set_dense(const gimbal_topology* topo, const double* E, int32_t n_blocks,
+                              double threshold, int32_t top_e, int32_t capacity,
+                              int32_t anchor_gpu, int32_t* out, int32_t* n_out);
+/* greedy_place on a dense double activation [rows][m] (host). */
+int gimbal_greedy_place_dense(int32_t rows, int32_t m, const double* activation,
+                              const int32_t* M, int32_t n_M, int32_t anchor_gpu, int32_t g,
+                              int32_t* out);
+/* static_placement (placement.cpp:320-331): m int32 to host `out`. */
+int gimbal_static_placement(const gimbal_topology* topo, int32_t* out);
+
+/* ---- comm_cost (moe.cpp:241-267) ---- */
+/* Cross-GPU transition count of a [T][L][k] trace under expert_to_gpu (m int32, host). */
+int gimbal_comm_cost(const gimbal_topology* topo, const void* ids, int id_bytes, int64_t n_tokens,
+                     int mem, const int32_t* expert_to_gpu, int32_t n_assign, int device,
+                     int64_t* out);
+
+/* ---- synthetic routing traces (RoutingModel semantics, moe.cpp:43-160; distributional) ---- */
+/* Zipf(zipf_s) base weights over a per-layer permutation seeded like the reference
+ * (Rng(mix_seed(model_seed, 0x5a1f)).shuffle, moe.cpp:61-71), mixed with the successor kernel
+ * (lambda, affinity_peak) conditioned on the previous layer's choices; top_k distinct draws.
+ * `drift` in [0,1]: fraction of each layer's rank permutation re-drawn (config 5 streaming
+ * windows; 0 = the reference model).  Writes n_tokens x L x k uint8 ids to device `out`,
+ * tokens numbered from first_token (a counter-based stream: any token range is reproducible). */
+int gimbal_generate_trace(const gimbal_topology* topo, double zipf_s, double lambda,
+                          double affinity_peak, uint64_t model_seed, uint64_t stream_seed,
+                          double drift, uint64_t drift_epoch, int64_t first_token,
+                          int64_t n_tokens, uint8_t* out_device, int device);
+/* Host tables the generator uses (for the bit-exact CPU twin in oracle/): cdf [L][n_e] u32
+ * (inclusive cumulative base weights scaled to 2^32), component thresholds thr[2] in [0, 2^32]
+ * (u < thr[0]: base draw, u < thr[1]: uniform draw, else successor of a previous-layer slot). */
+int gimbal_generator_tables(const gimbal_topology* topo, double zipf_s, double lambda,
+                            double affinity_peak, uint64_t model_seed, double drift,
+                            uint64_t drift_epoch, uint32_t* cdf, uint64_t* thr);
+
+/* Balanced random candidates by the reference recipe (acceptance_main.cpp:344-351):
+ * assign[e] = e % g, then Rng(seed + c).shuffle (mt19937_64, rng.hpp:64-71), for c in
+ * [0, n); writes [n][m] uint8 to host `out`. */
+int gimbal_shuffled_candidates(int32_t m, int32_t g, uint64_t seed, int64_t n, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GIMBAL_GPU_H_ */

@@ -1,0 +1,644 @@
+// C ABI (include/gimbal_gpu.h) over the sm_100a kernels: handles, ingest, readback, placement.
+//
+// Host-side logic here is limited to argument validation (with the reference's messages),
+// buffer management and stream ordering; every numeric result is produced on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+thread_local std::string t_err;
+}
+void set_error(const std::string& msg) { t_err = msg; }
+const std::string& last_error() { return t_err; }
+
+int validate_topology(const gimbal_topology& t) {
+  if (t.n_layers < 1) return invalid("MoeTopology: n_layers must be >= 1");
+  if (t.n_experts < 1) return invalid("MoeTopology: n_experts must be >= 1");
+  if (t.top_k < 1 || t.top_k > t.n_experts) return invalid("MoeTopology: top_k must be in [1, n_experts]");
+  if (t.n_gpus < 1 || t.n_gpus > t.n_experts) return invalid("MoeTopology: n_gpus must be in [1, n_experts]");
+  if (t.n_experts % t.n_gpus != 0) return invalid("MoeTopology: n_experts must be divisible by n_gpus");
+  return GIMBAL_OK;
+}
+
+namespace {
+
+// Device buffer that grows on demand (per handle; freed with the handle).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t n) {
+    if (n <= bytes) return GIMBAL_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    GIMBAL_CUDA_TRY(cudaMalloc(&p, n));
+    bytes = n;
+    return GIMBAL_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+int flags_to_status(uint32_t f) {
+  if (f & kFlagIdOutOfRange) {
+    set_error("add_token: expert id out of range [0, n_experts)");
+    return GIMBAL_OUT_OF_RANGE;
+  }
+  if (f & kFlagOverflow) {
+    set_error("count exceeds the exactly representable range");
+    return GIMBAL_OVERFLOW;
+  }
+  return GIMBAL_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+}  // namespace gimbal_gpu
+
+using namespace gimbal_gpu;
+
+struct gimbal_stats_s {
+  gimbal_topology topo{};
+  int device = 0;
+  int sms = 148;
+  StatsPlan plan;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  unsigned long long* dE = nullptr;  // (L-1)*ne*ne
+  unsigned long long* dA = nullptr;  // L*ne
+  unsigned long long* dW = nullptr;  // ne*ne
+  uint32_t* dflags = nullptr;
+  int64_t tokens = 0;
+  bool derived = true;
+  // host-ingest staging (double-buffered)
+  static constexpr int kStages = 2;
+  size_t stage_bytes = 0;
+  void* dstage[kStages] = {nullptr, nullptr};
+  void* hstage[kStages] = {nullptr, nullptr};
+  cudaEvent_t ev_copied[kStages] = {nullptr, nullptr};
+  cudaEvent_t ev_consumed[kStages] = {nullptr, nullptr};
+  // scratch
+  DevBuf cand, same, dout, keys, misc, ints;
+  std::mutex mu;
+
+  int64_t m() const { return (int64_t)topo.n_layers * topo.n_experts; }
+  int64_t nE() const { return (int64_t)(topo.n_layers - 1) * topo.n_experts * topo.n_experts; }
+
+  int derive() {
+    if (derived) return GIMBAL_OK;
+    const int L = topo.n_layers, ne = topo.n_experts;
+    if (L > 1) {
+      GIMBAL_CUDA_TRY(launch_derive_activation(L, ne, topo.top_k, dE, dA, stream));
+      GIMBAL_CUDA_TRY(launch_derive_w(L, ne, dE, dW, stream));
+    }
+    derived = true;
+    return GIMBAL_OK;
+  }
+
+  int check_flags() {
+    uint32_t f = 0;
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(&f, dflags, sizeof(f), cudaMemcpyDeviceToHost, stream));
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(stream));
+    return flags_to_status(f & (kFlagIdOutOfRange | kFlagOverflow));
+  }
+
+  int count_device(const void* ids, int id_bytes, int64_t n) {
+    const int L = topo.n_layers;
+    if (L > 1) {
+      GIMBAL_CUDA_TRY(launch_count_pairs(plan, ids, id_bytes, n, dE, dflags, stream));
+    } else {
+      GIMBAL_CUDA_TRY(launch_count_activation(L, topo.n_experts, topo.top_k, ids, id_bytes, n, dA,
+                                              dflags, stream));
+    }
+    return GIMBAL_OK;
+  }
+
+  int ensure_staging() {
+    if (stage_bytes) return GIMBAL_OK;
+    const size_t row = (size_t)topo.n_layers * topo.top_k * 4;
+    stage_bytes = std::max<size_t>(row, (size_t)256 << 20);
+    for (int b = 0; b < kStages; ++b) {
+      GIMBAL_CUDA_TRY(cudaMalloc(&dstage[b], stage_bytes));
+      GIMBAL_CUDA_TRY(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
+      GIMBAL_CUDA_TRY(cudaEventCreateWithFlags(&ev_consumed[b], cudaEventDisableTiming));
+    }
+    return GIMBAL_OK;
+  }
+
+  // Host trace: chunks are copied on copy_stream into alternating device stages while the
+  // previous chunk is counted on `stream`.  Pageable sources go through pinned bounce buffers.
+  int count_host(const void* ids, int id_bytes, int64_t n) {
+    GIMBAL_TRY(ensure_staging());
+    const bool pinned = is_pinned_host(ids);
+    if (!pinned && !hstage[0]) {
+      for (int b = 0; b < kStages; ++b) GIMBAL_CUDA_TRY(cudaMallocHost(&hstage[b], stage_bytes));
+    }
+    const size_t row = (size_t)topo.n_layers * topo.top_k * id_bytes;
+    const int64_t per = (int64_t)(stage_bytes / row);
+    const char* src = static_cast<const char*>(ids);
+    int b = 0;
+    for (int64_t t0 = 0; t0 < n; t0 += per, b ^= 1) {
+      const int64_t cnt = std::min<int64_t>(per, n - t0);
+      const size_t bytes = (size_t)cnt * row;
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(copy_stream, ev_consumed[b], 0));
+      const void* from = src + (size_t)t0 * row;
+      if (!pinned) {
+        // the bounce buffer is free once its previous H2D completed
+        GIMBAL_CUDA_TRY(cudaEventSynchronize(ev_copied[b]));
+        std::memcpy(hstage[b], from, bytes);
+        from = hstage[b];
+      }
+      GIMBAL_CUDA_TRY(cudaMemcpyAsync(dstage[b], from, bytes, cudaMemcpyHostToDevice, copy_stream));
+      GIMBAL_CUDA_TRY(cudaEventRecord(ev_copied[b], copy_stream));
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_copied[b], 0));
+      GIMBAL_TRY(count_device(dstage[b], id_bytes, cnt));
+      GIMBAL_CUDA_TRY(cudaEventRecord(ev_consumed[b], stream));
+    }
+    return GIMBAL_OK;
+  }
+};
+
+namespace {
+
+int check_handle(gimbal_stats_t h) {
+  if (!h) return invalid("null gimbal_stats_t handle");
+  return GIMBAL_OK;
+}
+
+int copy_out(void* dst, const void* src, size_t bytes, int mem, cudaStream_t s) {
+  if (!dst || bytes == 0) return GIMBAL_OK;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes,
+                                  mem == GIMBAL_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                           : cudaMemcpyDeviceToHost,
+                                  s));
+  return GIMBAL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gimbal_abi_version(void) { return GIMBAL_ABI_VERSION; }
+const char* gimbal_last_error(void) { return last_error().c_str(); }
+
+int gimbal_topology_validate(const gimbal_topology* topo) {
+  if (!topo) return invalid("null topology");
+  return validate_topology(*topo);
+}
+
+int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t* out) {
+  if (!topo || !out) return invalid("gimbal_stats_create: null argument");
+  GIMBAL_TRY(validate_topology(*topo));
+  int ndev = 0;
+  GIMBAL_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return invalid("gimbal_stats_create: device out of range");
+  DeviceGuard g(device);
+  auto* h = new gimbal_stats_s();
+  h->topo = *topo;
+  h->device = device;
+  int optin = 0;
+  cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  h->plan = make_stats_plan(topo->n_layers, topo->n_experts, topo->top_k, h->sms, optin);
+  auto fail = [&](int st) {
+    gimbal_stats_destroy(h);
+    return st;
+  };
+  if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    set_error("gimbal_stats_create: stream creation failed");
+    return fail(GIMBAL_CUDA_ERROR);
+  }
+  const int64_t nA = (int64_t)topo->n_layers * topo->n_experts;
+  const int64_t nW = (int64_t)topo->n_experts * topo->n_experts;
+  const int64_t nE = std::max<int64_t>(h->nE(), 1);
+  if (cudaMalloc(&h->dE, nE * 8) != cudaSuccess || cudaMalloc(&h->dA, nA * 8) != cudaSuccess ||
+      cudaMalloc(&h->dW, nW * 8) != cudaSuccess || cudaMalloc(&h->dflags, 64) != cudaSuccess) {
+    set_error("gimbal_stats_create: device allocation failed");
+    return fail(GIMBAL_CUDA_ERROR);
+  }
+  *out = h;
+  int st = gimbal_stats_reset(h);
+  if (st != GIMBAL_OK) {
+    *out = nullptr;
+    return fail(st);
+  }
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_destroy(gimbal_stats_t h) {
+  if (!h) return GIMBAL_OK;
+  {
+    DeviceGuard g(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->copy_stream) cudaStreamSynchronize(h->copy_stream);
+    cudaFree(h->dE);
+    cudaFree(h->dA);
+    cudaFree(h->dW);
+    cudaFree(h->dflags);
+    for (int b = 0; b < gimbal_stats_s::kStages; ++b) {
+      if (h->dstage[b]) cudaFree(h->dstage[b]);
+      if (h->hstage[b]) cudaFreeHost(h->hstage[b]);
+      if (h->ev_copied[b]) cudaEventDestroy(h->ev_copied[b]);
+      if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
+    }
+    for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints}) b->release();
+    if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+  }
+  delete h;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_reset(gimbal_stats_t h) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  const int64_t nA = h->m();
+  const int64_t nW = (int64_t)h->topo.n_experts * h->topo.n_experts;
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dE, 0, std::max<int64_t>(h->nE(), 1) * 8, h->stream));
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dA, 0, nA * 8, h->stream));
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dW, 0, nW * 8, h->stream));
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 64, h->stream));
+  h->tokens = 0;
+  h->derived = true;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n_tokens, int mem) {
+  GIMBAL_TRY(check_handle(h));
+  if (id_bytes != 1 && id_bytes != 4) return invalid("add_token: id_bytes must be 1 or 4");
+  if (id_bytes == 1 && h->topo.n_experts > 256) return invalid("add_token: uint8 ids need n_experts <= 256");
+  if (n_tokens < 0) return invalid("add_token: negative token count");
+  if (n_tokens == 0) return GIMBAL_OK;
+  if (!ids) return invalid("add_token: null ids");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (mem == GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(h->count_device(ids, id_bytes, n_tokens));
+  } else {
+    GIMBAL_TRY(h->count_host(ids, id_bytes, n_tokens));
+  }
+  h->tokens += n_tokens;
+  h->derived = false;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_tokens(gimbal_stats_t h, int64_t* tokens) {
+  GIMBAL_TRY(check_handle(h));
+  if (!tokens) return invalid("null tokens");
+  *tokens = h->tokens;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_sync(gimbal_stats_t h) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  return h->check_flags();
+}
+
+int gimbal_stats_read(gimbal_stats_t h, uint64_t* A, uint64_t* E, uint64_t* W, int mem) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->derive());
+  const int64_t ne = h->topo.n_experts;
+  GIMBAL_TRY(copy_out(A, h->dA, h->m() * 8, mem, h->stream));
+  if (h->nE() > 0) GIMBAL_TRY(copy_out(E, h->dE, h->nE() * 8, mem, h->stream));
+  GIMBAL_TRY(copy_out(W, h->dW, ne * ne * 8, mem, h->stream));
+  return h->check_flags();
+}
+
+int gimbal_stats_flat(gimbal_stats_t h, double* flatA, double* flatW, int mem) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->derive());
+  const int L = h->topo.n_layers, ne = h->topo.n_experts;
+  const int64_t m = h->m();
+  const size_t bA = (size_t)L * m * 8, bW = (size_t)m * m * 8;
+  double* dA = nullptr;
+  double* dW = nullptr;
+  DevBuf tmpA, tmpW;
+  if (flatA) {
+    if (mem == GIMBAL_MEM_DEVICE) dA = flatA;
+    else {
+      GIMBAL_TRY(tmpA.ensure(bA));
+      dA = tmpA.as<double>();
+    }
+    GIMBAL_CUDA_TRY(cudaMemsetAsync(dA, 0, bA, h->stream));
+  }
+  if (flatW) {
+    if (mem == GIMBAL_MEM_DEVICE) dW = flatW;
+    else {
+      GIMBAL_TRY(tmpW.ensure(bW));
+      dW = tmpW.as<double>();
+    }
+    GIMBAL_CUDA_TRY(cudaMemsetAsync(dW, 0, bW, h->stream));
+  }
+  if (L > 1 || dA) GIMBAL_CUDA_TRY(launch_flat_forms(L, ne, h->dA, h->dE, dA, L > 1 ? dW : nullptr, h->stream));
+  if (mem != GIMBAL_MEM_DEVICE) {
+    if (flatA) GIMBAL_CUDA_TRY(cudaMemcpyAsync(flatA, dA, bA, cudaMemcpyDeviceToHost, h->stream));
+    if (flatW) GIMBAL_CUDA_TRY(cudaMemcpyAsync(flatW, dW, bW, cudaMemcpyDeviceToHost, h->stream));
+  }
+  int st = h->check_flags();
+  tmpA.release();
+  tmpW.release();
+  return st;
+}
+
+int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, void** stream) {
+  GIMBAL_TRY(check_handle(h));
+  if (E) *E = h->nE() > 0 ? reinterpret_cast<uint64_t*>(h->dE) : nullptr;
+  if (A) *A = reinterpret_cast<uint64_t*>(h->dA);
+  if (stream) *stream = h->stream;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
+  GIMBAL_TRY(check_handle(h));
+  if (global_tokens < 0) return invalid("mark_reduced: negative token count");
+  std::lock_guard<std::mutex> lk(h->mu);
+  h->tokens = global_tokens;
+  h->derived = h->topo.n_layers < 2;
+  return GIMBAL_OK;
+}
+
+int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, int cand_mem,
+                      double alpha, double beta, double* deviation, double* cut, double* objective,
+                      int64_t* argmin, int out_mem) {
+  GIMBAL_TRY(check_handle(h));
+  if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
+  if (C < 0) return invalid("eval_costs: negative candidate count");
+  if (C == 0) {
+    if (argmin) *argmin = -1;
+    return GIMBAL_OK;
+  }
+  if (!candidates || !deviation || !cut || !objective) return invalid("eval_costs: null argument");
+  if (h->topo.n_gpus > 255) return invalid("eval_costs: uint8 candidates need n_gpus <= 255");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->derive());
+  const int L = h->topo.n_layers, ne = h->topo.n_experts, gg = h->topo.n_gpus, k = h->topo.top_k;
+  const int64_t m = h->m();
+  const uint8_t* dc = candidates;
+  if (cand_mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(h->cand.ensure((size_t)C * m));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(h->cand.p, candidates, (size_t)C * m, cudaMemcpyHostToDevice, h->stream));
+    dc = h->cand.as<uint8_t>();
+  }
+  GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
+  double *dD = deviation, *dcut = cut, *dobj = objective;
+  long long* darg = nullptr;
+  GIMBAL_TRY(h->dout.ensure((size_t)C * 24 + 16));
+  if (out_mem != GIMBAL_MEM_DEVICE) {
+    dD = h->dout.as<double>();
+    dcut = dD + C;
+    dobj = dcut + C;
+  }
+  darg = reinterpret_cast<long long*>(h->dout.as<double>() + 3 * C);
+  GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
+                                    h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
+                                    h->dflags, h->sms, h->stream));
+  const unsigned long long total =
+      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
+  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
+                                     dobj, darg, h->dflags, h->stream));
+  uint32_t f = 0;
+  long long bad = 0, am = -1;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(&f, h->dflags, 4, cudaMemcpyDeviceToHost, h->stream));
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(&bad, h->same.as<unsigned long long>() + C, 8, cudaMemcpyDeviceToHost,
+                                  h->stream));
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(&am, darg, 8, cudaMemcpyDeviceToHost, h->stream));
+  if (out_mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(deviation, dD, C * 8, cudaMemcpyDeviceToHost, h->stream));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(cut, dcut, C * 8, cudaMemcpyDeviceToHost, h->stream));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(objective, dobj, C * 8, cudaMemcpyDeviceToHost, h->stream));
+  }
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (f & kFlagInfeasible) {
+    // clear the non-sticky flag, report like check_feasible (placement.cpp:30-50)
+    GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 4, h->stream));
+    uint32_t keep = f & ~(uint32_t)kFlagInfeasible;
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(h->dflags, &keep, 4, cudaMemcpyHostToDevice, h->stream));
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return invalid("placement: candidate " + std::to_string(bad) +
+                   " is infeasible (ids must be in [0, g) with exactly m/g experts per GPU)");
+  }
+  GIMBAL_TRY(flags_to_status(f));
+  if (argmin) *argmin = am;
+  return GIMBAL_OK;
+}
+
+int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity,
+                        int32_t anchor_gpu, int32_t* out, int32_t* n_out) {
+  GIMBAL_TRY(check_handle(h));
+  if (!out || !n_out) return invalid("build_affinity_set: null output");
+  if (anchor_gpu < 0 || anchor_gpu >= h->topo.n_gpus)
+    return invalid("build_affinity_set: anchor_gpu out of range");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  const int L = h->topo.n_layers, ne = h->topo.n_experts;
+  if (L < 2) {
+    *n_out = 0;
+    return h->check_flags();
+  }
+  const int64_t n = h->nE();
+  if (n >= (1ll << 24)) {
+    set_error("build_affinity_set: (L-1)*n_experts^2 must be < 2^24");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  const int64_t n_pad = next_pow2(n);
+  const int64_t m = h->m();
+  GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
+  GIMBAL_TRY(h->misc.ensure((size_t)((m + 31) / 32) * 4 + (size_t)m * 4 + 16));
+  uint32_t* bits = h->misc.as<uint32_t>();
+  int32_t* dout = reinterpret_cast<int32_t*>(bits + (m + 31) / 32);
+  int32_t* dn = dout + m;
+  GIMBAL_CUDA_TRY(launch_affinity_keys(L, ne, h->dE, threshold, h->keys.as<unsigned long long>(), n_pad,
+                                       h->dflags, h->stream));
+  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+  GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, h->keys.as<unsigned long long>(), n, top_e, capacity, bits,
+                                         dout, dn, h->stream));
+  int32_t cnt = 0;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (cnt > 0) {
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(out, dout, (size_t)cnt * 4, cudaMemcpyDeviceToHost, h->stream));
+  }
+  *n_out = cnt;
+  return h->check_flags();
+}
+
+// Reference validation order and messages (placement.cpp:243-252, 272-279).
+static int validate_greedy(int64_t m, int g, const int32_t* M, int32_t nM, int32_t anchor,
+                           std::vector<uint32_t>& bits) {
+  if (g < 1 || m < 1 || m % g != 0) return invalid("greedy_place: experts must be divisible by g");
+  const int64_t cap = m / g;
+  if (anchor < 0 || anchor >= g) return invalid("greedy_place: anchor_gpu out of range");
+  if (nM > cap) return invalid("greedy_place: affinity set exceeds anchor capacity");
+  bits.assign((size_t)((m + 31) / 32), 0u);
+  for (int i = 0; i < nM; ++i) {
+    const int64_t e = M[i];
+    if (e < 0 || e >= m) return invalid("greedy_place: affinity id out of range");
+    if ((bits[e >> 5] >> (e & 31)) & 1u) return invalid("greedy_place: duplicate affinity id");
+    bits[e >> 5] |= 1u << (e & 31);
+  }
+  return GIMBAL_OK;
+}
+
+int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t anchor, int32_t* out,
+                        int out_mem, uint8_t* out_u8) {
+  GIMBAL_TRY(check_handle(h));
+  if (!out && !out_u8) return invalid("greedy_place: null output");
+  if (nM < 0 || (nM > 0 && !M)) return invalid("greedy_place: bad affinity set");
+  const int L = h->topo.n_layers, ne = h->topo.n_experts, g = h->topo.n_gpus;
+  const int64_t m = h->m();
+  std::vector<uint32_t> bits;
+  GIMBAL_TRY(validate_greedy(m, g, M, nM, anchor, bits));
+  if (m >= (1ll << 24)) {
+    set_error("greedy_place: m must be < 2^24");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  GIMBAL_TRY(h->derive());
+  const int64_t n_pad = next_pow2(m);
+  GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
+  const size_t words = bits.size();
+  GIMBAL_TRY(h->ints.ensure(words * 4 + (size_t)std::max(nM, 1) * 4 + (size_t)m * 4 + 64));
+  uint32_t* dbits = h->ints.as<uint32_t>();
+  int32_t* dM = reinterpret_cast<int32_t*>(dbits + words);
+  int32_t* dres = dM + std::max(nM, 1);
+  if (out && out_mem == GIMBAL_MEM_DEVICE) dres = out;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(dbits, bits.data(), words * 4, cudaMemcpyHostToDevice, h->stream));
+  if (nM > 0) GIMBAL_CUDA_TRY(cudaMemcpyAsync(dM, M, (size_t)nM * 4, cudaMemcpyHostToDevice, h->stream));
+  GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, dbits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
+                                     h->stream));
+  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+  GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, dM, nM, anchor, h->keys.as<unsigned long long>(),
+                                     m, dres, out_u8, h->stream));
+  if (out && out_mem != GIMBAL_MEM_DEVICE)
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(out, dres, (size_t)m * 4, cudaMemcpyDeviceToHost, h->stream));
+  return h->check_flags();
+}
+
+int gimbal_static_placement(const gimbal_topology* topo, int32_t* out) {
+  if (!topo || !out) return invalid("static_placement: null argument");
+  GIMBAL_TRY(validate_topology(*topo));
+  const int per = topo->n_experts / topo->n_gpus;
+  for (int l = 0; l < topo->n_layers; ++l)
+    for (int e = 0; e < topo->n_experts; ++e) out[l * topo->n_experts + e] = e / per;
+  return GIMBAL_OK;
+}
+
+int gimbal_comm_cost(const gimbal_topology* topo, const void* ids, int id_bytes, int64_t T, int mem,
+                     const int32_t* assign, int32_t n_assign, int device, int64_t* out) {
+  if (!topo || !out) return invalid("comm_cost: null argument");
+  GIMBAL_TRY(validate_topology(*topo));
+  const int L = topo->n_layers, ne = topo->n_experts, k = topo->top_k;
+  const int64_t m = (int64_t)L * ne;
+  if (n_assign != m) return invalid("comm_cost: assignment size mismatch");
+  for (int i = 0; i < n_assign; ++i)
+    if (assign[i] < 0) return invalid("comm_cost: unplaced expert");
+  if (id_bytes != 1 && id_bytes != 4) return invalid("comm_cost: id_bytes must be 1 or 4");
+  if (k > 32) {
+    set_error("comm_cost: top_k > 32");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  // GPU ids only matter through equality: compact them to [0, 256)
+  std::vector<int32_t> compact(assign, assign + n_assign);
+  {
+    std::vector<int32_t> vals(compact);
+    std::sort(vals.begin(), vals.end());
+    vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+    if (vals.size() > 256) {
+      set_error("comm_cost: more than 256 distinct GPU ids");
+      return GIMBAL_NOT_SUPPORTED;
+    }
+    for (auto& v : compact) v = (int32_t)(std::lower_bound(vals.begin(), vals.end(), v) - vals.begin());
+  }
+  *out = 0;
+  if (T <= 0 || L < 2) return GIMBAL_OK;
+  DeviceGuard dg(device);
+  cudaStream_t s;
+  GIMBAL_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  DevBuf dids, dassign, dres;
+  int st = GIMBAL_OK;
+  const void* src = ids;
+  const size_t bytes = (size_t)T * L * k * id_bytes;
+  if (mem != GIMBAL_MEM_DEVICE) {
+    if ((st = dids.ensure(bytes)) == GIMBAL_OK) {
+      if (cudaMemcpyAsync(dids.p, ids, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) st = GIMBAL_CUDA_ERROR;
+      src = dids.p;
+    }
+  }
+  if (st == GIMBAL_OK) st = dassign.ensure((size_t)m * 4);
+  if (st == GIMBAL_OK) st = dres.ensure(16);
+  unsigned long long crossings = 0;
+  uint32_t flags = 0;
+  if (st == GIMBAL_OK) {
+    cudaMemcpyAsync(dassign.p, compact.data(), (size_t)m * 4, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(dres.p, 0, 16, s);
+    if (launch_comm_cost(L, ne, k, src, id_bytes, T, dassign.as<int32_t>(), dres.as<unsigned long long>(),
+                         reinterpret_cast<uint32_t*>(dres.as<unsigned long long>() + 1), s) != cudaSuccess) {
+      set_error("comm_cost: kernel launch failed");
+      st = GIMBAL_CUDA_ERROR;
+    } else {
+      cudaMemcpyAsync(&crossings, dres.p, 8, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(&flags, dres.as<unsigned long long>() + 1, 4, cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) {
+        set_error("comm_cost: execution failed");
+        st = GIMBAL_CUDA_ERROR;
+      }
+    }
+  }
+  dids.release();
+  dassign.release();
+  dres.release();
+  cudaStreamDestroy(s);
+  if (st != GIMBAL_OK) return st;
+  GIMBAL_TRY(flags_to_status(flags));
+  *out = (int64_t)crossings;
+  return GIMBAL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// Internal helpers shared by the sm_100a translation units of libgimbal_gpu.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "gimbal_gpu.h"
+
+namespace gimbal_gpu {
+
+// Thread-local last error (gimbal_last_error()).
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+struct Status {
+  int code = GIMBAL_OK;
+  std::string msg;
+};
+
+// Error flags raised inside kernels (sticky per handle).
+enum KernelFlag : uint32_t {
+  kFlagIdOutOfRange = 1u,
+  kFlagInfeasible = 2u,
+  kFlagOverflow = 4u,
+};
+
+#define GIMBAL_CUDA_TRY(expr)                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      ::gimbal_gpu::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_));     \
+      return GIMBAL_CUDA_ERROR;                                                        \
+    }                                                                                  \
+  } while (0)
+
+#define GIMBAL_TRY(expr)            \
+  do {                              \
+    int s_ = (expr);                \
+    if (s_ != GIMBAL_OK) return s_; \
+  } while (0)
+
+inline int invalid(const std::string& msg) {
+  set_error(msg);
+  return GIMBAL_INVALID_ARGUMENT;
+}
+
+// MoeTopology::validate (moe.cpp:12-24) with the reference's messages.
+int validate_topology(const gimbal_topology& t);
+
+// Scoped device guard.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ---- kernel launchers (stream-ordered, return cudaError_t of the launch) ----
+
+// Statistics plan: which layer pairs / row slices one CTA privatises in shared memory.
+struct StatsPlan {
+  int L = 0, ne = 0, k = 0;
+  int pairs_per_group = 1;   // consecutive layer pairs per CTA work unit
+  int rows_per_part = 0;     // rows j of E per CTA work unit
+  int n_groups = 0, n_parts = 0;
+  int smem_words = 0;        // u32 counters per CTA
+  int threads = 1024;
+  int ctas_per_sm = 1;
+  int sms = 148;
+};
+StatsPlan make_stats_plan(int L, int ne, int k, int sms, int max_smem_optin);
+
+cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
+                               unsigned long long* E, uint32_t* flags, cudaStream_t s);
+cudaError_t launch_count_activation(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,
+                                    unsigned long long* A, uint32_t* flags, cudaStream_t s);
+cudaError_t launch_derive_activation(int L, int ne, int k, const unsigned long long* E,
+                                     unsigned long long* A, cudaStream_t s);
+cudaError_t launch_derive_w(int L, int ne, const unsigned long long* E, unsigned long long* W,
+                            cudaStream_t s);
+cudaError_t launch_flat_forms(int L, int ne, const unsigned long long* A,
+                              const unsigned long long* E, double* flatA, double* flatW,
+                              cudaStream_t s);
+
+// placement
+cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
+                              const unsigned long long* E, const uint8_t* cands, int64_t C,
+                              double alpha, double beta, unsigned long long* scratch_same,
+                              double* D, double* cut, double* obj, long long* argmin,
+                              uint32_t* flags, int sms, cudaStream_t s);
+size_t eval_scratch_bytes(int64_t C);
+
+cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
+                               const unsigned long long* same, const double* D, double* cut,
+                               double* obj, long long* argmin, uint32_t* flags, cudaStream_t s);
+
+cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E, double threshold,
+                                 unsigned long long* keys, int64_t n_pad, uint32_t* flags,
+                                 cudaStream_t s);
+cudaError_t launch_affinity_select(int L, int ne, const unsigned long long* sorted_keys,
+                                   int64_t n_keys, int32_t top_e, int32_t capacity,
+                                   uint32_t* member_bits, int32_t* out, int32_t* n_out,
+                                   cudaStream_t s);
+
+cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uint32_t* anchored,
+                               unsigned long long* keys, int64_t n_pad, uint32_t* flags,
+                               cudaStream_t s);
+cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M,
+                               int32_t nM, int32_t anchor, const unsigned long long* keys,
+                               int64_t n_keys, int32_t* out, uint8_t* out_u8, cudaStream_t s);
+
+// Sort uint64 keys descending in place (bitonic; n must be a power of two).
+cudaError_t sort_u64_desc(unsigned long long* keys, int64_t n, cudaStream_t s);
+
+cudaError_t launch_comm_cost(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,
+                             const int32_t* assign, unsigned long long* out, uint32_t* flags,
+                             cudaStream_t s);
+
+cudaError_t launch_generate_trace(int L, int ne, int k, const uint32_t* cdf, uint64_t thr_base,
+                                  uint64_t thr_unif, uint64_t seed, int64_t t0, int64_t T,
+                                  uint8_t* out, cudaStream_t s);
+
+inline int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+}  // namespace gimbal_gpu

@@ -1,0 +1,526 @@
+// Placement scoring, strong-pair (hotspot) selection and greedy re-placement on sm_100a.
+//
+// Reference semantics (/root/reference/proj/src/placement.cpp):
+//   eval_cost          :58-85   loads(l,p) = sum_e A(l,e)[P(e)=p]; ideal_l = rowsum_l / g;
+//                               D = max |loads - ideal|; cut = sum over pairs on different GPUs;
+//                               objective = alpha*D + beta*cut
+//   check_feasible     :30-50   ids in [0,g), every GPU exactly m/g experts (global cap)
+//   build_affinity_set :186-238 pairs (w >= threshold && w > 0) sorted (w desc, a asc, b asc),
+//                               top_e, endpoint union trimmed to capacity
+//   greedy_place       :240-299 anchor M; order by (-total, id); home = first argmax row;
+//                               least-loaded GPU with headroom, strict <
+//
+// cut is evaluated on E directly (W = flat_pair_weights() is never materialised): for candidate
+// P, same = sum_l sum_{j,k} E_l(j,k) [P(l,j) == P(l+1,k)] and cut = total - same with
+// total = tokens * (L-1) * top_k^2 (every token adds exactly top_k^2 pairings per layer pair).
+// All sums are integers; converting the u64 result to double reproduces the reference's fp64
+// accumulation exactly while the value stays below 2^53 (checked, GIMBAL_OVERFLOW otherwise).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+
+constexpr int kEvalThreads = 256;
+constexpr int kEvalCellsPerThread = 32;             // E cells held in registers per thread
+constexpr int kEvalCands = 32;                      // candidates per CTA
+constexpr int kEvalCellsPerCta = kEvalThreads * kEvalCellsPerThread;
+
+// ---- cut: same[c] += sum over this CTA's E cells of E(j,k) [P(j) == P(k')] ----
+// The CTA owns kEvalCellsPerCta consecutive cells of the flattened E (row r = flat expert
+// f(l,j) of layer l < L-1, column k = expert of layer l+1), keeps them in registers and streams
+// kEvalCands candidates at a time through shared memory.
+__global__ void __launch_bounds__(kEvalThreads)
+    eval_same_kernel(int L, int ne, const unsigned long long* __restrict__ E,
+                     const uint8_t* __restrict__ cands, int64_t C, int64_t m,
+                     unsigned long long* __restrict__ same) {
+  extern __shared__ uint8_t sm[];
+  const int64_t nE = (int64_t)(L - 1) * ne * ne;
+  const int64_t cell0 = (int64_t)blockIdx.x * kEvalCellsPerCta;
+  const int64_t row_lo = cell0 / ne;
+  const int64_t cell_hi = min(nE, cell0 + kEvalCellsPerCta);
+  const int64_t row_hi = (cell_hi - 1) / ne;                 // inclusive
+  const int64_t span_lo = row_lo;                            // first flat id needed
+  const int64_t span_hi = min(m, (row_hi / ne + 2) * ne);    // end of layer (l_hi + 1)
+  const int span = (int)(span_hi - span_lo);
+  unsigned long long e[kEvalCellsPerThread];
+  int rowo[kEvalCellsPerThread];  // offset of P(row) in the staged span
+  int colo[kEvalCellsPerThread];  // offset of P(col) in the staged span
+#pragma unroll
+  for (int i = 0; i < kEvalCellsPerThread; ++i) {
+    const int64_t cell = cell0 + threadIdx.x + (int64_t)i * kEvalThreads;
+    if (cell < cell_hi) {
+      e[i] = E[cell];
+      const int64_t r = cell / ne;
+      const int64_t k = cell - r * ne;
+      const int64_t l = r / ne;
+      rowo[i] = (int)(r - span_lo);
+      colo[i] = (int)((l + 1) * ne + k - span_lo);
+    } else {
+      e[i] = 0;
+      rowo[i] = 0;
+      colo[i] = 0;
+    }
+  }
+  __shared__ unsigned long long red[kEvalThreads / 32][kEvalCands];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t c0 = 0; c0 < C; c0 += kEvalCands) {
+    const int nc = (int)min((int64_t)kEvalCands, C - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nc * span; idx += blockDim.x) {
+      const int c = idx / span, o = idx - c * span;
+      sm[c * span + o] = cands[(c0 + c) * m + span_lo + o];
+    }
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const uint8_t* P = sm + c * span;
+      unsigned long long s = 0;
+#pragma unroll
+      for (int i = 0; i < kEvalCellsPerThread; ++i) s += (P[rowo[i]] == P[colo[i]]) ? e[i] : 0ull;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) red[warp][c] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      unsigned long long s = 0;
+#pragma unroll
+      for (int w = 0; w < kEvalThreads / 32; ++w) s += red[w][threadIdx.x];
+      if (s) atomicAdd(&same[c0 + threadIdx.x], s);
+    }
+  }
+}
+
+// ---- deviation + feasibility: one CTA per candidate, one warp per layer at a time ----
+__global__ void __launch_bounds__(256)
+    eval_dev_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
+                    const uint8_t* __restrict__ cands, int64_t m, double* __restrict__ D,
+                    uint32_t* __restrict__ flags, long long* __restrict__ bad_index) {
+  extern __shared__ unsigned long long sh[];  // [warps][g] loads, then [g] counts (u32)
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* loads = sh + warp * g;
+  uint32_t* counts = reinterpret_cast<uint32_t*>(sh + warps * g);
+  const int64_t c = blockIdx.x;
+  const uint8_t* P = cands + c * m;
+  for (int p = threadIdx.x; p < g; p += blockDim.x) counts[p] = 0;
+  __shared__ double dmax[8];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  double dev = 0.0;
+  for (int l = warp; l < L; l += warps) {
+    for (int p = lane; p < g; p += 32) loads[p] = 0ull;
+    __syncwarp();
+    unsigned long long rowsum = 0;
+    for (int e = lane; e < ne; e += 32) {
+      const unsigned long long a = A[(int64_t)l * ne + e];
+      const int p = P[(int64_t)l * ne + e];
+      rowsum += a;
+      if (p >= g) {
+        bad = 1;
+        continue;
+      }
+      atomicAdd(&loads[p], a);
+      atomicAdd(&counts[p], 1u);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rowsum += __shfl_xor_sync(0xffffffffu, rowsum, o);
+    __syncwarp();
+    // ideal_l = A.row(l).sum() / g (placement.cpp:68); integer rowsum < 2^53 is exact in fp64
+    const double ideal = __ddiv_rn((double)rowsum, (double)g);
+    for (int p = lane; p < g; p += 32) {
+      const double d = fabs(__dsub_rn((double)loads[p], ideal));
+      dev = fmax(dev, d);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if (lane == 0) dmax[warp] = dev;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = 0.0;
+    for (int w = 0; w < warps; ++w) d = fmax(d, dmax[w]);
+    D[c] = d;
+    const uint32_t cap = (uint32_t)(m / g);
+    int infeasible = bad;
+    for (int p = 0; p < g; ++p)
+      if (counts[p] != cap) infeasible = 1;
+    if (infeasible) {
+      atomicOr(flags, (uint32_t)kFlagInfeasible);
+      atomicMin(bad_index, (long long)c);
+    }
+  }
+}
+
+// cut/objective per candidate, then the argmin (lowest index among minima) in one CTA.
+__global__ void eval_finish_kernel(int64_t C, unsigned long long total, double alpha, double beta,
+                                   const unsigned long long* __restrict__ same,
+                                   const double* __restrict__ D, double* __restrict__ cut,
+                                   double* __restrict__ obj, long long* __restrict__ argmin,
+                                   uint32_t* __restrict__ flags) {
+  __shared__ double bv[1024];
+  __shared__ long long bi[1024];
+  double best = 0.0;
+  long long besti = -1;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const unsigned long long cu = total - same[c];
+    if (cu > (1ull << 53)) atomicOr(flags, (uint32_t)kFlagOverflow);
+    const double cd = (double)cu;
+    // objective = alpha * D + beta * cut (placement.cpp:83): two roundings, no FMA contraction
+    const double o = __dadd_rn(__dmul_rn(alpha, D[c]), __dmul_rn(beta, cd));
+    cut[c] = cd;
+    obj[c] = o;
+    if (besti < 0 || o < best) {
+      best = o;
+      besti = c;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = besti;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double v2 = bv[threadIdx.x + s];
+      const long long i2 = bi[threadIdx.x + s];
+      const long long i1 = bi[threadIdx.x];
+      if (i2 >= 0 && (i1 < 0 || v2 < bv[threadIdx.x] || (v2 == bv[threadIdx.x] && i2 < i1))) {
+        bv[threadIdx.x] = v2;
+        bi[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && argmin) *argmin = bi[0];
+}
+
+// ---- build_affinity_set: composite sort keys over E ----
+// key = (w << 24) | (2^24 - 1 - idx) for qualifying cells, else 0; sorting keys in descending
+// order yields (w desc, idx asc), and idx = (l*ne + j)*ne + k orders exactly like the
+// reference's (a asc, b asc) tie-break (a = l*ne + j, b = (l+1)*ne + k).
+__global__ void affinity_keys_kernel(int L, int ne, const unsigned long long* __restrict__ E,
+                                     double threshold, unsigned long long* __restrict__ keys,
+                                     int64_t n, int64_t n_pad, uint32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0ull;
+    if (i < n) {
+      const unsigned long long w = E[i];
+      const double wd = (double)w;
+      if (wd >= threshold && wd > 0.0) {
+        if (w >= (1ull << 40)) atomicOr(flags, (uint32_t)kFlagOverflow);
+        key = (w << 24) | (unsigned long long)(0xffffffll - i);
+      }
+    }
+    keys[i] = key;
+  }
+}
+
+// Sequential endpoint union over the sorted pairs (placement.cpp:221-237): the result is the
+// union of the longest prefix (<= kept pairs) whose union fits `capacity`.
+__global__ void affinity_select_kernel(int L, int ne, const unsigned long long* __restrict__ keys,
+                                       int64_t n_keys, int32_t top_e, int32_t capacity,
+                                       uint32_t* __restrict__ bits, int32_t* __restrict__ out,
+                                       int32_t* __restrict__ n_out) {
+  const int64_t m = (int64_t)L * ne;
+  const int64_t words = (m + 31) / 32;
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) bits[w] = 0u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t members = 0;
+    const int64_t nn = (int64_t)ne * ne;
+    for (int64_t i = 0; i < n_keys; ++i) {
+      if (top_e >= 0 && i >= top_e) break;
+      const unsigned long long key = keys[i];
+      if (key == 0ull) break;
+      const int64_t idx = 0xffffffll - (int64_t)(key & 0xffffffull);
+      const int64_t a = idx / ne;
+      const int64_t b = (idx / nn + 1) * ne + (idx % ne);
+      const bool na = !((bits[a >> 5] >> (a & 31)) & 1u);
+      const bool nb = !((bits[b >> 5] >> (b & 31)) & 1u);
+      const int64_t grown = members + (na ? 1 : 0) + (nb ? 1 : 0);
+      if (grown > capacity) break;
+      if (na) bits[a >> 5] |= 1u << (a & 31);
+      if (nb) bits[b >> 5] |= 1u << (b & 31);
+      members = grown;
+    }
+    int32_t n = 0;
+    for (int64_t w = 0; w < words; ++w) {
+      uint32_t v = bits[w];
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        out[n++] = (int32_t)(w * 32 + bit);
+        v &= v - 1;
+      }
+    }
+    *n_out = n;
+  }
+}
+
+// ---- greedy_place on the compact flat activation ----
+// order keys = (A(e) << 24) | (2^24 - 1 - e) for unanchored experts (descending = (-total, id)),
+// 0 for anchored ones and padding.
+__global__ void greedy_keys_kernel(int64_t m, const unsigned long long* __restrict__ A,
+                                   const uint32_t* __restrict__ anchored,
+                                   unsigned long long* __restrict__ keys, int64_t n_pad,
+                                   uint32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pad;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long key = 0ull;
+    if (i < m && !((anchored[i >> 5] >> (i & 31)) & 1u)) {
+      const unsigned long long a = A[i];
+      if (a >= (1ull << 40)) atomicOr(flags, (uint32_t)kFlagOverflow);
+      key = (a << 24) | (unsigned long long)(0xffffffll - i);
+    }
+    keys[i] = key;
+  }
+}
+
+// One warp walks the sorted order; lanes hold GPUs p (g <= 32 per pass).
+__global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
+                                   const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
+                                   const unsigned long long* __restrict__ keys, int64_t n_keys,
+                                   int32_t* __restrict__ out, uint8_t* __restrict__ out_u8) {
+  extern __shared__ unsigned long long load[];  // [L][g]
+  int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
+  const int lane = threadIdx.x;
+  const int64_t m = (int64_t)L * ne;
+  const int cap = (int)(m / g);
+  for (int64_t i = lane; i < (int64_t)L * g; i += 32) load[i] = 0ull;
+  for (int p = lane; p < g; p += 32) counts[p] = 0;
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 0; i < nM; ++i) {  // placement.cpp:272-279
+      const int e = M[i];
+      out[e] = anchor;
+      if (out_u8) out_u8[e] = (uint8_t)anchor;
+      load[(int64_t)(e / ne) * g + anchor] += A[e];
+      counts[anchor] += 1;
+    }
+  }
+  __syncwarp();
+  for (int64_t i = 0; i < n_keys; ++i) {
+    const unsigned long long key = keys[i];
+    if (key == 0ull) break;
+    const int64_t e = 0xffffffll - (int64_t)(key & 0xffffffull);
+    const unsigned long long a = key >> 24;
+    // home = first argmax row of the flat column: its layer if A > 0, else row 0
+    const int64_t row = a > 0 ? e / ne : 0;
+    int best_p = -1;
+    unsigned long long best_v = 0ull;
+    for (int p0 = 0; p0 < g; p0 += 32) {
+      const int p = p0 + lane;
+      int cand = -1;
+      unsigned long long v = 0ull;
+      if (p < g && counts[p] < cap) {
+        cand = p;
+        v = load[row * g + p];
+      }
+      // warp argmin: smaller load, then lower p (== first strict-< winner in p order)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int c2 = __shfl_xor_sync(0xffffffffu, cand, o);
+        const unsigned long long v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        if (c2 >= 0 && (cand < 0 || v2 < v || (v2 == v && c2 < cand))) {
+          cand = c2;
+          v = v2;
+        }
+      }
+      if (cand >= 0 && (best_p < 0 || v < best_v)) {
+        best_p = cand;
+        best_v = v;
+      }
+    }
+    if (lane == 0) {
+      out[e] = best_p;
+      if (out_u8) out_u8[e] = (uint8_t)best_p;
+      load[(e / ne) * g + best_p] += a;
+      counts[best_p] += 1;
+    }
+    __syncwarp();
+  }
+}
+
+// ---- bitonic sort (descending) of u64 keys, n a power of two ----
+constexpr int kSortLocal = 2048;  // keys per CTA in the shared-memory stages
+
+__global__ void bitonic_local_kernel(unsigned long long* keys, int64_t n, int64_t k_start,
+                                     int64_t k_end, bool full) {
+  // full: run the network for k in [2, min(kSortLocal, n)] entirely in shared memory.
+  // otherwise: for the current k (k_start), run the j < kSortLocal steps.
+  __shared__ unsigned long long s[kSortLocal];
+  const int64_t base = (int64_t)blockIdx.x * kSortLocal;
+  for (int i = threadIdx.x; i < kSortLocal; i += blockDim.x) s[i] = keys[base + i];
+  __syncthreads();
+  const int64_t kmax = full ? min((int64_t)kSortLocal, n) : k_start;
+  const int64_t kmin = full ? 2 : k_start;
+  for (int64_t k = kmin; k <= kmax; k <<= 1) {
+    for (int64_t j = (full ? k : kSortLocal) >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < kSortLocal / 2; t += blockDim.x) {
+        const int64_t lo_local = 2 * j * (t / j) + (t % j);
+        const int64_t i = base + lo_local;
+        const int64_t pi = i + j;
+        const bool desc = ((i & k) == 0);
+        const unsigned long long a = s[lo_local], b = s[lo_local + j];
+        if (desc ? (a < b) : (a > b)) {
+          s[lo_local] = b;
+          s[lo_local + j] = a;
+        }
+        (void)pi;
+      }
+      __syncthreads();
+    }
+  }
+  (void)k_end;
+  for (int i = threadIdx.x; i < kSortLocal; i += blockDim.x) keys[base + i] = s[i];
+}
+
+__global__ void bitonic_global_kernel(unsigned long long* keys, int64_t n, int64_t k, int64_t j) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n / 2;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = 2 * j * (t / j) + (t % j);
+    const bool desc = ((i & k) == 0);
+    const unsigned long long a = keys[i], b = keys[i + j];
+    if (desc ? (a < b) : (a > b)) {
+      keys[i] = b;
+      keys[i + j] = a;
+    }
+  }
+}
+
+// n < kSortLocal: one CTA sorts everything in shared memory.
+__global__ void bitonic_small_kernel(unsigned long long* keys, int n) {
+  __shared__ unsigned long long s[kSortLocal];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = keys[i];
+  __syncthreads();
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
+        const int i = 2 * j * (t / j) + (t % j);
+        const bool desc = ((i & k) == 0);
+        const unsigned long long a = s[i], b = s[i + j];
+        if (desc ? (a < b) : (a > b)) {
+          s[i] = b;
+          s[i + j] = a;
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = s[i];
+}
+
+}  // namespace
+
+cudaError_t sort_u64_desc(unsigned long long* keys, int64_t n, cudaStream_t s) {
+  if (n <= 1) return cudaSuccess;
+  if (n <= kSortLocal) {
+    bitonic_small_kernel<<<1, 1024, 0, s>>>(keys, (int)n);
+    return cudaGetLastError();
+  }
+  const int64_t blocks = n / kSortLocal;
+  bitonic_local_kernel<<<(unsigned)blocks, 1024, 0, s>>>(keys, n, 0, 0, true);
+  for (int64_t k = 2 * kSortLocal; k <= n; k <<= 1) {
+    for (int64_t j = k >> 1; j >= kSortLocal; j >>= 1) {
+      const int grid = (int)std::min<int64_t>(4 * 1184, (n / 2 + 255) / 256);
+      bitonic_global_kernel<<<grid, 256, 0, s>>>(keys, n, k, j);
+    }
+    bitonic_local_kernel<<<(unsigned)blocks, 1024, 0, s>>>(keys, n, k, k, false);
+  }
+  return cudaGetLastError();
+}
+
+size_t eval_scratch_bytes(int64_t C) {
+  return (size_t)C * sizeof(unsigned long long) + sizeof(long long) * 2;
+}
+
+cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
+                              const unsigned long long* E, const uint8_t* cands, int64_t C,
+                              double alpha, double beta, unsigned long long* scratch_same,
+                              double* D, double* cut, double* obj, long long* argmin,
+                              uint32_t* flags, int sms, cudaStream_t s) {
+  (void)sms;
+  if (C <= 0) return cudaSuccess;
+  const int64_t m = (int64_t)L * ne;
+  cudaError_t e = cudaMemsetAsync(scratch_same, 0, (size_t)C * sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  long long* bad_index = reinterpret_cast<long long*>(scratch_same + C);
+  // bad_index starts at LLONG_MAX
+  const long long init = 0x7fffffffffffffffll;
+  e = cudaMemcpyAsync(bad_index, &init, sizeof(init), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  if (L > 1) {
+    const int64_t nE = (int64_t)(L - 1) * ne * ne;
+    const int64_t ctas = (nE + kEvalCellsPerCta - 1) / kEvalCellsPerCta;
+    // staged span per candidate: rows of this CTA plus the next layer
+    const int64_t max_span = std::min<int64_t>(m, (int64_t)kEvalCellsPerCta / ne + 3 * ne);
+    const size_t smem = (size_t)kEvalCands * (size_t)max_span;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(eval_same_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    eval_same_kernel<<<(unsigned)ctas, kEvalThreads, smem, s>>>(L, ne, E, cands, C, m, scratch_same);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const int threads = 256;
+    const size_t smem = (size_t)(threads / 32) * g * 8 + (size_t)g * 4 + 8;
+    e = cudaFuncSetAttribute(eval_dev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    eval_dev_kernel<<<(unsigned)C, threads, smem, s>>>(L, ne, g, A, cands, m, D, flags, bad_index);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
+                               const unsigned long long* same, const double* D, double* cut,
+                               double* obj, long long* argmin, uint32_t* flags, cudaStream_t s) {
+  eval_finish_kernel<<<1, 1024, 0, s>>>(C, total, alpha, beta, same, D, cut, obj, argmin, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E,
+                                       double threshold, unsigned long long* keys, int64_t n_pad,
+                                       uint32_t* flags, cudaStream_t s) {
+  const int64_t n = (int64_t)(L - 1) * ne * ne;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 1184, (n_pad + 255) / 256));
+  affinity_keys_kernel<<<grid, 256, 0, s>>>(L, ne, E, threshold, keys, n, n_pad, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_affinity_select(int L, int ne, const unsigned long long* sorted_keys,
+                                   int64_t n_keys, int32_t top_e, int32_t capacity,
+                                   uint32_t* member_bits, int32_t* out, int32_t* n_out,
+                                   cudaStream_t s) {
+  affinity_select_kernel<<<1, 256, 0, s>>>(L, ne, sorted_keys, n_keys, top_e, capacity,
+                                           member_bits, out, n_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uint32_t* anchored,
+                               unsigned long long* keys, int64_t n_pad, uint32_t* flags,
+                               cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 1184, (n_pad + 255) / 256));
+  greedy_keys_kernel<<<grid, 256, 0, s>>>(m, A, anchored, keys, n_pad, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M,
+                               int32_t nM, int32_t anchor, const unsigned long long* keys,
+                               int64_t n_keys, int32_t* out, uint8_t* out_u8, cudaStream_t s) {
+  const size_t smem = (size_t)L * g * 8 + (size_t)g * 4;
+  cudaError_t e = cudaFuncSetAttribute(greedy_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  greedy_walk_kernel<<<1, 32, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
+  return cudaGetLastError();
+}
+
+}  // namespace gimbal_gpu

@@ -1,0 +1,148 @@
+"""The north-star pass: trace -> A/E/W -> strong-pair set M -> greedy -> C-candidate scoring ->
+argmin, on one B200 or sharded over ranks.
+
+Single GPU (``HotPath.run``): every stage is a kernel on the stats handle's stream; the only host
+round trips are the strong-pair set (<= 2*top_e ids, validated on the host like the reference)
+and the argmin / error flags.
+
+Multi-GPU (``HotPath.run_distributed``): trace tokens shard into contiguous ranges per rank (A/E
+are sums over tokens); partial u64 E is all-reduced in place (``torch.distributed``, NCCL over
+NVLink; int64 SUM is bit-identical to u64 addition), M and greedy are recomputed identically on
+every rank, candidates split into contiguous slices per rank and the per-candidate objectives
+are all-gathered for a global argmin with the lowest index winning ties.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .moe import MoeTopology, RoutingStats
+from .placement import AffinitySet, build_affinity_set, eval_costs, greedy_place
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Contiguous [lo, hi) slice of n items for rank (the same split the oracle uses)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def merge_argmin(objectives: np.ndarray) -> int:
+    """Lowest index among the minimal objectives (placement argmin tie rule)."""
+    if objectives.size == 0:
+        return -1
+    return int(np.flatnonzero(objectives == objectives.min())[0])
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device pointer (no copy)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<i8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def allreduce_counts(stats: RoutingStats, group=None) -> None:
+    """In-place SUM all-reduce of the handle's counted buffer over the process group."""
+    import torch
+    import torch.distributed as dist
+
+    topo = stats.topo
+    e_ptr, a_ptr, _ = stats.device_buffers()
+    if topo.n_layers > 1:
+        n, ptr = (topo.n_layers - 1) * topo.n_experts * topo.n_experts, e_ptr
+    else:
+        n, ptr = topo.n_layers * topo.n_experts, a_ptr
+    stats.sync()
+    dev = torch.device("cuda", stats.device)
+    view = torch.as_tensor(_CudaArray(ptr, n), device=dev)
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(view, op=dist.ReduceOp.SUM, group=group)
+        torch.cuda.current_stream(dev).synchronize()
+    else:
+        host = view.cpu()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+        view.copy_(host)
+        torch.cuda.synchronize(dev)
+    tok = torch.tensor([stats.tokens()], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        tok = tok.to(dev)
+    dist.all_reduce(tok, op=dist.ReduceOp.SUM, group=group)
+    stats.mark_reduced(int(tok.item()))
+
+
+@dataclass
+class HotPathResult:
+    affinity: AffinitySet
+    greedy: list
+    argmin: int
+    objective: Optional[float] = None
+
+
+class HotPath:
+    """One stats handle + device scratch for repeated passes of the same topology."""
+
+    def __init__(self, topo: MoeTopology, device: int = 0, threshold: float = 0.0, top_e: int = 4,
+                 anchor_gpu: int = 0, alpha: float = 1.0, beta: float = 1.0):
+        topo.validate()
+        self.topo = topo
+        self.device = device
+        self.stats = RoutingStats(topo, device)
+        self.threshold, self.top_e, self.anchor_gpu = threshold, top_e, anchor_gpu
+        self.alpha, self.beta = alpha, beta
+        self._out = None
+
+    def _scores(self, C: int):
+        import torch
+
+        if self._out is None or self._out.shape[1] != C:
+            self._out = torch.empty((3, C), dtype=torch.float64, device=f"cuda:{self.device}")
+        return self._out
+
+    def place(self, candidates, greedy_row: bool = True):
+        """Stats already counted: M -> greedy (written into candidates[0] if greedy_row) ->
+        scores -> argmin.  candidates: CUDA uint8 tensor [C][m]."""
+        topo = self.topo
+        M = build_affinity_set(self.stats, topo, self.threshold, self.top_e,
+                               topo.total_experts() // topo.n_gpus, self.anchor_gpu)
+        gp = greedy_place(self.stats, M, topo.n_gpus, out_u8_device=candidates[0] if greedy_row else None)
+        out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
+        return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
+
+    def run(self, trace, candidates, greedy_row: bool = True) -> HotPathResult:
+        """One full pass over a trace (CUDA uint8 [T][L][k] or host array)."""
+        self.stats.reset()
+        self.stats.add_tokens(trace)
+        return self.place(candidates, greedy_row)
+
+    def run_distributed(self, trace_shard, candidates_shard, cand_offset: int, n_candidates: int,
+                        group=None) -> HotPathResult:
+        """This rank's token shard and candidate slice; returns the global argmin."""
+        import torch
+        import torch.distributed as dist
+
+        self.stats.reset()
+        self.stats.add_tokens(trace_shard)
+        allreduce_counts(self.stats, group)
+        topo = self.topo
+        M = build_affinity_set(self.stats, topo, self.threshold, self.top_e,
+                               topo.total_experts() // topo.n_gpus, self.anchor_gpu)
+        gp = greedy_place(self.stats, M, topo.n_gpus,
+                          out_u8_device=candidates_shard[0] if cand_offset == 0 else None)
+        world = dist.get_world_size(group)
+        n_local = candidates_shard.shape[0]
+        dev = torch.device("cuda", self.device)
+        local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
+        if n_local:
+            out, _ = eval_costs(self.stats, candidates_shard, self.alpha, self.beta, out=self._scores(n_local))
+            local[cand_offset:cand_offset + n_local] = out[2]
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(local, op=dist.ReduceOp.MIN, group=group)
+            objs = local.cpu().numpy()
+        else:
+            host = local.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.MIN, group=group)
+            objs = host.numpy()
+        del world
+        return HotPathResult(affinity=M, greedy=gp.assign, argmin=merge_argmin(objs),
+                             objective=float(objs.min()) if objs.size else None)
