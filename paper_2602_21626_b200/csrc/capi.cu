@@ -114,6 +114,16 @@ struct gimbal_stats_s {
   void* hstage[kStages] = {nullptr, nullptr};
   cudaEvent_t ev_copied[kStages] = {nullptr, nullptr};
   cudaEvent_t ev_consumed[kStages] = {nullptr, nullptr};
+  // layer-major ingest buffers (ingest.cu)
+  static constexpr int64_t kLm8BufferBytes = (int64_t)4 << 30;
+  Lm8Plan lm8_plan;
+  cudaStream_t t_stream = nullptr;
+  unsigned long long* lm8[kStages] = {nullptr, nullptr};
+  int64_t lm8_tokens = 0;
+  int lm8_next = 0;
+  cudaEvent_t ev_lm8_ready[kStages] = {nullptr, nullptr};
+  cudaEvent_t ev_lm8_free[kStages] = {nullptr, nullptr};
+  cudaEvent_t ev_order = nullptr;
   // scratch
   DevBuf cand, same, dout, keys, misc, ints;
   std::mutex mu;
@@ -139,8 +149,47 @@ struct gimbal_stats_s {
     return flags_to_status(f & (kFlagIdOutOfRange | kFlagOverflow));
   }
 
+  // Layer-major ingest: the trace is transposed chunk by chunk on t_stream into one of two LM8
+  // buffers while the previous chunk is counted on `stream`.
+  int count_lm8(const uint8_t* ids, int64_t n) {
+    const int L = topo.n_layers, ne = topo.n_experts, k = topo.top_k;
+    const int64_t per_token = (int64_t)L * 8;
+    const int64_t cap_tokens = std::max<int64_t>(1, kLm8BufferBytes / per_token);
+    const int64_t ch = std::min<int64_t>(n, cap_tokens);
+    if (ch > lm8_tokens) {
+      for (int b = 0; b < kStages; ++b) {
+        if (lm8[b]) {
+          GIMBAL_CUDA_TRY(cudaStreamSynchronize(stream));
+          cudaFree(lm8[b]);
+          lm8[b] = nullptr;
+        }
+        GIMBAL_CUDA_TRY(cudaMalloc(&lm8[b], (size_t)ch * per_token));
+      }
+      lm8_tokens = ch;
+    }
+    const int64_t row = (int64_t)L * k;
+    for (int64_t t0 = 0; t0 < n; t0 += ch) {
+      const int b = lm8_next;
+      lm8_next ^= 1;
+      const int64_t cnt = std::min<int64_t>(ch, n - t0);
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(t_stream, ev_lm8_free[b], 0));
+      GIMBAL_CUDA_TRY(launch_transpose_lm8(ids + t0 * row, cnt, L, ne, k, lm8[b], lm8_tokens, dflags, t_stream));
+      GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_ready[b], t_stream));
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_lm8_ready[b], 0));
+      GIMBAL_CUDA_TRY(launch_count_lm8(lm8_plan, lm8[b], cnt, lm8_tokens, dE, stream));
+      GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_free[b], stream));
+    }
+    return GIMBAL_OK;
+  }
+
   int count_device(const void* ids, int id_bytes, int64_t n) {
     const int L = topo.n_layers;
+    if (lm8_supported(L, topo.n_experts, topo.top_k, id_bytes)) {
+      // the transposition must see work already queued on `stream` (e.g. host staging)
+      GIMBAL_CUDA_TRY(cudaEventRecord(ev_order, stream));
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(t_stream, ev_order, 0));
+      return count_lm8(static_cast<const uint8_t*>(ids), n);
+    }
     if (L > 1) {
       GIMBAL_CUDA_TRY(launch_count_pairs(plan, ids, id_bytes, n, dE, dflags, stream));
     } else {
@@ -153,7 +202,7 @@ struct gimbal_stats_s {
   int ensure_staging() {
     if (stage_bytes) return GIMBAL_OK;
     const size_t row = (size_t)topo.n_layers * topo.top_k * 4;
-    stage_bytes = std::max<size_t>(row, (size_t)256 << 20);
+    stage_bytes = std::max<size_t>(row, (size_t)1 << 30);
     for (int b = 0; b < kStages; ++b) {
       GIMBAL_CUDA_TRY(cudaMalloc(&dstage[b], stage_bytes));
       GIMBAL_CUDA_TRY(cudaEventCreateWithFlags(&ev_copied[b], cudaEventDisableTiming));
@@ -241,10 +290,20 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
     gimbal_stats_destroy(h);
     return st;
   };
+  h->lm8_plan = make_lm8_plan(topo->n_layers, topo->n_experts, topo->top_k, h->sms, optin);
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->t_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_order, cudaEventDisableTiming) != cudaSuccess) {
     set_error("gimbal_stats_create: stream creation failed");
     return fail(GIMBAL_CUDA_ERROR);
+  }
+  for (int b = 0; b < gimbal_stats_s::kStages; ++b) {
+    if (cudaEventCreateWithFlags(&h->ev_lm8_ready[b], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_lm8_free[b], cudaEventDisableTiming) != cudaSuccess) {
+      set_error("gimbal_stats_create: event creation failed");
+      return fail(GIMBAL_CUDA_ERROR);
+    }
   }
   const int64_t nA = (int64_t)topo->n_layers * topo->n_experts;
   const int64_t nW = (int64_t)topo->n_experts * topo->n_experts;
@@ -280,8 +339,16 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
     }
     for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints}) b->release();
+    if (h->t_stream) cudaStreamSynchronize(h->t_stream);
+    for (int b = 0; b < gimbal_stats_s::kStages; ++b) {
+      if (h->lm8[b]) cudaFree(h->lm8[b]);
+      if (h->ev_lm8_ready[b]) cudaEventDestroy(h->ev_lm8_ready[b]);
+      if (h->ev_lm8_free[b]) cudaEventDestroy(h->ev_lm8_free[b]);
+    }
+    if (h->ev_order) cudaEventDestroy(h->ev_order);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->t_stream) cudaStreamDestroy(h->t_stream);
   }
   delete h;
   return GIMBAL_OK;

@@ -1,0 +1,332 @@
+// Routing-trace ingestion and transition counting on sm_100a (the DS-V3-class fast path).
+//
+// 1. transpose_lm8_kernel: token-major uint8 trace [T][L][k] (the reference's RoutedStream order,
+//    moe.hpp:75-83) -> layer-major packed form "LM8" [L][T] uint64, each word holding one token's
+//    k <= 8 ids of one layer.  Whole token rows are read coalesced (one HBM pass over the trace),
+//    ids are range-checked here (moe.cpp:176-187 leaves out-of-range ids undefined; we flag them).
+// 2. count_lm8_kernel: one CTA work unit = (token chunk, group of consecutive layer pairs, slice
+//    of rows j).  It streams the two layers of each pair it owns as contiguous 8-byte words and
+//    increments u32 counters privatised in shared memory (ATOMS.POPC.INC), then flushes them to
+//    the u64 tensor once.  When a pair's 256x256 table does not fit shared memory the rows are
+//    split; the row filter would leave lanes idle in every atomic, so each warp first compacts
+//    its passing (row, token) items into a shared queue and then drains the queue with all 32
+//    lanes issuing atomics.
+//
+// Counting: E_l(j,k) += 1 for every (j in slots_l, k in slots_{l+1}) pairing of every token,
+// with multiplicity (moe.cpp:179-188).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+
+constexpr int kTransposeTile = 64;   // tokens per transposition CTA
+constexpr int kBatch = 128;          // tokens per warp batch in the split kernel
+constexpr int kSplitWarps = 24;      // warps per CTA in the split kernel
+
+template <int K>
+__global__ void __launch_bounds__(256)
+    transpose_lm8_kernel(const uint8_t* __restrict__ trace, int64_t T, int L, int ne,
+                         unsigned long long* __restrict__ X, int64_t ld, uint32_t* __restrict__ flags) {
+  extern __shared__ uint8_t tile[];  // kTransposeTile * L * K bytes
+  const int64_t t0 = (int64_t)blockIdx.x * kTransposeTile;
+  const int n = (int)min((int64_t)kTransposeTile, T - t0);
+  const int row = L * K;
+  const int bytes = n * row;
+  const uint8_t* src = trace + t0 * row;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(src);
+  if ((row & 15) == 0 && (addr & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(tile);
+    for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+  } else if ((row & 3) == 0 && (addr & 3) == 0) {
+    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d4 = reinterpret_cast<uint32_t*>(tile);
+    for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+  } else {
+    for (int i = threadIdx.x; i < bytes; i += blockDim.x) tile[i] = src[i];
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int idx = threadIdx.x; idx < L * kTransposeTile; idx += blockDim.x) {
+    const int l = idx / kTransposeTile, i = idx - l * kTransposeTile;
+    if (i >= n) continue;
+    const uint8_t* p = tile + i * row + l * K;
+    unsigned long long w = 0;
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const uint32_t e = p[a];
+      bad |= e >= (uint32_t)ne;
+      w |= (unsigned long long)e << (8 * a);
+    }
+    X[(int64_t)l * ld + t0 + i] = w;
+  }
+  if (bad) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
+}
+
+struct Lm8Params {
+  int L, ne;
+  int P, R;        // pairs per group, rows per part
+  uint32_t swz;    // column XOR swizzle (row r stores column k at k ^ (r & swz))
+  int n_groups, n_parts;
+  int64_t n_units;
+  int64_t chunk_tokens;
+  int64_t T;       // tokens in X
+  int64_t ld;      // row stride of X (tokens)
+};
+
+__device__ __forceinline__ uint32_t id_of(unsigned long long w, int a) {
+  return (uint32_t)(w >> (8 * a)) & 0xffu;
+}
+
+// Whole layer pairs per unit: every slot passes, no filtering.
+template <int K>
+__global__ void __launch_bounds__(1024, 1)
+    count_lm8_pairs_kernel(Lm8Params prm, const unsigned long long* __restrict__ X,
+                           unsigned long long* __restrict__ E) {
+  extern __shared__ uint32_t cnt[];
+  const int ne = prm.ne;
+  const int upc = prm.n_groups;
+  for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
+    const int64_t chunk = unit / upc;
+    const int group = (int)(unit % upc);
+    const int l0 = group * prm.P;
+    const int l1 = min(l0 + prm.P, prm.L - 1);
+    const int words = (l1 - l0) * ne * ne;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) cnt[w] = 0u;
+    __syncthreads();
+    const int64_t t_begin = chunk * prm.chunk_tokens;
+    const int64_t t_end = min(prm.T, t_begin + prm.chunk_tokens);
+    for (int64_t t = t_begin + threadIdx.x; t < t_end; t += blockDim.x) {
+      unsigned long long cur = __ldcs(X + (int64_t)l0 * prm.ld + t);
+      for (int l = l0; l < l1; ++l) {
+        const unsigned long long nxt = __ldcs(X + (int64_t)(l + 1) * prm.ld + t);
+        uint32_t* blk = cnt + (l - l0) * ne * ne;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          const uint32_t j = id_of(cur, a);
+          uint32_t* rowp = blk + j * ne;
+          const uint32_t sw = j & prm.swz;
+#pragma unroll
+          for (int b = 0; b < K; ++b) atomicAdd(rowp + (id_of(nxt, b) ^ sw), 1u);
+        }
+        cur = nxt;
+      }
+    }
+    __syncthreads();
+    const int nn = ne * ne;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) {
+      const uint32_t v = cnt[w];
+      if (v == 0u) continue;
+      const int pr = w / nn;
+      const int r = w - pr * nn;
+      const int j = r / ne;
+      const int kk = (r - j * ne) ^ (j & prm.swz);
+      atomicAdd(E + ((int64_t)(l0 + pr) * ne + j) * ne + kk, (unsigned long long)v);
+    }
+    __syncthreads();
+  }
+}
+
+// One layer pair, rows [j0, j0 + R) per unit, with warp-level compaction of the row filter.
+template <int K>
+__global__ void __launch_bounds__(kSplitWarps * 32, 1)
+    count_lm8_split_kernel(Lm8Params prm, const unsigned long long* __restrict__ X,
+                           unsigned long long* __restrict__ E) {
+  extern __shared__ uint32_t cnt[];
+  const int ne = prm.ne;
+  const int R = prm.R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* stage =
+      reinterpret_cast<unsigned long long*>(cnt + R * ne) + warp * kBatch;  // next-layer ids
+  uint16_t* queue = reinterpret_cast<uint16_t*>(
+                        reinterpret_cast<unsigned long long*>(cnt + R * ne) + kSplitWarps * kBatch) +
+                    warp * (kBatch * K);
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const int upc = prm.n_groups * prm.n_parts;
+  for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
+    const int64_t chunk = unit / upc;
+    const int rem = (int)(unit % upc);
+    const int l = rem / prm.n_parts;
+    const int part = rem - l * prm.n_parts;
+    const int j0 = part * R;
+    const int jR = min(R, ne - j0);
+    const int words = R * ne;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) cnt[w] = 0u;
+    __syncthreads();
+    const int64_t t_begin = chunk * prm.chunk_tokens;
+    const int64_t t_end = min(prm.T, t_begin + prm.chunk_tokens);
+    const unsigned long long* Xl = X + (int64_t)l * prm.ld;
+    const unsigned long long* Xn = X + (int64_t)(l + 1) * prm.ld;
+    for (int64_t base = t_begin + (int64_t)warp * kBatch; base < t_end;
+         base += (int64_t)kSplitWarps * kBatch) {
+      unsigned long long cur[kBatch / 32];
+      bool valid[kBatch / 32];
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q) {
+        const int64_t t = base + q * 32 + lane;
+        valid[q] = t < t_end;
+        cur[q] = valid[q] ? __ldcs(Xl + t) : 0ull;
+        stage[q * 32 + lane] = valid[q] ? __ldcs(Xn + t) : 0ull;
+      }
+      int n_items = 0;
+#pragma unroll
+      for (int q = 0; q < kBatch / 32; ++q) {
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          const uint32_t j = id_of(cur[q], a) - (uint32_t)j0;
+          const bool pass = valid[q] && j < (uint32_t)jR;
+          const uint32_t m = __ballot_sync(0xffffffffu, pass);
+          if (pass) queue[n_items + __popc(m & lt_mask)] = (uint16_t)(j | ((q * 32 + lane) << 8));
+          n_items += __popc(m);
+        }
+      }
+      __syncwarp();
+      for (int i = lane; i < n_items; i += 32) {
+        const uint32_t it = queue[i];
+        const uint32_t r = it & 0xffu;
+        const unsigned long long nx = stage[it >> 8];
+        uint32_t* rowp = cnt + r * ne;
+        const uint32_t sw = r & prm.swz;
+#pragma unroll
+        for (int b = 0; b < K; ++b) atomicAdd(rowp + (id_of(nx, b) ^ sw), 1u);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < jR * ne; w += blockDim.x) {
+      const uint32_t v = cnt[w];
+      if (v == 0u) continue;
+      const int j = w / ne;
+      const int kk = (w - j * ne) ^ (j & prm.swz);
+      atomicAdd(E + ((int64_t)l * ne + (j0 + j)) * ne + kk, (unsigned long long)v);
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+cudaError_t launch_transpose_k(const uint8_t* trace, int64_t T, int L, int ne, unsigned long long* X,
+                               int64_t ld, uint32_t* flags, cudaStream_t s) {
+  const size_t smem = (size_t)kTransposeTile * L * K;
+  auto kern = transpose_lm8_kernel<K>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t grid = (T + kTransposeTile - 1) / kTransposeTile;
+  kern<<<(unsigned)grid, 256, smem, s>>>(trace, T, L, ne, X, ld, flags);
+  return cudaGetLastError();
+}
+
+template <int K>
+cudaError_t launch_count_k(const Lm8Plan& plan, const Lm8Params& prm, const unsigned long long* X,
+                           unsigned long long* E, cudaStream_t s, int grid) {
+  if (plan.split) {
+    auto kern = count_lm8_split_kernel<K>;
+    const size_t smem = (size_t)plan.R * plan.ne * 4 + (size_t)kSplitWarps * kBatch * 8 +
+                        (size_t)kSplitWarps * kBatch * K * 2;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kSplitWarps * 32, smem, s>>>(prm, X, E);
+  } else {
+    auto kern = count_lm8_pairs_kernel<K>;
+    const size_t smem = (size_t)plan.P * plan.ne * plan.ne * 4;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 1024, smem, s>>>(prm, X, E);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool lm8_supported(int L, int ne, int k, int id_bytes) {
+  return id_bytes == 1 && L > 1 && k >= 1 && k <= 8 && ne <= 256 && (int64_t)kTransposeTile * L * k <= 200 * 1024;
+}
+
+Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin) {
+  Lm8Plan p;
+  p.L = L;
+  p.ne = ne;
+  p.k = k;
+  p.sms = sms;
+  const int pairs = L - 1;
+  const int budget = std::min(max_smem_optin, 200 * 1024);
+  const int pair_bytes = ne * ne * 4;
+  if (pair_bytes <= budget) {
+    p.split = false;
+    p.R = ne;
+    p.n_parts = 1;
+    p.P = std::max(1, std::min(pairs, budget / pair_bytes));
+    const int ng = (pairs + p.P - 1) / p.P;
+    p.P = (pairs + ng - 1) / ng;
+    p.n_groups = (pairs + p.P - 1) / p.P;
+  } else {
+    p.split = true;
+    p.P = 1;
+    const int queue_bytes = kSplitWarps * kBatch * (8 + 2 * k);
+    const int split_budget = max_smem_optin - 4096;
+    const int max_rows = std::max(1, std::min(256, (split_budget - queue_bytes) / (ne * 4)));
+    p.n_parts = (ne + max_rows - 1) / max_rows;
+    p.R = (ne + p.n_parts - 1) / p.n_parts;
+    p.n_groups = pairs;
+  }
+  return p;
+}
+
+cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne, int k,
+                                 unsigned long long* X, int64_t ld, uint32_t* flags, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  switch (k) {
+    case 1: return launch_transpose_k<1>(trace, T, L, ne, X, ld, flags, s);
+    case 2: return launch_transpose_k<2>(trace, T, L, ne, X, ld, flags, s);
+    case 3: return launch_transpose_k<3>(trace, T, L, ne, X, ld, flags, s);
+    case 4: return launch_transpose_k<4>(trace, T, L, ne, X, ld, flags, s);
+    case 5: return launch_transpose_k<5>(trace, T, L, ne, X, ld, flags, s);
+    case 6: return launch_transpose_k<6>(trace, T, L, ne, X, ld, flags, s);
+    case 7: return launch_transpose_k<7>(trace, T, L, ne, X, ld, flags, s);
+    case 8: return launch_transpose_k<8>(trace, T, L, ne, X, ld, flags, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, int64_t T, int64_t ld,
+                             unsigned long long* E, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  Lm8Params prm;
+  prm.L = plan.L;
+  prm.ne = plan.ne;
+  prm.P = plan.P;
+  prm.R = plan.R;
+  prm.swz = (plan.ne % 32 == 0) ? 31u : 0u;
+  prm.n_groups = plan.n_groups;
+  prm.n_parts = plan.n_parts;
+  prm.T = T;
+  prm.ld = ld;
+  const int64_t base_units = (int64_t)plan.n_groups * plan.n_parts;
+  const int64_t resident = plan.sms;
+  // ~4 waves of units for load balance (hot rows make units uneven), at least 16K tokens each
+  int64_t n_chunks = std::max<int64_t>(1, (4 * resident + base_units - 1) / base_units);
+  n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
+  prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
+  n_chunks = (T + prm.chunk_tokens - 1) / prm.chunk_tokens;
+  prm.n_units = n_chunks * base_units;
+  const int grid = (int)std::min<int64_t>(prm.n_units, resident);
+  switch (plan.k) {
+    case 1: return launch_count_k<1>(plan, prm, X, E, s, grid);
+    case 2: return launch_count_k<2>(plan, prm, X, E, s, grid);
+    case 3: return launch_count_k<3>(plan, prm, X, E, s, grid);
+    case 4: return launch_count_k<4>(plan, prm, X, E, s, grid);
+    case 5: return launch_count_k<5>(plan, prm, X, E, s, grid);
+    case 6: return launch_count_k<6>(plan, prm, X, E, s, grid);
+    case 7: return launch_count_k<7>(plan, prm, X, E, s, grid);
+    case 8: return launch_count_k<8>(plan, prm, X, E, s, grid);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace gimbal_gpu

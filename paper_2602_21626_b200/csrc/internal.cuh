@@ -78,6 +78,19 @@ struct StatsPlan {
 };
 StatsPlan make_stats_plan(int L, int ne, int k, int sms, int max_smem_optin);
 
+// Layer-major packed ingest path (ingest.cu): uint8 ids, top_k <= 8.
+struct Lm8Plan {
+  int L = 0, ne = 0, k = 0, sms = 148;
+  bool split = false;  // rows of one pair split over units (with warp compaction)
+  int P = 1, R = 0, n_groups = 0, n_parts = 1;
+};
+bool lm8_supported(int L, int ne, int k, int id_bytes);
+Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin);
+cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne, int k,
+                                 unsigned long long* X, int64_t ld, uint32_t* flags, cudaStream_t s);
+cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, int64_t T, int64_t ld,
+                             unsigned long long* E, cudaStream_t s);
+
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_count_activation(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,

@@ -33,6 +33,7 @@ namespace {
 struct CountParams {
   int L, ne, k;
   int P, R;            // pairs per group, rows per part
+  uint32_t swz;        // column XOR swizzle mask (row j stores column k at k ^ (j & swz))
   int n_groups, n_parts;
   int64_t n_units;
   int64_t chunk_tokens;
@@ -123,8 +124,9 @@ __global__ void __launch_bounds__(1024, 1)
           const uint32_t j = cur[a] - (uint32_t)j0;
           if (j < (uint32_t)jR) {
             uint32_t* rowp = blk + j * ne;
+            const uint32_t sw = j & prm.swz;
 #pragma unroll
-            for (int b = 0; b < K; ++b) atomicAdd(rowp + nxt[b], 1u);
+            for (int b = 0; b < K; ++b) atomicAdd(rowp + (nxt[b] ^ sw), 1u);
           }
         }
 #pragma unroll
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(1024, 1)
       const int pr = w / rows_ne;
       const int r = w - pr * rows_ne;
       const int j = r / ne;
-      const int kk = r - j * ne;
+      const int kk = (r - j * ne) ^ (j & prm.swz);
       atomicAdd(E + ((int64_t)(l0 + pr) * ne + (j0 + j)) * ne + kk, (unsigned long long)v);
     }
     __syncthreads();
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(1024, 1)
           const uint32_t j = (uint32_t)row[(int64_t)l * K + a] - (uint32_t)j0;
           if (j >= (uint32_t)jR) continue;
           for (int b = 0; b < K; ++b)
-            atomicAdd(blk + j * ne + (uint32_t)row[(int64_t)(l + 1) * K + b], 1u);
+            atomicAdd(blk + j * ne + ((uint32_t)row[(int64_t)(l + 1) * K + b] ^ (j & prm.swz)), 1u);
         }
       }
     }
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(1024, 1)
       const int pr = w / rows_ne;
       const int r = w - pr * rows_ne;
       const int j = r / ne;
-      const int kk = r - j * ne;
+      const int kk = (r - j * ne) ^ (j & prm.swz);
       atomicAdd(E + ((int64_t)(l0 + pr) * ne + (j0 + j)) * ne + kk, (unsigned long long)v);
     }
     __syncthreads();
@@ -379,6 +381,9 @@ cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_by
   prm.k = plan.k;
   prm.P = plan.pairs_per_group;
   prm.R = plan.rows_per_part;
+  // Zipf-hot columns would otherwise put many lanes of one warp into one bank with different
+  // rows; XOR-ing the low 5 column bits with the row spreads them (needs n_e % 32 == 0).
+  prm.swz = (plan.ne % 32 == 0) ? 31u : 0u;
   prm.n_groups = plan.n_groups;
   prm.n_parts = plan.n_parts;
   prm.T = T;

@@ -133,8 +133,20 @@ class RoutingStats:
     def add_tokens(self, ids) -> None:
         self._flush()
         ptr, ib, n, mem, keep = _trace_arg(ids, self.topo)
+        if mem == N.MEM_DEVICE:
+            self._after_torch(keep)
         N.check(N.lib().gimbal_stats_add_tokens(self._h, C.c_void_p(ptr), ib, n, mem), "add_tokens")
         del keep
+
+    def _after_torch(self, tensor) -> None:
+        """Orders the handle's stream after torch's current stream (device inputs produced by
+        torch), without a host synchronisation."""
+        import torch
+
+        s = C.c_void_p()
+        N.check(N.lib().gimbal_stats_device_buffers(self._h, None, None, C.byref(s)), "buffers")
+        ours = torch.cuda.ExternalStream(s.value, device=tensor.device)
+        ours.wait_stream(torch.cuda.current_stream(tensor.device))
 
     def _flush(self) -> None:
         if self._pending:

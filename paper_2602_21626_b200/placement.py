@@ -97,6 +97,8 @@ def eval_costs(stats: RoutingStats, candidates, alpha: float = 1.0, beta: float 
     if hasattr(candidates, "data_ptr"):
         cptr, cmem, n, keep = candidates.data_ptr(), (N.MEM_DEVICE if candidates.is_cuda else N.MEM_HOST), \
             candidates.shape[0], candidates
+        if cmem == N.MEM_DEVICE:
+            stats._after_torch(candidates)
     else:
         keep = np.ascontiguousarray(np.asarray(candidates, np.uint8))
         cptr, cmem, n = keep.ctypes.data, N.MEM_HOST, keep.shape[0]
