@@ -255,6 +255,7 @@ Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin) {
   p.k = k;
   p.sms = sms;
   const int pairs = L - 1;
+  if (pairs < 1) return p;  // no layer pairs: A is counted directly (stats.cu)
   const int budget = std::min(max_smem_optin, 200 * 1024);
   const int pair_bytes = ne * ne * 4;
   if (pair_bytes <= budget) {

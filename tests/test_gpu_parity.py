@@ -195,3 +195,113 @@ def test_generator_bit_exact_with_cpu_twin(G, orc):
                               drift_epoch=epoch, device=0)
         twin = orc.generate_trace(L, ne, k, cdf.ravel(), int(thr[0]), int(thr[1]), 17, 1000, 3000)
         assert np.array_equal(tr.cpu().numpy(), twin)
+
+
+# ---- the reference's KATs and golden fixtures through the GPU path ----
+
+def test_kats_through_gpu(G):
+    import kat_util as K
+
+    k = K.kats()
+    for c in k["stats"]:
+        s = G.RoutingStats(G.MoeTopology(c["L"], c["ne"], c["k"], 2), 0)
+        s.add_tokens(K.trace(c))
+        A, E, W = s.read()
+        assert np.array_equal(A, np.asarray(c["A"], np.uint64)) and s.tokens() == c["tokens"], c["src"]
+        assert np.array_equal(E, K.expected_e(c)) and np.array_equal(W, K.expected_w(c)), c["src"]
+    for c in k["comm_cost"]:
+        topo = G.MoeTopology(c["L"], c["ne"], c["k"], 2)
+        st = G.RoutedStream(topo, len(c["choices"]), K.trace(c))
+        if c.get("error"):
+            with pytest.raises(ValueError):
+                G.comm_cost(st, c["assign"])
+        else:
+            assert G.comm_cost(st, c["assign"]) == c["expected"], c["src"]
+    for c in k["eval_cost"]:
+        A = np.asarray(c["A"], np.float64)
+        p = G.PlacementProblem(A=A, W=K.dense_w(c["W"], A.shape[1]), g=c["g"], alpha=c.get("alpha", 1.0),
+                               beta=c.get("beta", 1.0))
+        if c.get("error"):
+            with pytest.raises(ValueError):
+                G.eval_cost(p, G.Placement(c["assign"]))
+            continue
+        cost = G.eval_cost(p, G.Placement(c["assign"]))
+        for key, attr in (("D", "deviation"), ("cut", "cut"), ("objective", "objective")):
+            if key in c:
+                assert getattr(cost, attr) == c[key], c["src"]
+    for c in k["affinity_set"]:
+        topo = G.MoeTopology(c["L"], c["ne"], 1, c["g"])
+        E = K.e_from_nonzero(c).astype(np.float64)
+        got = G.build_affinity_set(G.AffinityTensor(E=E, W=E.sum(0)), topo, c["threshold"], c["top_e"],
+                                   c["capacity"], c["anchor"])
+        assert got.experts == c["expected"] and got.anchor_gpu == c["anchor"], c["src"]
+    for c in k["greedy"]:
+        A = np.asarray(c["A"], np.float64)
+        if c.get("error"):
+            with pytest.raises(ValueError):
+                G.greedy_place(A, G.AffinitySet(c["M"], c["anchor"]), c["g"])
+            continue
+        pl = G.greedy_place(A, G.AffinitySet(c["M"], c["anchor"]), c["g"])
+        if "expected" in c:
+            assert pl.assign == c["expected"], c["src"]
+        if "deviation" in c:
+            p = G.PlacementProblem(A=A, W=np.zeros((A.shape[1],) * 2), g=c["g"])
+            assert G.eval_cost(p, pl).deviation == c["deviation"]
+    for c in k["maybe_relocate"]:
+        A = np.asarray(c["A"], np.float64)
+        r = G.maybe_relocate(c["step"], c["tau"], G.AffinitySet(), A, c["g"], G.Placement(c["prev"]))
+        assert (r is not None) == c["fires"]
+        if r is not None:
+            again = G.maybe_relocate(2 * c["step"], c["tau"], G.AffinitySet(), A, c["g"], r.placement)
+            assert again.moved == c["again_moved"] and again.placement.assign == r.placement.assign
+
+
+def test_golden_fixtures_through_gpu(G):
+    import kat_util as K
+
+    for c in K.golden_cases():
+        L, ne, k, g = (int(x) for x in c["topo"])
+        thr, top = float(c["params"][3]), int(c["params"][4])
+        topo = G.MoeTopology(L, ne, k, g)
+        s = G.RoutingStats(topo, 0)
+        s.add_tokens(c["ids"])
+        A, E, W = s.read()
+        assert np.array_equal(A, c["A"]) and np.array_equal(E, c["E"]) and np.array_equal(W, c["W"])
+        assert s.tokens() == int(c["tokens"])
+        # flat forms (moe.cpp:207-231) as the reference builds them
+        fA, fW = s.flat_activation(), s.flat_pair_weights()
+        assert fA.shape == (L, L * ne) and fW.shape == (L * ne, L * ne)
+        assert np.array_equal(fA.sum(0), np.concatenate(list(c["A"])).astype(np.float64))
+        assert G.comm_cost(G.RoutedStream(topo, int(c["tokens"]), c["ids"]), c["assign"]) == int(c["comm_cost"])
+        D, cut, obj, _ = G.eval_costs(s, np.asarray([c["assign"]], np.uint8))
+        assert (D[0], cut[0], obj[0]) == tuple(c["cost"])
+        D, cut, obj, _ = G.eval_costs(s, np.asarray([c["assign"]], np.uint8), 2.5, 0.75)
+        assert (D[0], cut[0], obj[0]) == tuple(c["cost_ab"])
+        # dense reference form on the flat matrices agrees too
+        dense = G.eval_cost(G.PlacementProblem(A=fA, W=fW, g=g), G.Placement(list(c["assign"])))
+        assert (dense.deviation, dense.cut, dense.objective) == tuple(c["cost"])
+        M = G.build_affinity_set(s, topo, thr, top, L * ne // g, g - 1)
+        assert M.experts == list(c["M"])
+        gp = G.greedy_place(s, M, g)
+        assert gp.assign == list(c["greedy"])
+        assert G.greedy_place(fA, M, g).assign == list(c["greedy"])
+
+
+def test_bench_scale_properties(G):
+    """Size-independent identities at a BASELINE-scale token count (DS-V3 shape, 4M tokens):
+    A row sums = T*k, sum E_l = T*k^2, W = sum_l E_l, and cut == comm_cost for two placements."""
+    L, ne, k, g = SHAPES["dsv3"]
+    topo = G.MoeTopology(L, ne, k, g)
+    T = 1 << 22
+    trace = G.generate_trace(topo, T, model_seed=1, stream_seed=2, device=0)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(trace)
+    A, E, W = s.read()
+    assert (A.sum(axis=1) == T * k).all()
+    assert (E.reshape(L - 1, -1).sum(axis=1) == T * k * k).all()
+    assert np.array_equal(W, E.sum(axis=0, dtype=np.uint64))
+    assert (E.sum(axis=2) == A[:-1] * k).all() and (E[-1].sum(axis=0) == A[-1] * k).all()
+    stream = G.RoutedStream(topo, T, trace)
+    for assign in (G.static_placement(topo).assign, list(G.shuffled_candidates(L * ne, g, 5, 1)[0])):
+        _, cut, _, _ = G.eval_costs(s, np.asarray([assign], np.uint8))
+        assert cut[0] == float(G.comm_cost(stream, assign))

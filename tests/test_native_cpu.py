@@ -1,0 +1,131 @@
+"""The C ABI library without a GPU: it loads, exports every symbol include/gimbal_gpu.h declares,
+and its host-side validation / utilities match the reference (no kernel launches here)."""
+import ctypes as C
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import kat_util as K
+
+
+def header_functions():
+    from paper_2602_21626_b200 import _native as N
+
+    text = open(N.HEADER_PATH).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(gimbal_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(G):
+    from paper_2602_21626_b200 import _native as N
+
+    names = header_functions()
+    assert len(names) >= 20
+    lib = N.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+    nm = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", nm), f"{n} not exported"
+    # the ctypes table covers exactly the header
+    assert sorted(s[0] for s in N.SIGNATURES) == names
+
+
+def test_library_is_sm100a_only(G):
+    from paper_2602_21626_b200 import _native as N
+
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_abi_version(G):
+    assert G._native.lib().gimbal_abi_version() == 1
+
+
+def test_topology_validation_messages(G):
+    for c in K.kats()["topology_invalid"]:
+        with pytest.raises(ValueError, match="MoeTopology"):
+            G.MoeTopology(*c["topo"]).validate()
+    G.MoeTopology(58, 256, 8, 8).validate()
+
+
+def test_static_placement_kat(G, orc):
+    for c in K.kats()["static_placement"]:
+        assert G.static_placement(G.MoeTopology(c["L"], c["ne"], c["k"], c["g"])).assign == c["expected"]
+    for (L, ne, k, g) in ((58, 256, 8, 8), (26, 64, 6, 8), (3, 12, 2, 3)):
+        got = G.static_placement(G.MoeTopology(L, ne, k, g)).assign
+        assert got == list(orc.static_placement(L, ne, k, g))
+
+
+def test_dense_validation_errors_match_reference(G):
+    # errors raised before any device work (placement.cpp:13-50, 243-252)
+    p = G.PlacementProblem(A=np.ones((1, 4)), W=np.zeros((4, 4)), g=2)
+    for bad in ([0, 0, 0, 1], [0, 0, 1, 2]):
+        with pytest.raises(ValueError, match="placement"):
+            G.eval_cost(p, G.Placement(bad))
+    with pytest.raises(ValueError, match="alpha and beta"):
+        G.eval_cost(G.PlacementProblem(A=np.ones((1, 4)), W=np.zeros((4, 4)), g=2, alpha=0.0), G.Placement([0, 0, 1, 1]))
+    with pytest.raises(ValueError, match="divisible"):
+        G.eval_cost(G.PlacementProblem(A=np.ones((1, 3)), W=np.zeros((3, 3)), g=2), G.Placement([0, 0, 1]))
+    with pytest.raises(ValueError, match="exceeds anchor capacity"):
+        G.greedy_place(np.ones((1, 4)), G.AffinitySet([0, 1, 2], 0), 2)
+    with pytest.raises(ValueError, match="duplicate affinity id"):
+        G.greedy_place(np.ones((1, 4)), G.AffinitySet([1, 1], 0), 2)
+    with pytest.raises(ValueError, match="affinity id out of range"):
+        G.greedy_place(np.ones((1, 4)), G.AffinitySet([7], 0), 2)
+    with pytest.raises(ValueError, match="anchor_gpu out of range"):
+        G.greedy_place(np.ones((1, 4)), G.AffinitySet([], 2), 2)
+    with pytest.raises(ValueError, match="tau"):
+        G.maybe_relocate(1, 0, G.AffinitySet(), np.ones((1, 4)), 2, G.Placement())
+    assert G.maybe_relocate(2999, 3000, G.AffinitySet(), np.ones((1, 8)), 2, G.Placement()) is None
+    topo = G.MoeTopology(2, 8, 1, 2)
+    aff = G.AffinityTensor(E=np.zeros((1, 8, 8)), W=np.zeros((8, 8)))
+    with pytest.raises(ValueError, match="anchor_gpu out of range"):
+        G.build_affinity_set(aff, topo, 0.0, 4, 8, 5)
+    with pytest.raises(ValueError, match="depth mismatch"):
+        G.build_affinity_set(G.AffinityTensor(E=np.zeros((2, 8, 8)), W=np.zeros((8, 8))), topo, 0.0, 4, 8, 0)
+
+
+def test_comm_cost_validation(G):
+    topo = G.MoeTopology(2, 4, 1, 2)
+    s = G.RoutedStream(topo, 1, np.array([[[0], [0]]], np.uint8))
+    with pytest.raises(ValueError, match="unplaced expert"):
+        G.comm_cost(s, [0, 0, 1, 1, -1, 1, 1, 0])
+    with pytest.raises(ValueError, match="size mismatch"):
+        G.comm_cost(s, [0, 0, 1])
+
+
+def test_shuffled_candidates_follow_reference_recipe(G, ref):
+    # assign[e] = e % g then Rng(seed).shuffle (acceptance_main.cpp:344-351), rng.hpp:64-71
+    c = G.shuffled_candidates(96, 8, 40, 5)
+    for i in range(5):
+        assert list(c[i]) == list(ref.shuffled_balanced(96, 8, 40 + i))
+    assert all(np.bincount(row, minlength=8).tolist() == [12] * 8 for row in c)
+
+
+def test_generator_tables_follow_reference_model(G, ref):
+    # the base weights behind the CDF are the reference RoutingModel's (moe.cpp:61-80)
+    for (L, ne, s) in ((4, 8, 1.2), (3, 64, 1.0), (5, 256, 1.5)):
+        topo = G.MoeTopology(L, ne, 2, 2)
+        cdf, thr = G.generator_tables(topo, G.RoutingParams(zipf_s=s), model_seed=77)
+        base, kern = ref.model_weights(L, ne, 2, 2, 77, zipf_s=s)
+        q = np.diff(np.concatenate([np.zeros((L, 1)), cdf.astype(np.float64)], axis=1), axis=1) / 2.0 ** 32
+        q[:, -1] = 1.0 - cdf[:, -2] / 2.0 ** 32
+        assert np.allclose(q, base, atol=1e-8)
+        # mixture thresholds: P(base) = 1 - lambda, P(uniform) = lambda * rest * n_e
+        rest = (1 - 0.8) / (ne - 1)
+        assert abs(int(thr[0]) / 2 ** 32 - 0.5) < 1e-9
+        assert abs(int(thr[1]) / 2 ** 32 - (0.5 + 0.5 * rest * ne)) < 1e-9
+        assert np.allclose(kern[np.arange(ne), (np.arange(ne) + 1) % ne], 0.8)
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    from paper_2602_21626_b200 import _native as N
+
+    monkeypatch.setattr(N, "_LIB", None)
+    monkeypatch.setattr(N, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(ImportError):
+        N.lib()
