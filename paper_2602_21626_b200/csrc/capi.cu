@@ -107,6 +107,10 @@ struct gimbal_stats_s {
   uint32_t* dflags = nullptr;
   int64_t tokens = 0;
   bool derived = true;
+  // evaluator choice cached per count state (counts only change through add/reset/reduce,
+  // each of which changes `tokens` or resets max_tokens)
+  int64_t max_tokens = -1;
+  bool small_cells = false;
   // host-ingest staging (double-buffered)
   static constexpr int kStages = 2;
   size_t stage_bytes = 0;
@@ -365,6 +369,7 @@ int gimbal_stats_reset(gimbal_stats_t h) {
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dW, 0, nW * 8, h->stream));
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 64, h->stream));
   h->tokens = 0;
+  h->max_tokens = -1;
   h->derived = true;
   return GIMBAL_OK;
 }
@@ -465,6 +470,7 @@ int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
   if (global_tokens < 0) return invalid("mark_reduced: negative token count");
   std::lock_guard<std::mutex> lk(h->mu);
   h->tokens = global_tokens;
+  h->max_tokens = -1;
   h->derived = h->topo.n_layers < 2;
   return GIMBAL_OK;
 }
@@ -502,9 +508,19 @@ int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, in
     dobj = dcut + C;
   }
   darg = reinterpret_cast<long long*>(h->dout.as<double>() + 3 * C);
+  if (h->max_tokens != h->tokens) {
+    // cells < 2^27 lets the evaluator keep 32-bit partial sums (one host sync per new count state)
+    unsigned long long mx = 0;
+    GIMBAL_TRY(h->misc.ensure(64));
+    GIMBAL_CUDA_TRY(launch_max_cell(h->dE, h->nE(), h->misc.as<unsigned long long>(), h->stream));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(&mx, h->misc.p, 8, cudaMemcpyDeviceToHost, h->stream));
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    h->small_cells = mx < (1ull << 27);
+    h->max_tokens = h->tokens;
+  }
   GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
                                     h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
-                                    h->dflags, h->sms, h->stream));
+                                    h->dflags, h->small_cells, h->stream));
   const unsigned long long total =
       (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
   GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,

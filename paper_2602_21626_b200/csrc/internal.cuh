@@ -108,8 +108,10 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
                               const unsigned long long* E, const uint8_t* cands, int64_t C,
                               double alpha, double beta, unsigned long long* scratch_same,
                               double* D, double* cut, double* obj, long long* argmin,
-                              uint32_t* flags, int sms, cudaStream_t s);
+                              uint32_t* flags, bool small_cells, cudaStream_t s);
 size_t eval_scratch_bytes(int64_t C);
+// max over E cells (for choosing 32-bit partial sums in the evaluator)
+cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s);
 
 cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
                                const unsigned long long* same, const double* D, double* cut,

@@ -96,6 +96,76 @@ __global__ void __launch_bounds__(kEvalThreads)
   }
 }
 
+// Fast form for n_e in {32, 64, 128, 256} and E cells < 2^27 (u32 partial sums): thread owns
+// column k of 32 consecutive rows of one layer pair, so per candidate it reads its column's GPU
+// once and the 32 rows' GPUs as two broadcast 16-byte shared loads.
+__global__ void __launch_bounds__(kEvalThreads)
+    eval_same_fast_kernel(int L, int ne, const unsigned long long* __restrict__ E,
+                          const uint8_t* __restrict__ cands, int64_t C, int64_t m,
+                          unsigned long long* __restrict__ same) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int rows_per_cta = kEvalCellsPerCta / ne;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;          // first flat row of this CTA
+  const int64_t n_rows = (int64_t)(L - 1) * ne;
+  const int grp = threadIdx.x / ne;                                 // 32-row group of this thread
+  const int k = threadIdx.x - grp * ne;
+  const int64_t rg = r0 + (int64_t)grp * 32;                         // its first row
+  const int64_t layer = rg / ne;                                     // rows rg..rg+31 share it
+  const int64_t span_hi = min(m, (min(n_rows, r0 + rows_per_cta) - 1) / ne * ne + 2 * ne);
+  const int span = (int)((span_hi - r0 + 15) & ~15ll);               // 16-byte aligned stride
+  uint32_t e[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) e[i] = rg + i < n_rows ? (uint32_t)E[(rg + i) * ne + k] : 0u;
+  const int rowo = (int)(rg - r0);
+  const int colo = (int)((layer + 1) * ne + k - r0);
+  const bool active = rg < n_rows;
+  __shared__ unsigned long long red[kEvalThreads / 32][kEvalCands];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t c0 = 0; c0 < C; c0 += kEvalCands) {
+    const int nc = (int)min((int64_t)kEvalCands, C - c0);
+    const int live = (int)(span_hi - r0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nc * live; idx += blockDim.x) {
+      const int c = idx / live, o = idx - c * live;
+      sm[c * span + o] = cands[(c0 + c) * m + r0 + o];
+    }
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const uint8_t* P = sm + c * span;
+      uint32_t s = 0;
+      if (active) {
+        const uint32_t q = P[colo];
+        const uint4 w0 = *reinterpret_cast<const uint4*>(P + rowo);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(P + rowo + 16);
+        const uint32_t w[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s += (((w[i >> 2] >> (8 * (i & 3))) & 0xffu) == q) ? e[i] : 0u;
+      }
+      unsigned long long s64 = s;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+      if (lane == 0) red[warp][c] = s64;
+    }
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      unsigned long long s = 0;
+#pragma unroll
+      for (int w = 0; w < kEvalThreads / 32; ++w) s += red[w][threadIdx.x];
+      if (s) atomicAdd(&same[c0 + threadIdx.x], s);
+    }
+  }
+}
+
+__global__ void max_cell_kernel(const unsigned long long* __restrict__ E, int64_t n,
+                                unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, E[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
 // ---- deviation + feasibility: one CTA per candidate, one warp per layer at a time ----
 __global__ void __launch_bounds__(256)
     eval_dev_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
@@ -282,20 +352,20 @@ __global__ void greedy_keys_kernel(int64_t m, const unsigned long long* __restri
   }
 }
 
-// One warp walks the sorted order; lanes hold GPUs p (g <= 32 per pass).
+constexpr int kGreedyKeyChunk = 8192;  // sorted keys staged per round (64 KB)
+
 __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
                                    const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
                                    const unsigned long long* __restrict__ keys, int64_t n_keys,
                                    int32_t* __restrict__ out, uint8_t* __restrict__ out_u8) {
-  extern __shared__ unsigned long long load[];  // [L][g]
+  extern __shared__ unsigned long long load[];  // [L][g], then counts [g], then staged keys
   int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
-  const int lane = threadIdx.x;
   const int64_t m = (int64_t)L * ne;
   const int cap = (int)(m / g);
-  for (int64_t i = lane; i < (int64_t)L * g; i += 32) load[i] = 0ull;
-  for (int p = lane; p < g; p += 32) counts[p] = 0;
-  __syncwarp();
-  if (lane == 0) {
+  for (int64_t i = threadIdx.x; i < (int64_t)L * g; i += blockDim.x) load[i] = 0ull;
+  for (int p = threadIdx.x; p < g; p += blockDim.x) counts[p] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
     for (int i = 0; i < nM; ++i) {  // placement.cpp:272-279
       const int e = M[i];
       out[e] = anchor;
@@ -304,46 +374,44 @@ __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long lon
       counts[anchor] += 1;
     }
   }
-  __syncwarp();
-  for (int64_t i = 0; i < n_keys; ++i) {
-    const unsigned long long key = keys[i];
-    if (key == 0ull) break;
-    const int64_t e = 0xffffffll - (int64_t)(key & 0xffffffull);
-    const unsigned long long a = key >> 24;
-    // home = first argmax row of the flat column: its layer if A > 0, else row 0
-    const int64_t row = a > 0 ? e / ne : 0;
-    int best_p = -1;
-    unsigned long long best_v = 0ull;
-    for (int p0 = 0; p0 < g; p0 += 32) {
-      const int p = p0 + lane;
-      int cand = -1;
-      unsigned long long v = 0ull;
-      if (p < g && counts[p] < cap) {
-        cand = p;
-        v = load[row * g + p];
-      }
-      // warp argmin: smaller load, then lower p (== first strict-< winner in p order)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const int c2 = __shfl_xor_sync(0xffffffffu, cand, o);
-        const unsigned long long v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        if (c2 >= 0 && (cand < 0 || v2 < v || (v2 == v && c2 < cand))) {
-          cand = c2;
-          v = v2;
+  __syncthreads();
+  // The walk is inherently sequential (each choice reads the loads the previous ones wrote), so
+  // one thread walks while the CTA stages the sorted keys through shared memory ahead of it.
+  unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(counts + ((g + 1) & ~1));
+  bool done = false;
+  for (int64_t base = 0; base < n_keys && !done; base += kGreedyKeyChunk) {
+    const int nk = (int)min((int64_t)kGreedyKeyChunk, n_keys - base);
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) kbuf[i] = keys[base + i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const unsigned long long key = kbuf[i];
+        if (key == 0ull) {
+          done = true;
+          break;
         }
-      }
-      if (cand >= 0 && (best_p < 0 || v < best_v)) {
-        best_p = cand;
-        best_v = v;
+        const int e = 0xffffff - (int)(key & 0xffffffull);
+        const unsigned long long a = key >> 24;
+        const int layer = e / ne;
+        // home = first argmax row of the flat column: its layer if A > 0, else row 0
+        const unsigned long long* lr = load + (a > 0 ? layer : 0) * g;
+        int best = -1;
+        unsigned long long bv = 0ull;
+        for (int p = 0; p < g; ++p) {  // placement.cpp:290-295: strict <, lowest p first
+          if (counts[p] >= cap) continue;
+          const unsigned long long v = lr[p];
+          if (best < 0 || v < bv) {
+            best = p;
+            bv = v;
+          }
+        }
+        out[e] = best;
+        if (out_u8) out_u8[e] = (uint8_t)best;
+        load[layer * g + best] += a;
+        counts[best] += 1;
       }
     }
-    if (lane == 0) {
-      out[e] = best_p;
-      if (out_u8) out_u8[e] = (uint8_t)best_p;
-      load[(e / ne) * g + best_p] += a;
-      counts[best_p] += 1;
-    }
-    __syncwarp();
+    done = __syncthreads_or(done);
   }
 }
 
@@ -443,8 +511,7 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
                               const unsigned long long* E, const uint8_t* cands, int64_t C,
                               double alpha, double beta, unsigned long long* scratch_same,
                               double* D, double* cut, double* obj, long long* argmin,
-                              uint32_t* flags, int sms, cudaStream_t s) {
-  (void)sms;
+                              uint32_t* flags, bool small_cells, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
   const int64_t m = (int64_t)L * ne;
   cudaError_t e = cudaMemsetAsync(scratch_same, 0, (size_t)C * sizeof(unsigned long long), s);
@@ -454,7 +521,19 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
   const long long init = 0x7fffffffffffffffll;
   e = cudaMemcpyAsync(bad_index, &init, sizeof(init), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
-  if (L > 1) {
+  const bool fast = small_cells && ne % 32 == 0 && 256 % ne == 0;
+  if (L > 1 && fast) {
+    const int64_t rows = (int64_t)(L - 1) * ne;
+    const int rows_per_cta = kEvalCellsPerCta / ne;
+    const int64_t ctas = (rows + rows_per_cta - 1) / rows_per_cta;
+    const int64_t span = (std::min<int64_t>(m, rows_per_cta + 2 * ne) + 15) & ~15ll;
+    const size_t smem = (size_t)kEvalCands * (size_t)span;
+    e = cudaFuncSetAttribute(eval_same_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    eval_same_fast_kernel<<<(unsigned)ctas, kEvalThreads, smem, s>>>(L, ne, E, cands, C, m, scratch_same);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  } else if (L > 1) {
     const int64_t nE = (int64_t)(L - 1) * ne * ne;
     const int64_t ctas = (nE + kEvalCellsPerCta - 1) / kEvalCellsPerCta;
     // staged span per candidate: rows of this CTA plus the next layer
@@ -477,6 +556,15 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256));
+  max_cell_kernel<<<grid, 256, 0, s>>>(E, n, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
@@ -515,11 +603,11 @@ cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uin
 cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M,
                                int32_t nM, int32_t anchor, const unsigned long long* keys,
                                int64_t n_keys, int32_t* out, uint8_t* out_u8, cudaStream_t s) {
-  const size_t smem = (size_t)L * g * 8 + (size_t)g * 4;
+  const size_t smem = (size_t)L * g * 8 + (size_t)((g + 1) & ~1) * 4 + (size_t)kGreedyKeyChunk * 8;
   cudaError_t e = cudaFuncSetAttribute(greedy_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  greedy_walk_kernel<<<1, 32, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
+  greedy_walk_kernel<<<1, 256, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
   return cudaGetLastError();
 }
 
