@@ -576,11 +576,25 @@ int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32
   uint32_t* bits = h->misc.as<uint32_t>();
   int32_t* dout = reinterpret_cast<int32_t*>(bits + (m + 31) / 32);
   int32_t* dn = dout + m;
-  GIMBAL_CUDA_TRY(launch_affinity_keys(L, ne, h->dE, threshold, h->keys.as<unsigned long long>(), n_pad,
-                                       h->dflags, h->stream));
-  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
-  GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, h->keys.as<unsigned long long>(), n, top_e, capacity, bits,
-                                         dout, dn, h->stream));
+  if (top_e >= 1 && top_e <= kTopkMax) {
+    // only the top_e heaviest pairs can survive truncation: segment top-K, no full sort
+    unsigned long long* ka = h->keys.as<unsigned long long>();
+    unsigned long long* kb = ka + n_pad / 2;
+    unsigned long long* sorted = nullptr;
+    if ((n + 2047) / 2048 * (int64_t)top_e > n_pad / 2) {
+      GIMBAL_TRY(h->keys.ensure((size_t)((n + 2047) / 2048 * (int64_t)top_e) * 16));
+      ka = h->keys.as<unsigned long long>();
+      kb = ka + (n + 2047) / 2048 * (int64_t)top_e;
+    }
+    GIMBAL_CUDA_TRY(launch_affinity_topk(L, ne, h->dE, threshold, top_e, ka, kb, h->dflags, &sorted, h->stream));
+    GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, sorted, top_e, top_e, capacity, bits, dout, dn, h->stream));
+  } else {
+    GIMBAL_CUDA_TRY(launch_affinity_keys(L, ne, h->dE, threshold, h->keys.as<unsigned long long>(), n_pad,
+                                         h->dflags, h->stream));
+    GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+    GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, h->keys.as<unsigned long long>(), n, top_e, capacity, bits,
+                                           dout, dn, h->stream));
+  }
   int32_t cnt = 0;
   GIMBAL_CUDA_TRY(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, h->stream));
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));

@@ -120,6 +120,10 @@ cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha
 cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E, double threshold,
                                  unsigned long long* keys, int64_t n_pad, uint32_t* flags,
                                  cudaStream_t s);
+cudaError_t launch_affinity_topk(int L, int ne, const unsigned long long* E, double threshold, int K,
+                                 unsigned long long* a, unsigned long long* b, uint32_t* flags,
+                                 unsigned long long** result, cudaStream_t s);
+constexpr int kTopkMax = 1024;  // top_e up to this uses segment top-K instead of a full sort
 cudaError_t launch_affinity_select(int L, int ne, const unsigned long long* sorted_keys,
                                    int64_t n_keys, int32_t top_e, int32_t capacity,
                                    uint32_t* member_bits, int32_t* out, int32_t* n_out,

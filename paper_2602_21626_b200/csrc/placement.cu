@@ -292,6 +292,49 @@ __global__ void affinity_keys_kernel(int L, int ne, const unsigned long long* __
   }
 }
 
+// Top-K selection for small top_e (placement.cpp:217-219 keeps only the top_e heaviest pairs):
+// each CTA sorts a 2048-key segment in shared memory (descending) and keeps its first K keys;
+// repeated until one segment remains.  FROM_E builds the composite keys from E on the fly.
+template <bool FROM_E>
+__global__ void __launch_bounds__(1024)
+    topk_segment_kernel(const unsigned long long* __restrict__ in, int64_t n, double threshold, int K,
+                        unsigned long long* __restrict__ out, uint32_t* __restrict__ flags) {
+  __shared__ unsigned long long s[kSortLocal];
+  const int64_t base = (int64_t)blockIdx.x * kSortLocal;
+  for (int i = threadIdx.x; i < kSortLocal; i += blockDim.x) {
+    const int64_t idx = base + i;
+    unsigned long long key = 0ull;
+    if (idx < n) {
+      if constexpr (FROM_E) {
+        const unsigned long long w = in[idx];
+        const double wd = (double)w;
+        if (wd >= threshold && wd > 0.0) {
+          if (w >= (1ull << 40)) atomicOr(flags, (uint32_t)kFlagOverflow);
+          key = (w << 24) | (unsigned long long)(0xffffffll - idx);
+        }
+      } else {
+        key = in[idx];
+      }
+    }
+    s[i] = key;
+  }
+  __syncthreads();
+  for (int k = 2; k <= kSortLocal; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < kSortLocal / 2; t += blockDim.x) {
+        const int i = 2 * j * (t / j) + (t % j);
+        const bool desc = ((i & k) == 0);
+        const unsigned long long a = s[i], b = s[i + j];
+        if (desc ? (a < b) : (a > b)) {
+          s[i] = b;
+          s[i + j] = a;
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < K; i += blockDim.x) out[(int64_t)blockIdx.x * K + i] = s[i];
+}
+
 // Sequential endpoint union over the sorted pairs (placement.cpp:221-237): the result is the
 // union of the longest prefix (<= kept pairs) whose union fits `capacity`.
 __global__ void affinity_select_kernel(int L, int ne, const unsigned long long* __restrict__ keys,
@@ -354,6 +397,7 @@ __global__ void greedy_keys_kernel(int64_t m, const unsigned long long* __restri
 
 constexpr int kGreedyKeyChunk = 8192;  // sorted keys staged per round (64 KB)
 
+template <int G>  // G = n_gpus when specialised, 0 = runtime
 __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
                                    const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
                                    const unsigned long long* __restrict__ keys, int64_t n_keys,
@@ -362,6 +406,7 @@ __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long lon
   int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
   const int64_t m = (int64_t)L * ne;
   const int cap = (int)(m / g);
+  const unsigned long long inv_ne = ((1ull << 40) + (unsigned long long)ne - 1) / (unsigned long long)ne;
   for (int64_t i = threadIdx.x; i < (int64_t)L * g; i += blockDim.x) load[i] = 0ull;
   for (int p = threadIdx.x; p < g; p += blockDim.x) counts[p] = 0;
   __syncthreads();
@@ -392,17 +437,33 @@ __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long lon
         }
         const int e = 0xffffff - (int)(key & 0xffffffull);
         const unsigned long long a = key >> 24;
-        const int layer = e / ne;
+        const int layer = (int)(((unsigned long long)e * inv_ne) >> 40);  // e / ne, exact for e < 2^24
         // home = first argmax row of the flat column: its layer if A > 0, else row 0
         const unsigned long long* lr = load + (a > 0 ? layer : 0) * g;
         int best = -1;
         unsigned long long bv = 0ull;
-        for (int p = 0; p < g; ++p) {  // placement.cpp:290-295: strict <, lowest p first
-          if (counts[p] >= cap) continue;
-          const unsigned long long v = lr[p];
-          if (best < 0 || v < bv) {
-            best = p;
-            bv = v;
+        if constexpr (G > 0) {
+          unsigned long long v[G];
+          int cn[G];
+#pragma unroll
+          for (int p = 0; p < G; ++p) {  // issue all shared loads before the compare chain
+            v[p] = lr[p];
+            cn[p] = counts[p];
+          }
+#pragma unroll
+          for (int p = 0; p < G; ++p)  // placement.cpp:290-295: strict <, lowest p first
+            if (cn[p] < cap && (best < 0 || v[p] < bv)) {
+              best = p;
+              bv = v[p];
+            }
+        } else {
+          for (int p = 0; p < g; ++p) {
+            if (counts[p] >= cap) continue;
+            const unsigned long long v = lr[p];
+            if (best < 0 || v < bv) {
+              best = p;
+              bv = v;
+            }
           }
         }
         out[e] = best;
@@ -583,6 +644,31 @@ cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E,
   return cudaGetLastError();
 }
 
+// Reduces (L-1)*ne^2 cells to the sorted top-K keys in `a`/`b` ping-pong buffers (each >=
+// ceil(n/2048)*K keys); returns the buffer holding the final sorted K keys.
+cudaError_t launch_affinity_topk(int L, int ne, const unsigned long long* E, double threshold, int K,
+                                 unsigned long long* a, unsigned long long* b, uint32_t* flags,
+                                 unsigned long long** result, cudaStream_t s) {
+  const int64_t n = (int64_t)(L - 1) * ne * ne;
+  int64_t blocks = (n + kSortLocal - 1) / kSortLocal;
+  topk_segment_kernel<true><<<(unsigned)blocks, 1024, 0, s>>>(E, n, threshold, K, a, flags);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int64_t cur = blocks * K;
+  unsigned long long* src = a;
+  unsigned long long* dst = b;
+  do {  // at least one pass so the survivors come out globally sorted
+    blocks = (cur + kSortLocal - 1) / kSortLocal;
+    topk_segment_kernel<false><<<(unsigned)blocks, 1024, 0, s>>>(src, cur, 0.0, K, dst, flags);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cur = blocks * K;
+    std::swap(src, dst);
+  } while (blocks > 1);
+  *result = src;
+  return cudaSuccess;
+}
+
 cudaError_t launch_affinity_select(int L, int ne, const unsigned long long* sorted_keys,
                                    int64_t n_keys, int32_t top_e, int32_t capacity,
                                    uint32_t* member_bits, int32_t* out, int32_t* n_out,
@@ -604,10 +690,11 @@ cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A
                                int32_t nM, int32_t anchor, const unsigned long long* keys,
                                int64_t n_keys, int32_t* out, uint8_t* out_u8, cudaStream_t s) {
   const size_t smem = (size_t)L * g * 8 + (size_t)((g + 1) & ~1) * 4 + (size_t)kGreedyKeyChunk * 8;
-  cudaError_t e = cudaFuncSetAttribute(greedy_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = g == 8 ? greedy_walk_kernel<8> : g == 4 ? greedy_walk_kernel<4> : g == 2 ? greedy_walk_kernel<2>
+            : g == 16 ? greedy_walk_kernel<16> : greedy_walk_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  greedy_walk_kernel<<<1, 256, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
+  kern<<<1, 256, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
   return cudaGetLastError();
 }
 
