@@ -30,6 +30,7 @@ constexpr int kEvalThreads = 256;
 constexpr int kEvalCellsPerThread = 32;             // E cells held in registers per thread
 constexpr int kEvalCands = 32;                      // candidates per CTA
 constexpr int kEvalCellsPerCta = kEvalThreads * kEvalCellsPerThread;
+constexpr int kSortLocal = 2048;  // keys per CTA in the shared-memory sort / top-K stages
 
 // ---- cut: same[c] += sum over this CTA's E cells of E(j,k) [P(j) == P(k')] ----
 // The CTA owns kEvalCellsPerCta consecutive cells of the flattened E (row r = flat expert
@@ -477,7 +478,6 @@ __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long lon
 }
 
 // ---- bitonic sort (descending) of u64 keys, n a power of two ----
-constexpr int kSortLocal = 2048;  // keys per CTA in the shared-memory stages
 
 __global__ void bitonic_local_kernel(unsigned long long* keys, int64_t n, int64_t k_start,
                                      int64_t k_end, bool full) {
