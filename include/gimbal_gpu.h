@@ -95,6 +95,10 @@ int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, vo
 int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens);
 /* Synchronises the handle's stream and returns sticky errors. */
 int gimbal_stats_sync(gimbal_stats_t h);
+/* Adds externally held counts into the handle: E [(L-1)][n_e][n_e] (or A [L][n_e] when L == 1)
+ * and their token count (host or device).  Restores a snapshot taken with gimbal_stats_read
+ * (checkpoint / resume of windowed statistics), copies a handle, or merges a peer's shard. */
+int gimbal_stats_merge(gimbal_stats_t h, const uint64_t* counts, int64_t tokens, int mem);
 
 /* ---- placement over the handle's statistics (placement.cpp:58-85, 186-331) ---- */
 

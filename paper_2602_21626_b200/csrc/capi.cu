@@ -465,6 +465,31 @@ int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, vo
   return GIMBAL_OK;
 }
 
+int gimbal_stats_merge(gimbal_stats_t h, const uint64_t* counts, int64_t tokens, int mem) {
+  GIMBAL_TRY(check_handle(h));
+  if (tokens < 0) return invalid("merge: negative token count");
+  if (!counts) return invalid("merge: null counts");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  const bool pairs = h->topo.n_layers > 1;
+  const int64_t n = pairs ? h->nE() : h->m();
+  unsigned long long* dst = pairs ? h->dE : h->dA;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(counts);
+  DevBuf tmp;
+  if (mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(tmp.ensure((size_t)n * 8));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(tmp.p, counts, (size_t)n * 8, cudaMemcpyHostToDevice, h->stream));
+    src = tmp.as<unsigned long long>();
+  }
+  GIMBAL_CUDA_TRY(launch_add_u64(dst, src, n, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  tmp.release();
+  h->tokens += tokens;
+  h->derived = !pairs;
+  h->max_tokens = -1;
+  return GIMBAL_OK;
+}
+
 int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
   GIMBAL_TRY(check_handle(h));
   if (global_tokens < 0) return invalid("mark_reduced: negative token count");

@@ -99,6 +99,7 @@ cudaError_t launch_derive_activation(int L, int ne, int k, const unsigned long l
                                      unsigned long long* A, cudaStream_t s);
 cudaError_t launch_derive_w(int L, int ne, const unsigned long long* E, unsigned long long* W,
                             cudaStream_t s);
+cudaError_t launch_add_u64(unsigned long long* dst, const unsigned long long* src, int64_t n, cudaStream_t s);
 cudaError_t launch_flat_forms(int L, int ne, const unsigned long long* A,
                               const unsigned long long* E, double* flatA, double* flatW,
                               cudaStream_t s);

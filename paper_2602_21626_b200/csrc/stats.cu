@@ -439,6 +439,19 @@ cudaError_t launch_derive_w(int L, int ne, const unsigned long long* E, unsigned
   return cudaGetLastError();
 }
 
+__global__ void add_u64_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src,
+                               int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+cudaError_t launch_add_u64(unsigned long long* dst, const unsigned long long* src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 1184, (n + 255) / 256));
+  add_u64_kernel<<<grid, 256, 0, s>>>(dst, src, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_flat_forms(int L, int ne, const unsigned long long* A,
                               const unsigned long long* E, double* flatA, double* flatW,
                               cudaStream_t s) {

@@ -60,6 +60,17 @@ def main():
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref_cases.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(CASES)} cases, {os.path.getsize(path)} bytes")
+    # byte-stable simulator reports of the reference over its own expert layer
+    # (oracle/sim_report_main.cpp linked with proj/src/{sim,moe,placement,...}.cpp)
+    import subprocess
+
+    sim = os.path.join(oracle.HERE, "_ref", "sim_report_ref")
+    for s in (0, 1, 2):
+        rep = subprocess.run([sim, str(s)], capture_output=True, text=True, check=True).stdout
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"sim_report_{s}.json")
+        with open(p, "w") as f:
+            f.write(rep)
+        print(f"wrote {p}: {len(rep)} bytes")
 
 
 if __name__ == "__main__":
