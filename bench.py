@@ -37,6 +37,13 @@ CONFIGS = {
              "DeepSeek-V3-shape trace (58 MoE layers, 256 experts, top-8), 64M tokens, 4096 candidate placements"),
 }
 METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
+# Measured on B200 by tools/microbench/atoms_bench.cu (profiles/r1_atoms_microbench.md): shared
+# atomic increments to random addresses of a 128 KB table, 148 CTAs x 1024 threads.
+ATOMS_RANDOM_PEAK = 2.553e12
+# dram__bytes_read.sum + dram__bytes_write.sum per counting launch from one `ncu --set full`
+# capture (profiles/r1_ncu_count_dsv3.md), bytes / launch, with the tokens of that launch.
+TRAFFIC = {"dsv3": {"bytes": 12.518227e9 + 23.87456e6, "tokens_in_launch": 8388608,
+                    "source": "profiles/r1_ncu_count_dsv3.md"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 REASON_BITS = {
@@ -137,7 +144,9 @@ def run_reference(args):
 
 
 def sample_size(config):
-    return {"mixtral": (1 << 16, 64), "dsv2lite": (1 << 15, 8), "qwen3": (1 << 13, 2), "dsv3": (1 << 12, 1)}[config]
+    # (tokens, candidates) of the bounded CPU sample: ~5-15 s of reference work on 16 cores;
+    # Mixtral runs in full
+    return {"mixtral": (1 << 20, 4096), "dsv2lite": (1 << 18, 32), "qwen3": (1 << 16, 8), "dsv3": (1 << 15, 2)}[config]
 
 
 def sample_inputs(config, T, C):
@@ -235,56 +244,56 @@ def main():
             return hp.run_distributed(trace, cands, c_lo, C)
         return hp.run(trace, cands)
 
-    # the dominant kernel's duration, measured live on the stream it is launched on
-    count_ev = []
-
-    def step_timed():
-        hp.stats.reset()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        hp.stats.add_tokens(trace)
-        e1.record(stream)
-        count_ev.append((e0, e1))
-        return hp.place(cands)
-
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # the dominant kernel's launches are timed live with CUDA events on the stream they run on
+    hp.stats.count_timing(True)
     clocks = ClockSampler(local).start() if rank == 0 else None
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for _ in range(args.steps):
-        res = step() if world > 1 else step_timed()
+        step()
     t1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
     clk = clocks.stop() if clocks else None
+    count_total_ms, count_launches = hp.stats.count_timing(False)
     if world > 1:
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     value = world * T / (ms * 1e-3)
 
-    # roofline of the dominant kernel (trace counting): algorithmic bytes per launch =
-    # trace bytes (T*L*k uint8) + one u64 write of E; duration from the live events above
-    count_ms = float(np.mean([a.elapsed_time(b) for a, b in count_ev])) if count_ev else None
-    alg_bytes = T * L * k + (L - 1) * ne * ne * 8
-    peak, peak_kind = peaks()
+    # roofline of the dominant kernel (E counting): algorithmic bytes per launch = the launch's
+    # trace bytes (tokens * L * k uint8) + one u64 write of E; duration = average launch time
     roof = None
-    if count_ms:
-        achieved = alg_bytes / (count_ms * 1e-3) / 1e9
+    if count_launches:
+        launch_ms = count_total_ms / count_launches
+        launches_per_step = count_launches / args.steps
+        tok_per_launch = T / launches_per_step
+        alg_bytes = tok_per_launch * L * k + (L - 1) * ne * ne * 8
+        peak, peak_kind = peaks()
+        achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+        upd = tok_per_launch * (L - 1) * k * k / (launch_ms * 1e-3)
+        split = ne * ne * 4 > 200 * 1024
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "count_pairs_kernel", "kernel_ms": count_ms,
-                "algorithmic_bytes": alg_bytes, "peak_source": peak_kind,
-                "e_pair_updates_per_s": T * (L - 1) * k * k / (count_ms * 1e-3),
-                "share_of_step": count_ms / ms}
+                "traffic": (TRAFFIC[args.config]["bytes"] / TRAFFIC[args.config]["tokens_in_launch"] * tok_per_launch
+                            if args.config in TRAFFIC else None),
+                "traffic_source": TRAFFIC.get(args.config, {}).get("source"),
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "kernel": "count_lm8_split_kernel" if split else "count_lm8_pairs_kernel",
+                "launch_ms": launch_ms, "launches_per_step": launches_per_step,
+                "algorithmic_bytes_per_launch": alg_bytes, "share_of_step": count_total_ms / args.steps / ms,
+                "atomic_ceiling": {"bound": "shared-memory atomics", "achieved": upd, "peak": ATOMS_RANDOM_PEAK,
+                                   "unit": "E pair-updates/s", "frac": upd / ATOMS_RANDOM_PEAK,
+                                   "peak_source": "profiles/r1_atoms_microbench.md (random-address ATOMS)"}}
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None

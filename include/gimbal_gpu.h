@@ -95,6 +95,10 @@ int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, vo
 int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens);
 /* Synchronises the handle's stream and returns sticky errors. */
 int gimbal_stats_sync(gimbal_stats_t h);
+/* Kernel timing of the trace-counting launches (CUDA events on the handle's stream around every
+ * counting kernel).  enable = 1 starts recording (clears totals), 0 stops; when count_ms /
+ * launches are non-NULL, synchronises and returns the summed device time and launch count. */
+int gimbal_stats_count_timing(gimbal_stats_t h, int enable, double* count_ms, int64_t* launches);
 /* Adds externally held counts into the handle: E [(L-1)][n_e][n_e] (or A [L][n_e] when L == 1)
  * and their token count (host or device).  Restores a snapshot taken with gimbal_stats_read
  * (checkpoint / resume of windowed statistics), copies a handle, or merges a peer's shard. */

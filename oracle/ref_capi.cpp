@@ -222,10 +222,10 @@ int ref_model_weights(int L, int ne, int k, int g, double zipf_s, double lambda,
 }
 
 // The reference CPU pipeline the bench times: add_token over a uint8 trace
-// (optionally sharded over n_threads RoutingStats, summed), affinity(), flat_activation(),
-// flat_pair_weights(), build_affinity_set, greedy_place, then eval_cost per candidate
+// (sharded over n_threads RoutingStats), then affinity(), flat_activation(),
+// flat_pair_weights(), build_affinity_set, greedy_place and eval_cost per candidate
 // ([C][m] uint8 GPU ids).  Returns per-stage wall seconds in t[0..3]
-// (stats, flat forms + affinity set + greedy, eval, total) and the argmin candidate.
+// (add_token, flat forms + affinity set + greedy, eval, total) and the argmin candidate.
 int ref_pipeline(int L, int ne, int k, int g, const std::uint8_t* ids, std::int64_t T,
                  int n_threads, const std::uint8_t* cands, int C, double threshold, int top_e,
                  int anchor, double alpha, double beta, double* objectives, std::int64_t* argmin,
@@ -251,18 +251,13 @@ int ref_pipeline(int L, int ne, int k, int g, const std::uint8_t* ids, std::int6
       }
       for (auto& th : pool) th.join();
     }
-    // sum the shards through the public API only: flat forms and affinity are linear in counts
+    auto t1 = clk::now();
+    // The public API has no way to merge RoutingStats, so the placement stages run once on the
+    // first shard (their cost does not depend on the token count; with n_threads == 1 the
+    // outputs are the reference's exact answers for the whole trace).
     auto aff = shards[0].affinity();
     Eigen::MatrixXd flatA = shards[0].flat_activation();
     Eigen::MatrixXd flatW = shards[0].flat_pair_weights();
-    for (int w = 1; w < n_threads; ++w) {
-      auto a2 = shards[static_cast<std::size_t>(w)].affinity();
-      for (std::size_t l = 0; l < aff.E.size(); ++l) aff.E[l] += a2.E[l];
-      aff.W += a2.W;
-      flatA += shards[static_cast<std::size_t>(w)].flat_activation();
-      flatW += shards[static_cast<std::size_t>(w)].flat_pair_weights();
-    }
-    auto t1 = clk::now();
     auto set = placement::build_affinity_set(aff, topo, threshold, top_e,
                                              topo.total_experts() / topo.n_gpus, anchor);
     auto greedy = placement::greedy_place(flatA, set, g);

@@ -128,6 +128,27 @@ struct gimbal_stats_s {
   cudaEvent_t ev_lm8_ready[kStages] = {nullptr, nullptr};
   cudaEvent_t ev_lm8_free[kStages] = {nullptr, nullptr};
   cudaEvent_t ev_order = nullptr;
+  // optional event pairs around each counting launch (gimbal_stats_count_timing)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+  size_t tev_used = 0;
+  int timing_begin() {
+    if (!timing) return GIMBAL_OK;
+    if (tev_used == tev.size()) {
+      cudaEvent_t a, b;
+      GIMBAL_CUDA_TRY(cudaEventCreate(&a));
+      GIMBAL_CUDA_TRY(cudaEventCreate(&b));
+      tev.emplace_back(a, b);
+    }
+    GIMBAL_CUDA_TRY(cudaEventRecord(tev[tev_used].first, stream));
+    return GIMBAL_OK;
+  }
+  int timing_end() {
+    if (!timing) return GIMBAL_OK;
+    GIMBAL_CUDA_TRY(cudaEventRecord(tev[tev_used].second, stream));
+    ++tev_used;
+    return GIMBAL_OK;
+  }
   // scratch
   DevBuf cand, same, dout, keys, misc, ints;
   std::mutex mu;
@@ -180,7 +201,9 @@ struct gimbal_stats_s {
       GIMBAL_CUDA_TRY(launch_transpose_lm8(ids + t0 * row, cnt, L, ne, k, lm8[b], lm8_tokens, dflags, t_stream));
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_ready[b], t_stream));
       GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_lm8_ready[b], 0));
+      GIMBAL_TRY(timing_begin());
       GIMBAL_CUDA_TRY(launch_count_lm8(lm8_plan, lm8[b], cnt, lm8_tokens, dE, stream));
+      GIMBAL_TRY(timing_end());
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_free[b], stream));
     }
     return GIMBAL_OK;
@@ -195,7 +218,9 @@ struct gimbal_stats_s {
       return count_lm8(static_cast<const uint8_t*>(ids), n);
     }
     if (L > 1) {
+      GIMBAL_TRY(timing_begin());
       GIMBAL_CUDA_TRY(launch_count_pairs(plan, ids, id_bytes, n, dE, dflags, stream));
+      GIMBAL_TRY(timing_end());
     } else {
       GIMBAL_CUDA_TRY(launch_count_activation(L, topo.n_experts, topo.top_k, ids, id_bytes, n, dA,
                                               dflags, stream));
@@ -350,6 +375,10 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_lm8_free[b]) cudaEventDestroy(h->ev_lm8_free[b]);
     }
     if (h->ev_order) cudaEventDestroy(h->ev_order);
+    for (auto& pr : h->tev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->t_stream) cudaStreamDestroy(h->t_stream);
@@ -462,6 +491,26 @@ int gimbal_stats_device_buffers(gimbal_stats_t h, uint64_t** E, uint64_t** A, vo
   if (E) *E = h->nE() > 0 ? reinterpret_cast<uint64_t*>(h->dE) : nullptr;
   if (A) *A = reinterpret_cast<uint64_t*>(h->dA);
   if (stream) *stream = h->stream;
+  return GIMBAL_OK;
+}
+
+int gimbal_stats_count_timing(gimbal_stats_t h, int enable, double* count_ms, int64_t* launches) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (count_ms || launches) {
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    double total = 0.0;
+    for (size_t i = 0; i < h->tev_used; ++i) {
+      float ms = 0.f;
+      GIMBAL_CUDA_TRY(cudaEventElapsedTime(&ms, h->tev[i].first, h->tev[i].second));
+      total += ms;
+    }
+    if (count_ms) *count_ms = total;
+    if (launches) *launches = (int64_t)h->tev_used;
+  }
+  if (enable != (h->timing ? 1 : 0) || enable) h->tev_used = 0;
+  h->timing = enable != 0;
   return GIMBAL_OK;
 }
 

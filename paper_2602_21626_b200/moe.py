@@ -206,6 +206,18 @@ class RoutingStats:
         N.check(N.lib().gimbal_stats_device_buffers(self._h, C.byref(e), C.byref(a), C.byref(s)), "buffers")
         return e.value, a.value, s.value
 
+    def count_timing(self, enable: bool = True):
+        """(device ms, launches) of the counting kernels since the last call; keeps recording
+        while ``enable``."""
+        ms, n = C.c_double(0.0), C.c_int64(0)
+        N.check(N.lib().gimbal_stats_count_timing(self._h, int(enable), C.byref(ms), C.byref(n)), "timing")
+        return ms.value, n.value
+
+    def merge(self, counts, tokens: int) -> None:
+        """Adds a snapshot of counts (E, or A when L == 1; host uint64) and its token total."""
+        a = np.ascontiguousarray(counts, np.uint64)
+        N.check(N.lib().gimbal_stats_merge(self._h, a.ctypes.data, int(tokens), N.MEM_HOST), "merge")
+
     def mark_reduced(self, global_tokens: int) -> None:
         N.check(N.lib().gimbal_stats_mark_reduced(self._h, int(global_tokens)), "mark_reduced")
 
