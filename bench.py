@@ -317,18 +317,21 @@ def main():
                        "parallelism": f"token-shard dp{world}",
                        "l2": f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": launches_per_step(topo) * args.steps,
+            "gpu_launches": kernel_launches_per_step(topo, count_launches / args.steps) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def launches_per_step(topo):
-    """Kernels of ours per step: memsets are not kernels; count_pairs 1, derive A 1, derive W 1,
-    affinity keys 1 + sort (local + global passes) + select 1, greedy keys 1 + sort + walk 1,
-    eval same 1 + dev 1 + finish 1."""
-    L, ne = topo.n_layers, topo.n_experts
+def kernel_launches_per_step(topo, count_launches_per_step, top_e=4):
+    """Our kernels per step (memsets/copies are not kernels): per ingest chunk one transposition
+    (layer-major path) + one counting launch (measured), derive A + derive W, max-cell, the
+    strong-pair set (segment top-K passes + select), greedy (keys + bitonic sort + walk) and the
+    evaluator (same + dev + finish)."""
+    L, ne, k = topo.n_layers, topo.n_experts, topo.top_k
+    lm8 = L > 1 and k <= 8 and ne <= 256
+    ingest = count_launches_per_step * (2 if lm8 else 1)
 
     def sort_launches(n):
         p = 1
@@ -336,18 +339,27 @@ def launches_per_step(topo):
             p <<= 1
         if p <= 2048:
             return 1
-        c = 1
-        k = 4096
-        while k <= p:
-            j = k // 2
+        c, kk = 1, 4096
+        while kk <= p:
+            j = kk // 2
             while j >= 2048:
                 c += 1
                 j //= 2
             c += 1
-            k *= 2
+            kk *= 2
         return c
 
-    return 3 + 2 + sort_launches((L - 1) * ne * ne) + 2 + sort_launches(L * ne) + 3
+    cells = (L - 1) * ne * ne
+    blocks = -(-cells // 2048)
+    topk = 1
+    cur = blocks * top_e
+    while True:
+        b = -(-cur // 2048)
+        topk += 1
+        cur = b * top_e
+        if b <= 1:
+            break
+    return int(round(ingest + 2 + 1 + topk + 1 + 1 + sort_launches(L * ne) + 1 + 3))
 
 
 def run_e2e(G, topo, trace, cands_host, T, args, local):
