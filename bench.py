@@ -42,7 +42,7 @@ METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
 ATOMS_RANDOM_PEAK = 2.553e12
 # dram__bytes_read.sum + dram__bytes_write.sum per counting launch from one `ncu --set full`
 # capture (profiles/r1_ncu_count_dsv3.md), bytes / launch, with the tokens of that launch.
-TRAFFIC = {"dsv3": {"bytes": 12.518227e9 + 23.87456e6, "tokens_in_launch": 8388608,
+TRAFFIC = {"dsv3": {"bytes": 13.992643e9 + 20.467712e6, "tokens_in_launch": 9256395,
                     "source": "profiles/r1_ncu_count_dsv3.md"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
