@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <random>
 #include <string>
@@ -121,6 +122,7 @@ struct gimbal_stats_s {
   // layer-major ingest buffers (ingest.cu)
   static constexpr int64_t kLm8BufferBytes = (int64_t)4 << 30;
   Lm8Plan lm8_plan;
+  bool use_mma = false;  // tcgen05 contraction instead of shared-memory counting (n_e <= 128)
   cudaStream_t t_stream = nullptr;
   unsigned long long* lm8[kStages] = {nullptr, nullptr};
   int64_t lm8_tokens = 0;
@@ -202,7 +204,11 @@ struct gimbal_stats_s {
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_ready[b], t_stream));
       GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_lm8_ready[b], 0));
       GIMBAL_TRY(timing_begin());
-      GIMBAL_CUDA_TRY(launch_count_lm8(lm8_plan, lm8[b], cnt, lm8_tokens, dE, stream));
+      if (use_mma) {
+        GIMBAL_CUDA_TRY(launch_count_mma(L, ne, k, sms, lm8[b], cnt, lm8_tokens, dE, stream));
+      } else {
+        GIMBAL_CUDA_TRY(launch_count_lm8(lm8_plan, lm8[b], cnt, lm8_tokens, dE, stream));
+      }
       GIMBAL_TRY(timing_end());
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_free[b], stream));
     }
@@ -320,6 +326,12 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
     return st;
   };
   h->lm8_plan = make_lm8_plan(topo->n_layers, topo->n_experts, topo->top_k, h->sms, optin);
+  {
+    // GIMBAL_COUNT_PATH=atomic|mma overrides the default (tensor cores where supported)
+    const char* path = std::getenv("GIMBAL_COUNT_PATH");
+    const bool want_mma = !(path && std::string(path) == "atomic");
+    h->use_mma = want_mma && mma_count_supported(topo->n_layers, topo->n_experts, topo->top_k);
+  }
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->t_stream, cudaStreamNonBlocking) != cudaSuccess ||

@@ -91,6 +91,11 @@ cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne,
 cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, int64_t T, int64_t ld,
                              unsigned long long* E, cudaStream_t s);
 
+// tcgen05 int8 multi-hot contraction (mma_count.cu), n_e in [32, 128], top_k <= 8, on LM8 input.
+bool mma_count_supported(int L, int ne, int k);
+cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
+                             unsigned long long* E, cudaStream_t s);
+
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_count_activation(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,

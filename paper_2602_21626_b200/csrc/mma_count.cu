@@ -1,0 +1,266 @@
+// Transition counting on the 5th-generation tensor cores (tcgen05, kind::i8) for n_e <= 128.
+//
+// E_l = X_l^T X_{l+1}, where X_l is the T x n_e multi-hot matrix of layer l's routing choices
+// (X_l(t, e) = number of slots of token t at layer l that chose e).  Every product of the
+// reference's k x k pairing loop (moe.cpp:179-188) is one term of this contraction, multiplicity
+// included, so the integer result is exactly the reference's E.
+//
+// Per CTA work unit = (group of P <= 4 consecutive layer pairs, token range).  For each tile of
+// 128 tokens the CTA builds the P+1 layer tiles as u8 operands in shared memory, laid out
+// MN-major (a token's 128 expert indicators contiguous, the canonical no-swizzle UMMA layout:
+// core matrix = 16 experts x 8 tokens = 128 B), one elected thread issues
+// tcgen05.mma.cta_group::1.kind::i8 (M = 128 experts j, N = 128 experts k, K = 32 tokens) into a
+// per-pair s32 accumulator in tensor memory (4 x 128 of the 512 TMEM columns), and
+// tcgen05.commit releases the stage through an mbarrier while the other stage is being built.
+// At the end of the unit the accumulators are read back with tcgen05.ld and added to the u64 E.
+//
+// Dense work is n_e^2 MACs per token-pair against k^2 useful ones: 64x at Qwen3's 128 experts /
+// top-8 and 114x at DS-V2-Lite's 64 / top-6, which the int8 tensor rate (~7.7 K MAC/clk/SM)
+// absorbs with the shared-memory tile construction as the co-bottleneck.  At 256 experts the
+// ratio is 1024x and the shared-memory counting kernels (ingest.cu) win instead.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+
+constexpr int kTok = 128;                  // tokens per tile (MMA K, 4 instructions of 32)
+constexpr int kRows = 128;                 // experts per tile row block (MMA M, N <= 128)
+constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
+constexpr int kMaxPairs = 4;               // accumulators: 4 x 128 TMEM columns
+constexpr int kStages = 2;
+constexpr int kThreads = 256;
+constexpr int kStageBytes = (kMaxPairs + 1) * kTileBytes;
+
+struct MmaParams {
+  int L, ne, N;      // N = MMA n (n_e rounded up to 16)
+  int P;             // pairs per group
+  int n_groups;
+  int64_t n_units;
+  int64_t range_tokens;  // tokens per unit
+  int64_t T, ld;
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// Shared-memory matrix descriptor: no swizzle, MN-major.  Core matrix = 8 K-rows of 16 bytes;
+// K-groups (8 tokens) are LBO = 1024 B apart, MN-groups (16 experts) SBO = 128 B apart.
+__device__ __forceinline__ uint64_t operand_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fffu);
+  d |= (uint64_t)((1024u >> 4) & 0x3fffu) << 16;  // leading byte offset (K direction)
+  d |= (uint64_t)((128u >> 4) & 0x3fffu) << 32;   // stride byte offset (MN direction)
+  d |= (uint64_t)1 << 46;                          // descriptor version 1 (sm_100)
+  return d;                                        // base offset 0, layout SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 1)
+    count_mma_kernel(MmaParams prm, const unsigned long long* __restrict__ X, unsigned long long* __restrict__ E) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bars[kStages + 1];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s <= kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  const int ne = prm.ne;
+  uint32_t it_global = 0;        // tiles issued by this CTA (stage = it % 2, commit index = it / 2)
+  uint32_t final_waits = 0;      // commits of the end-of-unit barrier
+  for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
+    const int group = (int)(unit % prm.n_groups);
+    const int64_t range = unit / prm.n_groups;
+    const int l0 = group * prm.P;
+    const int np = min(prm.P, prm.L - 1 - l0);
+    const int64_t t_begin = range * prm.range_tokens;
+    const int64_t t_end = min(prm.T, t_begin + prm.range_tokens);
+    const int n_tiles = (int)((t_end - t_begin + kTok - 1) / kTok);
+    for (int it = 0; it < n_tiles; ++it, ++it_global) {
+      const int s = it_global & 1;
+      if (it_global >= kStages) mbar_wait(&bars[s], ((it_global >> 1) - 1) & 1);
+      uint8_t* stage = smem + s * kStageBytes;
+      const int64_t t0 = t_begin + (int64_t)it * kTok;
+      // Build np+1 layer tiles.  Block b = (layer q, K-group g of 8 tokens) is 1 KB contiguous;
+      // warps own whole blocks: zero it, then set each token's expert bytes.
+      const int n_blocks = (np + 1) * (kTok / 8);
+      for (int b = warp; b < n_blocks; b += kThreads / 32) {
+        const int q = b / (kTok / 8), g = b - q * (kTok / 8);
+        uint8_t* blk = stage + q * kTileBytes + g * 1024;
+        const int tt = lane & 7;
+        const int64_t t = t0 + g * 8 + tt;
+        const unsigned long long w = t < t_end ? __ldcs(X + (int64_t)(l0 + q) * prm.ld + t) : 0ull;
+        uint4 z = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(blk)[lane] = z;
+        reinterpret_cast<uint4*>(blk)[lane + 32] = z;
+        __syncwarp();
+        if (t < t_end) {
+#pragma unroll
+          for (int a = lane >> 3; a < K; a += 4) {
+            const uint32_t e = (uint32_t)(w >> (8 * a)) & 0xffu;
+            // byte (t, e) = (e / 16) * SBO + (t % 8) * 16 + e % 16 within the K-group block;
+            // repeated ids accumulate (multiplicity), so add instead of store
+            uint8_t* p = blk + (e >> 4) * 128 + tt * 16 + (e & 15);
+            atomicAdd(reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)),
+                      1u << (8 * (reinterpret_cast<uintptr_t>(p) & 3)));
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = smem_u32(stage);
+        for (int p = 0; p < np; ++p) {
+#pragma unroll
+          for (int kk = 0; kk < kTok / 32; ++kk) {
+            const uint64_t a = operand_desc(base + p * kTileBytes + kk * 4 * 1024);
+            const uint64_t bdesc = operand_desc(base + (p + 1) * kTileBytes + kk * 4 * 1024);
+            mma_i8(tmem + p * kRows, a, bdesc, prm.idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          }
+        }
+        mma_commit(&bars[s]);
+      }
+    }
+    // all MMAs of this unit complete -> read the accumulators
+    if (threadIdx.x == 0) mma_commit(&bars[kStages]);
+    mbar_wait(&bars[kStages], final_waits & 1);
+    ++final_waits;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp < 4) {
+      const int j = warp * 32 + lane;  // accumulator row = TMEM lane = expert j of layer l
+      for (int p = 0; p < np; ++p) {
+        for (int c0 = 0; c0 < prm.N; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(p * kRows + c0), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (j < ne) {
+            unsigned long long* row = E + ((int64_t)(l0 + p) * ne + j) * ne;
+#pragma unroll
+            for (int c = 0; c < 16; ++c)
+              if (v[c] != 0u && c0 + c < ne) atomicAdd(row + c0 + c, (unsigned long long)v[c]);
+          }
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+  }
+  // drain: every commit on the stage barriers has been waited for except the last one per stage
+  if (it_global >= 1) mbar_wait(&bars[(it_global - 1) & 1], ((it_global - 1) >> 1) & 1);
+  if (it_global >= 2) mbar_wait(&bars[(it_global - 2) & 1], ((it_global - 2) >> 1) & 1);
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int K>
+cudaError_t launch_k(const MmaParams& prm, const unsigned long long* X, unsigned long long* E, cudaStream_t s,
+                     int grid) {
+  auto kern = count_mma_kernel<K>;
+  const int smem = kStages * kStageBytes;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, smem, s>>>(prm, X, E);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool mma_count_supported(int L, int ne, int k) { return L > 1 && k >= 1 && k <= 8 && ne >= 32 && ne <= 128; }
+
+cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
+                             unsigned long long* E, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  MmaParams prm;
+  prm.L = L;
+  prm.ne = ne;
+  prm.N = (ne + 15) / 16 * 16;
+  prm.P = kMaxPairs;
+  prm.n_groups = (L - 1 + prm.P - 1) / prm.P;
+  prm.T = T;
+  prm.ld = ld;
+  // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
+  prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+  // one unit per CTA: token ranges so that groups x ranges fills the SMs; s32 accumulators hold
+  // per-unit counts up to tokens * k^2 < 2^31
+  int64_t ranges = std::max<int64_t>(1, sms / prm.n_groups);
+  const int64_t cap = ((int64_t)1 << 31) / ((int64_t)k * k) - kTok;
+  int64_t per = (T + ranges - 1) / ranges;
+  if (per > cap) per = cap;
+  per = (per + kTok - 1) / kTok * kTok;
+  ranges = (T + per - 1) / per;
+  prm.range_tokens = per;
+  prm.n_units = ranges * prm.n_groups;
+  const int grid = (int)std::min<int64_t>(prm.n_units, sms);
+  switch (k) {
+    case 1: return launch_k<1>(prm, X, E, s, grid);
+    case 2: return launch_k<2>(prm, X, E, s, grid);
+    case 3: return launch_k<3>(prm, X, E, s, grid);
+    case 4: return launch_k<4>(prm, X, E, s, grid);
+    case 5: return launch_k<5>(prm, X, E, s, grid);
+    case 6: return launch_k<6>(prm, X, E, s, grid);
+    case 7: return launch_k<7>(prm, X, E, s, grid);
+    case 8: return launch_k<8>(prm, X, E, s, grid);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace gimbal_gpu
