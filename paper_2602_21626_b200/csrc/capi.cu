@@ -182,7 +182,9 @@ struct gimbal_stats_s {
     const int L = topo.n_layers, ne = topo.n_experts, k = topo.top_k;
     const int64_t per_token = (int64_t)L * 8;
     const int64_t cap_tokens = std::max<int64_t>(1, kLm8BufferBytes / per_token);
-    const int64_t ch = std::min<int64_t>(n, cap_tokens);
+    // row stride (tokens) a multiple of 16 so every layer row is 16-byte aligned for TMA bulk
+    // copies; 64 B of slack for the rounded-up tail copy of the last row
+    const int64_t ch = (std::min<int64_t>(n, cap_tokens) + 15) / 16 * 16;
     if (ch > lm8_tokens) {
       for (int b = 0; b < kStages; ++b) {
         if (lm8[b]) {
@@ -190,7 +192,7 @@ struct gimbal_stats_s {
           cudaFree(lm8[b]);
           lm8[b] = nullptr;
         }
-        GIMBAL_CUDA_TRY(cudaMalloc(&lm8[b], (size_t)ch * per_token));
+        GIMBAL_CUDA_TRY(cudaMalloc(&lm8[b], (size_t)ch * per_token + 64));
       }
       lm8_tokens = ch;
     }

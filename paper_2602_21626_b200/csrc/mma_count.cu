@@ -34,7 +34,10 @@ constexpr int kRows = 128;                 // experts per tile row block (MMA M,
 constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
 constexpr int kMaxPairs = 4;               // accumulators: 4 x 128 TMEM columns
 constexpr int kStages = 2;
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
+constexpr int kIdSlots = 3;                                 // TMA ring of LM8 word tiles
+constexpr int kIdSlotWords = (kMaxPairs + 1) * kTok;        // 5 layers x 128 tokens
+constexpr int kSmemBytes = kStages * (kMaxPairs + 1) * kTileBytes + kIdSlots * kIdSlotWords * 8;
 constexpr int kStageBytes = (kMaxPairs + 1) * kTileBytes;
 
 struct MmaParams {
@@ -104,8 +107,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     count_mma_kernel(MmaParams prm, const unsigned long long* __restrict__ X, unsigned long long* __restrict__ E) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kStages + 1];
+  __shared__ uint64_t id_bars[kIdSlots];
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* ids = reinterpret_cast<unsigned long long*>(smem + kStages * kStageBytes);
+  uint32_t fill_count = 0;  // id-ring fills issued (identical in every thread)
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
@@ -114,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s <= kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kIdSlots; ++s) mbar_init(&id_bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -132,33 +139,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t t_begin = range * prm.range_tokens;
     const int64_t t_end = min(prm.T, t_begin + prm.range_tokens);
     const int n_tiles = (int)((t_end - t_begin + kTok - 1) / kTok);
+    const int n_rows = (np + 1) * kTok;  // token-layer rows per tile
+    // The LM8 words of a tile (np+1 layers x 128 tokens, 1 KB contiguous per layer) arrive by TMA
+    // bulk copies into a 3-slot ring, two tiles ahead of construction.
+    auto fetch = [&](int it) {
+      const uint32_t slot = fill_count % kIdSlots;
+      if (threadIdx.x == 0) {
+        const int64_t t0 = t_begin + (int64_t)it * kTok;
+        const uint32_t bytes = (uint32_t)(((min((int64_t)kTok, t_end - t0) * 8) + 15) & ~15ll);
+        const uint32_t bar = smem_u32(&id_bars[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * (np + 1))
+                     : "memory");
+        for (int q = 0; q <= np; ++q) {
+          const unsigned long long* src = X + (int64_t)(l0 + q) * prm.ld + t0;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(ids + slot * kIdSlotWords + q * kTok)),
+                       "l"(src), "r"(bytes), "r"(bar)
+                       : "memory");
+        }
+      }
+      ++fill_count;
+    };
+    fetch(0);
+    if (n_tiles > 1) fetch(1);
     for (int it = 0; it < n_tiles; ++it, ++it_global) {
+      if (it + 2 < n_tiles) fetch(it + 2);
+      const uint32_t use = fill_count - (uint32_t)min(2, n_tiles - 1 - it) - 1;  // fill index of tile it
+      mbar_wait(&id_bars[use % kIdSlots], (use / kIdSlots) & 1);
+      const unsigned long long* w_tile = ids + (use % kIdSlots) * kIdSlotWords;
       const int s = it_global & 1;
       if (it_global >= kStages) mbar_wait(&bars[s], ((it_global >> 1) - 1) & 1);
       uint8_t* stage = smem + s * kStageBytes;
       const int64_t t0 = t_begin + (int64_t)it * kTok;
-      // Build np+1 layer tiles.  Block b = (layer q, K-group g of 8 tokens) is 1 KB contiguous;
-      // warps own whole blocks: zero it, then set each token's expert bytes.
-      const int n_blocks = (np + 1) * (kTok / 8);
-      for (int b = warp; b < n_blocks; b += kThreads / 32) {
-        const int q = b / (kTok / 8), g = b - q * (kTok / 8);
-        uint8_t* blk = stage + q * kTileBytes + g * 1024;
-        const int tt = lane & 7;
-        const int64_t t = t0 + g * 8 + tt;
-        const unsigned long long w = t < t_end ? __ldcs(X + (int64_t)(l0 + q) * prm.ld + t) : 0ull;
-        uint4 z = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4*>(blk)[lane] = z;
-        reinterpret_cast<uint4*>(blk)[lane + 32] = z;
-        __syncwarp();
-        if (t < t_end) {
+      // one thread per token-layer row: zero its 128 expert bytes (8 chunks, SBO apart), then
+      // count its ids (read-modify-write keeps repeated ids' multiplicity)
+      for (int r = threadIdx.x; r < n_rows; r += kThreads) {
+        const int q = r / kTok, tt = r - q * kTok;
+        uint8_t* row = stage + q * kTileBytes + (tt >> 3) * 1024 + (tt & 7) * 16;
+        const uint4 z = make_uint4(0, 0, 0, 0);
 #pragma unroll
-          for (int a = lane >> 3; a < K; a += 4) {
+        for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(row + c * 128) = z;
+        if (t0 + tt < t_end) {
+          const unsigned long long w = w_tile[q * kTok + tt];
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
             const uint32_t e = (uint32_t)(w >> (8 * a)) & 0xffu;
-            // byte (t, e) = (e / 16) * SBO + (t % 8) * 16 + e % 16 within the K-group block;
-            // repeated ids accumulate (multiplicity), so add instead of store
-            uint8_t* p = blk + (e >> 4) * 128 + tt * 16 + (e & 15);
-            atomicAdd(reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(3)),
-                      1u << (8 * (reinterpret_cast<uintptr_t>(p) & 3)));
+            uint8_t* p = row + (e >> 4) * 128 + (e & 15);
+            *p = (uint8_t)(*p + 1);
           }
         }
       }
@@ -215,7 +242,7 @@ template <int K>
 cudaError_t launch_k(const MmaParams& prm, const unsigned long long* X, unsigned long long* E, cudaStream_t s,
                      int grid) {
   auto kern = count_mma_kernel<K>;
-  const int smem = kStages * kStageBytes;
+  const int smem = kSmemBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, s>>>(prm, X, E);
