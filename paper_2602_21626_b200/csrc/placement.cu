@@ -70,8 +70,11 @@ __global__ void __launch_bounds__(kEvalThreads)
   }
   __shared__ unsigned long long red[kEvalThreads / 32][kEvalCands];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t c0 = 0; c0 < C; c0 += kEvalCands) {
-    const int nc = (int)min((int64_t)kEvalCands, C - c0);
+  // grid.y splits the candidates so small E tensors still fill the machine
+  const int64_t per_y = ((C + gridDim.y - 1) / gridDim.y + kEvalCands - 1) / kEvalCands * kEvalCands;
+  const int64_t c_end = min(C, (int64_t)(blockIdx.y + 1) * per_y);
+  for (int64_t c0 = (int64_t)blockIdx.y * per_y; c0 < c_end; c0 += kEvalCands) {
+    const int nc = (int)min((int64_t)kEvalCands, c_end - c0);
     __syncthreads();
     for (int idx = threadIdx.x; idx < nc * span; idx += blockDim.x) {
       const int c = idx / span, o = idx - c * span;
@@ -122,8 +125,11 @@ __global__ void __launch_bounds__(kEvalThreads)
   const bool active = rg < n_rows;
   __shared__ unsigned long long red[kEvalThreads / 32][kEvalCands];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t c0 = 0; c0 < C; c0 += kEvalCands) {
-    const int nc = (int)min((int64_t)kEvalCands, C - c0);
+  // grid.y splits the candidates so small E tensors still fill the machine
+  const int64_t per_y = ((C + gridDim.y - 1) / gridDim.y + kEvalCands - 1) / kEvalCands * kEvalCands;
+  const int64_t c_end = min(C, (int64_t)(blockIdx.y + 1) * per_y);
+  for (int64_t c0 = (int64_t)blockIdx.y * per_y; c0 < c_end; c0 += kEvalCands) {
+    const int nc = (int)min((int64_t)kEvalCands, c_end - c0);
     const int live = (int)(span_hi - r0);
     __syncthreads();
     for (int idx = threadIdx.x; idx < nc * live; idx += blockDim.x) {
@@ -568,6 +574,13 @@ size_t eval_scratch_bytes(int64_t C) {
   return (size_t)C * sizeof(unsigned long long) + sizeof(long long) * 2;
 }
 
+// Candidate slices per cell block: at least ~4 CTAs per SM in total, at most one per 32 candidates.
+static unsigned candidate_splits(int64_t cell_ctas, int64_t C) {
+  const int64_t want = (4 * 148 + cell_ctas - 1) / cell_ctas;
+  const int64_t most = (C + kEvalCands - 1) / kEvalCands;
+  return (unsigned)std::max<int64_t>(1, std::min(want, most));
+}
+
 cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
                               const unsigned long long* E, const uint8_t* cands, int64_t C,
                               double alpha, double beta, unsigned long long* scratch_same,
@@ -591,7 +604,8 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     const size_t smem = (size_t)kEvalCands * (size_t)span;
     e = cudaFuncSetAttribute(eval_same_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    eval_same_fast_kernel<<<(unsigned)ctas, kEvalThreads, smem, s>>>(L, ne, E, cands, C, m, scratch_same);
+    eval_same_fast_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
+        L, ne, E, cands, C, m, scratch_same);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   } else if (L > 1) {
@@ -603,7 +617,8 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     e = cudaFuncSetAttribute(eval_same_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    eval_same_kernel<<<(unsigned)ctas, kEvalThreads, smem, s>>>(L, ne, E, cands, C, m, scratch_same);
+    eval_same_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
+        L, ne, E, cands, C, m, scratch_same);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
