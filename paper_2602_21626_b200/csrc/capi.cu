@@ -207,7 +207,7 @@ struct gimbal_stats_s {
       GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_lm8_ready[b], 0));
       GIMBAL_TRY(timing_begin());
       if (use_mma) {
-        GIMBAL_CUDA_TRY(launch_count_mma(L, ne, k, sms, lm8[b], cnt, lm8_tokens, dE, stream));
+        GIMBAL_CUDA_TRY(launch_count_mma(L, ne, k, sms, lm8[b], cnt, lm8_tokens, dE, dflags, stream));
       } else {
         GIMBAL_CUDA_TRY(launch_count_lm8(lm8_plan, lm8[b], cnt, lm8_tokens, dE, stream));
       }

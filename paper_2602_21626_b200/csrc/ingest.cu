@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "internal.cuh"
 
@@ -53,20 +55,30 @@ __global__ void __launch_bounds__(256)
   }
   __syncthreads();
   bool bad = false;
+  int dup = 0;
   for (int idx = threadIdx.x; idx < L * kTransposeTile; idx += blockDim.x) {
     const int l = idx / kTransposeTile, i = idx - l * kTransposeTile;
     if (i >= n) continue;
     const uint8_t* p = tile + i * row + l * K;
     unsigned long long w = 0;
+    uint32_t e_[K];
 #pragma unroll
     for (int a = 0; a < K; ++a) {
       const uint32_t e = p[a];
+      e_[a] = e;
       bad |= e >= (uint32_t)ne;
       w |= (unsigned long long)e << (8 * a);
     }
+#pragma unroll
+    for (int a = 0; a < K; ++a)
+#pragma unroll
+      for (int b = a + 1; b < K; ++b) dup |= e_[a] == e_[b];
     X[(int64_t)l * ld + t0 + i] = w;
   }
   if (bad) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
+  // repeated ids within a token-layer (legal, counted with multiplicity) disable the
+  // one-count-per-cell fast paths of the counting kernels
+  if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagDuplicates);
 }
 
 struct Lm8Params {
@@ -128,6 +140,63 @@ __global__ void __launch_bounds__(1024, 1)
       const int j = r / ne;
       const int kk = (r - j * ne) ^ (j & prm.swz);
       atomicAdd(E + ((int64_t)(l0 + pr) * ne + j) * ne + kk, (unsigned long long)v);
+    }
+    __syncthreads();
+  }
+}
+
+// One whole layer pair per unit with 15-bit counters, two per 32-bit word (k even: bits 0-14,
+// k odd: bits 16-30; bits 15 and 31 are guards), so a 256 x 256 pair fits in 128 KB and no row
+// filter is needed.  An increment that carries a half into its guard bit (the half held 0x7FFF)
+// is detected from the atomic's return value: that thread moves 32768 to the u64 tensor and
+// clears the guard, so counts never wrap and never carry into the neighbour.
+template <int K>
+__global__ void __launch_bounds__(1024, 1)
+    count_lm8_u15_kernel(Lm8Params prm, const unsigned long long* __restrict__ X,
+                         unsigned long long* __restrict__ E) {
+  extern __shared__ uint32_t cnt[];
+  const int ne = prm.ne;
+  const int wpr = ne >> 1;  // words per row
+  const int pairs = prm.L - 1;
+  for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
+    const int64_t chunk = unit / pairs;
+    const int l = (int)(unit - chunk * pairs);
+    for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) cnt[w] = 0u;
+    __syncthreads();
+    const int64_t t_begin = chunk * prm.chunk_tokens;
+    const int64_t t_end = min(prm.T, t_begin + prm.chunk_tokens);
+    const unsigned long long* Xl = X + (int64_t)l * prm.ld;
+    const unsigned long long* Xn = Xl + prm.ld;
+    unsigned long long* El = E + (int64_t)l * ne * ne;
+    for (int64_t t = t_begin + threadIdx.x; t < t_end; t += blockDim.x) {
+      const unsigned long long cur = __ldcs(Xl + t);
+      const unsigned long long nxt = __ldcs(Xn + t);
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const uint32_t j = id_of(cur, a);
+        uint32_t* rowp = cnt + j * wpr;
+        const uint32_t sw = j & 31u;
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          const uint32_t k = id_of(nxt, b);
+          const uint32_t shift = (k & 1u) << 4;
+          const uint32_t old = atomicAdd(rowp + ((k >> 1) ^ sw), 1u << shift);
+          if (((old >> shift) & 0x7fffu) == 0x7fffu) {  // this increment filled the half
+            atomicSub(rowp + ((k >> 1) ^ sw), 0x8000u << shift);
+            atomicAdd(El + (int64_t)j * ne + k, 32768ull);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) {
+      const uint32_t v = cnt[w];
+      if (v == 0u) continue;
+      const int j = w / wpr;
+      const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+      unsigned long long* rowE = El + (int64_t)j * ne;
+      if (v & 0xffffu) atomicAdd(rowE + k0, (unsigned long long)(v & 0xffffu));
+      if (v >> 16) atomicAdd(rowE + k0 + 1, (unsigned long long)(v >> 16));
     }
     __syncthreads();
   }
@@ -225,7 +294,13 @@ cudaError_t launch_transpose_k(const uint8_t* trace, int64_t T, int L, int ne, u
 template <int K>
 cudaError_t launch_count_k(const Lm8Plan& plan, const Lm8Params& prm, const unsigned long long* X,
                            unsigned long long* E, cudaStream_t s, int grid) {
-  if (plan.split) {
+  if (plan.u15) {
+    auto kern = count_lm8_u15_kernel<K>;
+    const size_t smem = (size_t)plan.ne * plan.ne * 2;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 1024, smem, s>>>(prm, X, E);
+  } else if (plan.split) {
     auto kern = count_lm8_split_kernel<K>;
     const size_t smem = (size_t)plan.R * plan.ne * 4 + (size_t)kSplitWarps * kBatch * 8 +
                         (size_t)kSplitWarps * kBatch * K * 2;
@@ -266,6 +341,13 @@ Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin) {
     const int ng = (pairs + p.P - 1) / p.P;
     p.P = (pairs + ng - 1) / ng;
     p.n_groups = (pairs + p.P - 1) / p.P;
+  } else if (ne % 64 == 0 && ne * ne * 2 <= budget && !(std::getenv("GIMBAL_COUNT_PATH") &&
+                                                         std::string(std::getenv("GIMBAL_COUNT_PATH")) == "split")) {
+    p.u15 = true;
+    p.P = 1;
+    p.R = ne;
+    p.n_parts = 1;
+    p.n_groups = pairs;
   } else {
     p.split = true;
     p.P = 1;
@@ -311,7 +393,9 @@ cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, i
   const int64_t base_units = (int64_t)plan.n_groups * plan.n_parts;
   const int64_t resident = plan.sms;
   // ~4 waves of units for load balance (hot rows make units uneven), at least 16K tokens each
-  int64_t n_chunks = std::max<int64_t>(1, (4 * resident + base_units - 1) / base_units);
+  // u15 units are whole pairs with no flush pressure: more, smaller units balance hot pairs
+  const int64_t waves = plan.u15 ? 8 : 4;
+  int64_t n_chunks = std::max<int64_t>(1, (waves * resident + base_units - 1) / base_units);
   n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
   prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
   n_chunks = (T + prm.chunk_tokens - 1) / prm.chunk_tokens;

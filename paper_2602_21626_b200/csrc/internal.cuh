@@ -24,6 +24,7 @@ enum KernelFlag : uint32_t {
   kFlagIdOutOfRange = 1u,
   kFlagInfeasible = 2u,
   kFlagOverflow = 4u,
+  kFlagDuplicates = 8u,  // not an error: some token-layer repeats an id (multiplicity > 1)
 };
 
 #define GIMBAL_CUDA_TRY(expr)                                                          \
@@ -82,6 +83,7 @@ StatsPlan make_stats_plan(int L, int ne, int k, int sms, int max_smem_optin);
 struct Lm8Plan {
   int L = 0, ne = 0, k = 0, sms = 148;
   bool split = false;  // rows of one pair split over units (with warp compaction)
+  bool u15 = false;    // whole pair with guarded 15-bit counters (n_e^2 * 2 B fits, n_e % 64 == 0)
   int P = 1, R = 0, n_groups = 0, n_parts = 1;
 };
 bool lm8_supported(int L, int ne, int k, int id_bytes);
@@ -94,7 +96,7 @@ cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, i
 // tcgen05 int8 multi-hot contraction (mma_count.cu), n_e in [32, 128], top_k <= 8, on LM8 input.
 bool mma_count_supported(int L, int ne, int k);
 cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
-                             unsigned long long* E, cudaStream_t s);
+                             unsigned long long* E, const uint32_t* flags, cudaStream_t s);
 
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);

@@ -48,6 +48,7 @@ struct MmaParams {
   int64_t range_tokens;  // tokens per unit
   int64_t T, ld;
   uint32_t idesc;
+  const uint32_t* flags;  // kFlagDuplicates set by the transposition of this chunk
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   const int ne = prm.ne;
+  const bool dup = (*prm.flags & kFlagDuplicates) != 0;  // repeated ids: count, else set
   uint32_t it_global = 0;        // tiles issued by this CTA (stage = it % 2, commit index = it / 2)
   uint32_t final_waits = 0;      // commits of the end-of-unit barrier
   for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < K; ++a) {
             const uint32_t e = (uint32_t)(w >> (8 * a)) & 0xffu;
             uint8_t* p = row + (e >> 4) * 128 + (e & 15);
-            *p = (uint8_t)(*p + 1);
+            *p = dup ? (uint8_t)(*p + 1) : (uint8_t)1;
           }
         }
       }
@@ -254,7 +256,7 @@ cudaError_t launch_k(const MmaParams& prm, const unsigned long long* X, unsigned
 bool mma_count_supported(int L, int ne, int k) { return L > 1 && k >= 1 && k <= 8 && ne >= 32 && ne <= 128; }
 
 cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
-                             unsigned long long* E, cudaStream_t s) {
+                             unsigned long long* E, const uint32_t* flags, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   MmaParams prm;
   prm.L = L;
@@ -264,6 +266,7 @@ cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long 
   prm.n_groups = (L - 1 + prm.P - 1) / prm.P;
   prm.T = T;
   prm.ld = ld;
+  prm.flags = flags;
   // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
   prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
   // one unit per CTA: token ranges so that groups x ranges fills the SMs; s32 accumulators hold

@@ -86,6 +86,27 @@ def test_stats_odd_shapes(G, orc, L, ne, k):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+@pytest.mark.parametrize("dup", [False, True])
+def test_counter_overflow_paths(G, dup):
+    """Hot cells far beyond 2^15 / 2^16 per work unit (guarded 15-bit counters at n_e = 256,
+    s32 tensor-core accumulators at n_e = 128): 1 Mi identical tokens, with and without
+    repeated ids (multiplicity 64 per token-pair)."""
+    for (L, ne, k, g) in (SHAPES["dsv3"], SHAPES["qwen3"]):
+        topo = G.MoeTopology(L, ne, k, g)
+        T = 1 << 20
+        row = np.full((L, k), 3, np.uint8) if dup else np.tile(np.arange(k, dtype=np.uint8) * 5, (L, 1))
+        trace = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(row, (T, L, k)))).cuda()
+        s = G.RoutingStats(topo, 0)
+        s.add_tokens(trace)
+        A, E, W = s.read()
+        want = np.zeros((L - 1, ne, ne), np.uint64)
+        for a in range(k):
+            for b in range(k):
+                want[:, row[0, a], row[1, b]] += T
+        assert np.array_equal(E, want)
+        assert (A.sum(axis=1) == T * k).all()
+
+
 def test_zero_tokens(G):
     topo = G.MoeTopology(3, 4, 2, 2)
     s = G.RoutingStats(topo, 0)
