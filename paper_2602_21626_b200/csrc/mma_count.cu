@@ -253,7 +253,10 @@ cudaError_t launch_k(const MmaParams& prm, const unsigned long long* X, unsigned
 
 }  // namespace
 
-bool mma_count_supported(int L, int ne, int k) { return L > 1 && k >= 1 && k <= 8 && ne >= 32 && ne <= 128; }
+// Measured on B200 (profiles/r1_summary.md): the contraction beats shared-memory counting at
+// n_e = 128 (Qwen3: 1.07 vs 1.28 ns/token) but not at n_e = 64 (DS-V2-Lite: 0.54 vs 0.45 ns),
+// where the 128-row operand tiles are half padding.
+bool mma_count_supported(int L, int ne, int k) { return L > 1 && k >= 1 && k <= 8 && ne > 64 && ne <= 128; }
 
 cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
                              unsigned long long* E, const uint32_t* flags, cudaStream_t s) {
