@@ -176,14 +176,24 @@ __global__ void __launch_bounds__(1024, 1)
         const uint32_t j = id_of(cur, a);
         uint32_t* rowp = cnt + j * wpr;
         const uint32_t sw = j & 31u;
+        uint32_t old[K];
+        bool full = false;
 #pragma unroll
         for (int b = 0; b < K; ++b) {
           const uint32_t k = id_of(nxt, b);
           const uint32_t shift = (k & 1u) << 4;
-          const uint32_t old = atomicAdd(rowp + ((k >> 1) ^ sw), 1u << shift);
-          if (((old >> shift) & 0x7fffu) == 0x7fffu) {  // this increment filled the half
-            atomicSub(rowp + ((k >> 1) ^ sw), 0x8000u << shift);
-            atomicAdd(El + (int64_t)j * ne + k, 32768ull);
+          old[b] = atomicAdd(rowp + ((k >> 1) ^ sw), 1u << shift);
+          full |= ((old[b] >> shift) & 0x7fffu) == 0x7fffu;  // this increment filled the half
+        }
+        if (full) {  // rare: one branch per row instead of one per increment
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+            const uint32_t k = id_of(nxt, b);
+            const uint32_t shift = (k & 1u) << 4;
+            if (((old[b] >> shift) & 0x7fffu) == 0x7fffu) {
+              atomicSub(rowp + ((k >> 1) ^ sw), 0x8000u << shift);
+              atomicAdd(El + (int64_t)j * ne + k, 32768ull);
+            }
           }
         }
       }
