@@ -197,12 +197,16 @@ struct gimbal_stats_s {
       lm8_tokens = ch;
     }
     const int64_t row = (int64_t)L * k;
-    for (int64_t t0 = 0; t0 < n; t0 += ch) {
+    // the first transposition cannot overlap counting: keep that chunk short (1/8 of a buffer)
+    const int64_t first = n > ch ? std::max<int64_t>(16, (ch / 8 + 15) / 16 * 16) : ch;
+    for (int64_t t0 = 0; t0 < n;) {
       const int b = lm8_next;
       lm8_next ^= 1;
-      const int64_t cnt = std::min<int64_t>(ch, n - t0);
+      const int64_t cnt = std::min<int64_t>(t0 == 0 ? first : ch, n - t0);
+      const int64_t t_this = t0;
+      t0 += cnt;
       GIMBAL_CUDA_TRY(cudaStreamWaitEvent(t_stream, ev_lm8_free[b], 0));
-      GIMBAL_CUDA_TRY(launch_transpose_lm8(ids + t0 * row, cnt, L, ne, k, lm8[b], lm8_tokens, dflags, t_stream));
+      GIMBAL_CUDA_TRY(launch_transpose_lm8(ids + t_this * row, cnt, L, ne, k, lm8[b], lm8_tokens, dflags, t_stream));
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_lm8_ready[b], t_stream));
       GIMBAL_CUDA_TRY(cudaStreamWaitEvent(stream, ev_lm8_ready[b], 0));
       GIMBAL_TRY(timing_begin());

@@ -132,6 +132,14 @@ __global__ void __launch_bounds__(kEvalThreads)
     const int nc = (int)min((int64_t)kEvalCands, c_end - c0);
     const int live = (int)(span_hi - r0);
     __syncthreads();
+    if (((reinterpret_cast<uintptr_t>(cands) | (uintptr_t)m | (uintptr_t)r0 | (uintptr_t)live) & 3) == 0) {
+      const int live4 = live >> 2;  // stage 4 GPU ids per load
+      for (int idx = threadIdx.x; idx < nc * live4; idx += blockDim.x) {
+        const int c = idx / live4, o = idx - c * live4;
+        reinterpret_cast<uint32_t*>(sm + c * span)[o] =
+            __ldg(reinterpret_cast<const uint32_t*>(cands + (c0 + c) * m + r0) + o);
+      }
+    } else
     for (int idx = threadIdx.x; idx < nc * live; idx += blockDim.x) {
       const int c = idx / live, o = idx - c * live;
       sm[c * span + o] = cands[(c0 + c) * m + r0 + o];
