@@ -35,7 +35,13 @@ CONFIGS = {
     "qwen3": (48, 128, 8, 8, 32 << 20, 4096, "Qwen3-30B-A3B-shape trace (48 layers, 128 experts, top-8), 32M tokens"),
     "dsv3": (58, 256, 8, 8, 64 << 20, 4096,
              "DeepSeek-V3-shape trace (58 MoE layers, 256 experts, top-8), 64M tokens, 4096 candidate placements"),
+    "stream": (58, 256, 8, 8, 64 << 20, 256,
+               "streaming windowed re-placement: DeepSeek-V3 shape, 64 tumbling windows of 1Mi tokens, drifting "
+               "hotspots (5% of each layer's Zipf ranks re-drawn per window), fixed strong-pair set from a "
+               "calibration window, per-window stats + greedy + 256 scored candidates"),
 }
+STREAM_WINDOW = 1 << 20
+STREAM_DRIFT = 0.05
 METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
 # Measured on B200 by tools/microbench/atoms_bench.cu (profiles/r1_atoms_microbench.md): shared
 # atomic increments to random addresses of a 128 KB table, 148 CTAs x 1024 threads.
@@ -146,7 +152,8 @@ def run_reference(args):
 def sample_size(config):
     # (tokens, candidates) of the bounded CPU sample: ~5-15 s of reference work on 16 cores;
     # Mixtral runs in full
-    return {"mixtral": (1 << 20, 4096), "dsv2lite": (1 << 18, 32), "qwen3": (1 << 16, 8), "dsv3": (1 << 15, 2)}[config]
+    return {"mixtral": (1 << 20, 4096), "dsv2lite": (1 << 18, 32), "qwen3": (1 << 16, 8), "dsv3": (1 << 15, 2),
+            "stream": (1 << 15, 2)}[config]
 
 
 def sample_inputs(config, T, C):
@@ -230,6 +237,9 @@ def main():
     topo = G.MoeTopology(L, ne, k, g)
     m = topo.total_experts()
     dev = torch.device("cuda", local)
+
+    if args.config == "stream":
+        return run_stream(args, G, topo, world, rank, local, T, C, desc)
 
     # inputs resident in HBM: this rank's token shard (tokens rank*T .. (rank+1)*T of one stream)
     trace = G.generate_trace(topo, T, model_seed=1, stream_seed=2, first_token=rank * T, device=local)
@@ -360,6 +370,78 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4):
         if b <= 1:
             break
     return int(round(ingest + 2 + 1 + topk + 1 + 1 + sort_launches(L * ne) + 1 + 3))
+
+
+def run_stream(args, G, topo, world, rank, local, T, C, desc):
+    """BASELINE configs[4]: one step = the whole stream of T / STREAM_WINDOW tumbling windows.
+    Window w is generated with drift epoch w (STREAM_DRIFT of each layer's Zipf rank permutation
+    re-drawn per window); each rank holds its 1/N token shard of every window (weak in windows'
+    token rate: per-GPU shard fixed), E is all-reduced per window for N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21626_b200.pipeline import shard_range
+
+    L, k, g, m = topo.n_layers, topo.top_k, topo.n_gpus, topo.total_experts()
+    n_win = T // STREAM_WINDOW
+    per_rank = STREAM_WINDOW  # each rank counts a full window-sized shard: N x tokens per window
+    windows = []
+    for w in range(n_win):
+        windows.append(G.generate_trace(topo, per_rank, model_seed=1, stream_seed=2,
+                                        first_token=(w * world + rank) * per_rank, drift=STREAM_DRIFT,
+                                        drift_epoch=w + 1, device=local))
+    calib = G.generate_trace(topo, 20000, model_seed=1, stream_seed=3, first_token=0, drift=STREAM_DRIFT,
+                             drift_epoch=0, device=local)  # offline_tokens default (sim.hpp:41)
+    c_lo, c_hi = shard_range(C, rank, world)
+    cands = torch.from_numpy(G.shuffled_candidates(m, g, 1000 + c_lo, c_hi - c_lo)).to(f"cuda:{local}")
+    hp = G.HotPath(topo, device=local)
+    M = hp.calibrate(calib)
+    stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", local))
+
+    def step():
+        if world > 1:
+            return hp.stream_distributed(windows, cands, c_lo, C, M)
+        return hp.stream(windows, cands, M)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    clk = clocks.stop() if clocks else None
+    if world > 1:
+        tt = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens = world * per_rank * n_win
+    if rank == 0:
+        moved = [r[1] for r in res]
+        line = {
+            "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
+            "data": "synthetic (drifting Zipf RoutingModel-semantics windows generated on the GPU)",
+            "config": {"workload": desc, "windows": n_win, "window_tokens_per_gpu": per_rank, "candidates": C, "g": g,
+                       "parallelism": f"token-shard dp{world} per window",
+                       "strong_pair_set": M.experts, "mean_moved_per_window": float(np.mean(moved[1:])) if len(moved) > 1
+                       else None},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "clocks": clk,
+            "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_e2e(G, topo, trace, cands_host, T, args, local):

@@ -109,15 +109,66 @@ class HotPath:
         out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
         return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
 
+    def place_with(self, M: AffinitySet, candidates, greedy_row: bool = True) -> HotPathResult:
+        """Stats already counted, strong-pair set fixed (sim.cpp:94-104 computes M once from a
+        calibration pass and keeps it): greedy -> scores -> argmin."""
+        gp = greedy_place(self.stats, M, self.topo.n_gpus, out_u8_device=candidates[0] if greedy_row else None)
+        out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
+        return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
+
     def run(self, trace, candidates, greedy_row: bool = True) -> HotPathResult:
         """One full pass over a trace (CUDA uint8 [T][L][k] or host array)."""
         self.stats.reset()
         self.stats.add_tokens(trace)
         return self.place(candidates, greedy_row)
 
+    def calibrate(self, trace) -> AffinitySet:
+        """Offline calibration (sim.cpp:91-106): stats over a calibration trace -> strong-pair set."""
+        self.stats.reset()
+        self.stats.add_tokens(trace)
+        topo = self.topo
+        return build_affinity_set(self.stats, topo, self.threshold, self.top_e,
+                                  topo.total_experts() // topo.n_gpus, self.anchor_gpu)
+
+    def stream(self, windows, candidates, M: AffinitySet, previous=None):
+        """Tumbling-window re-placement (config 5; sim.cpp:149-165 semantics per window: the window
+        is counted from zero, greedy re-places with the fixed anchor set, all candidates are
+        scored, and `moved` counts experts whose GPU changed against the previous choice).
+        ``windows``: iterable of CUDA uint8 [T_w][L][k] traces.  Returns per-window
+        (argmin, moved, greedy placement)."""
+        out = []
+        prev = previous
+        for w in windows:
+            self.stats.reset()
+            self.stats.add_tokens(w)
+            res = self.place_with(M, candidates)
+            moved = (sum(1 for a, b in zip(prev, res.greedy) if a != b) if prev is not None
+                     and len(prev) == len(res.greedy) else len(res.greedy))
+            out.append((res.argmin, moved, res.greedy))
+            prev = res.greedy
+        return out
+
+    def stream_distributed(self, window_shards, candidates_shard, cand_offset: int, n_candidates: int,
+                           M: AffinitySet, group=None, previous=None):
+        """stream() with each window's tokens sharded over ranks: count the shard, all-reduce E,
+        re-place with the fixed M, score this rank's candidate slice, merge the argmin."""
+        out = []
+        prev = previous
+        for w in window_shards:
+            res = self._distributed_pass(w, candidates_shard, cand_offset, n_candidates, group, M)
+            moved = (sum(1 for a, b in zip(prev, res.greedy) if a != b) if prev is not None
+                     and len(prev) == len(res.greedy) else len(res.greedy))
+            out.append((res.argmin, moved, res.greedy))
+            prev = res.greedy
+        return out
+
     def run_distributed(self, trace_shard, candidates_shard, cand_offset: int, n_candidates: int,
                         group=None) -> HotPathResult:
         """This rank's token shard and candidate slice; returns the global argmin."""
+        return self._distributed_pass(trace_shard, candidates_shard, cand_offset, n_candidates, group, None)
+
+    def _distributed_pass(self, trace_shard, candidates_shard, cand_offset: int, n_candidates: int,
+                          group=None, M_fixed=None) -> HotPathResult:
         import torch
         import torch.distributed as dist
 
@@ -125,11 +176,10 @@ class HotPath:
         self.stats.add_tokens(trace_shard)
         allreduce_counts(self.stats, group)
         topo = self.topo
-        M = build_affinity_set(self.stats, topo, self.threshold, self.top_e,
-                               topo.total_experts() // topo.n_gpus, self.anchor_gpu)
+        M = M_fixed if M_fixed is not None else build_affinity_set(
+            self.stats, topo, self.threshold, self.top_e, topo.total_experts() // topo.n_gpus, self.anchor_gpu)
         gp = greedy_place(self.stats, M, topo.n_gpus,
                           out_u8_device=candidates_shard[0] if cand_offset == 0 else None)
-        world = dist.get_world_size(group)
         n_local = candidates_shard.shape[0]
         dev = torch.device("cuda", self.device)
         local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
@@ -143,6 +193,5 @@ class HotPath:
             host = local.cpu()
             dist.all_reduce(host, op=dist.ReduceOp.MIN, group=group)
             objs = host.numpy()
-        del world
         return HotPathResult(affinity=M, greedy=gp.assign, argmin=merge_argmin(objs),
                              objective=float(objs.min()) if objs.size else None)
