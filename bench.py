@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--candidates", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="use the multi-rank code path (NCCL all-reduce, candidate split) even with one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -227,7 +229,8 @@ def main():
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    dist_on = world > 1 or args.dist_path
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L, ne, k, g, T, C, desc = CONFIGS[args.config]
     if args.tokens:
@@ -250,7 +253,7 @@ def main():
     stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=dev)
 
     def step():
-        if world > 1:
+        if dist_on:
             return hp.run_distributed(trace, cands, c_lo, C)
         return hp.run(trace, cands)
 
@@ -399,7 +402,7 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
     stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", local))
 
     def step():
-        if world > 1:
+        if world > 1 or args.dist_path:
             return hp.stream_distributed(windows, cands, c_lo, C, M)
         return hp.stream(windows, cands, M)
 

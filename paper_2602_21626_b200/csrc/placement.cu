@@ -438,12 +438,73 @@ __global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long lon
   // The walk is inherently sequential (each choice reads the loads the previous ones wrote), so
   // one thread walks while the CTA stages the sorted keys through shared memory ahead of it.
   unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(counts + ((g + 1) & ~1));
+  int gcnt[G > 0 ? G : 1];  // per-GPU cardinalities (thread 0, specialised walk)
+#pragma unroll
+  for (int p = 0; p < (G > 0 ? G : 1); ++p) gcnt[p] = G > 0 ? counts[p] : 0;
   bool done = false;
   for (int64_t base = 0; base < n_keys && !done; base += kGreedyKeyChunk) {
     const int nk = (int)min((int64_t)kGreedyKeyChunk, n_keys - base);
     for (int i = threadIdx.x; i < nk; i += blockDim.x) kbuf[i] = keys[base + i];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if constexpr (G > 0) {
+      // Pipelined walk: the next expert's home-row loads are issued before the current decision
+      // and patched if the current placement lands in that row, so steps do not serialise on
+      // the shared-memory store -> load round trip.  GPU cardinalities live in registers.
+      if (threadIdx.x == 0) {
+        auto decode = [&](unsigned long long key, int& e, unsigned long long& a, int& layer, int& row) {
+          e = 0xffffff - (int)(key & 0xffffffull);
+          a = key >> 24;
+          layer = (int)(((unsigned long long)e * inv_ne) >> 40);  // e / ne, exact for e < 2^24
+          row = a > 0 ? layer : 0;  // first argmax row of the flat column (row 0 if all zero)
+        };
+        unsigned long long key = nk > 0 ? kbuf[0] : 0ull;
+        int e = 0, layer = 0, row = 0;
+        unsigned long long a = 0ull;
+        unsigned long long v[G];
+        if (key != 0ull) {
+          decode(key, e, a, layer, row);
+#pragma unroll
+          for (int p = 0; p < G; ++p) v[p] = load[row * G + p];
+        }
+        for (int i = 0; i < nk; ++i) {
+          if (key == 0ull) {
+            done = true;
+            break;
+          }
+          const unsigned long long key_n = i + 1 < nk ? kbuf[i + 1] : 0ull;
+          int e_n = 0, layer_n = 0, row_n = 0;
+          unsigned long long a_n = 0ull, v_n[G];
+          if (key_n != 0ull) {
+            decode(key_n, e_n, a_n, layer_n, row_n);
+#pragma unroll
+            for (int p = 0; p < G; ++p) v_n[p] = load[row_n * G + p];
+          }
+          int best = -1;
+          unsigned long long bv = 0ull;
+#pragma unroll
+          for (int p = 0; p < G; ++p)  // placement.cpp:290-295: strict <, lowest p first
+            if (gcnt[p] < cap && (best < 0 || v[p] < bv)) {
+              best = p;
+              bv = v[p];
+            }
+          out[e] = best;
+          if (out_u8) out_u8[e] = (uint8_t)best;
+          load[layer * G + best] += a;
+#pragma unroll
+          for (int p = 0; p < G; ++p) {
+            gcnt[p] += (p == best);
+            if (row_n == layer) v_n[p] += (p == best) ? a : 0ull;  // forward the pending update
+          }
+          key = key_n;
+          e = e_n;
+          a = a_n;
+          layer = layer_n;
+          row = row_n;
+#pragma unroll
+          for (int p = 0; p < G; ++p) v[p] = v_n[p];
+        }
+      }
+    } else if (threadIdx.x == 0) {
       for (int i = 0; i < nk; ++i) {
         const unsigned long long key = kbuf[i];
         if (key == 0ull) {
