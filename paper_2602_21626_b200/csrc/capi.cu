@@ -733,7 +733,7 @@ int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t 
   const int64_t n_pad = next_pow2(m);
   GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
   const size_t words = bits.size();
-  GIMBAL_TRY(h->ints.ensure(words * 4 + (size_t)std::max(nM, 1) * 4 + (size_t)m * 4 + 64));
+  GIMBAL_TRY(h->ints.ensure(words * 4 + (size_t)std::max(nM, 1) * 4 + (size_t)m * 4 + (size_t)m + 64));
   uint32_t* dbits = h->ints.as<uint32_t>();
   int32_t* dM = reinterpret_cast<int32_t*>(dbits + words);
   int32_t* dres = dM + std::max(nM, 1);
@@ -743,8 +743,9 @@ int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t 
   GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, dbits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
                                      h->stream));
   GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+  uint8_t* tent = reinterpret_cast<uint8_t*>(dM + std::max(nM, 1) + m);  // per-position scratch
   GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, dM, nM, anchor, h->keys.as<unsigned long long>(),
-                                     m, dres, out_u8, h->stream));
+                                     m, dres, out_u8, tent, h->stream));
   if (out && out_mem != GIMBAL_MEM_DEVICE)
     GIMBAL_CUDA_TRY(cudaMemcpyAsync(out, dres, (size_t)m * 4, cudaMemcpyDeviceToHost, h->stream));
   return h->check_flags();

@@ -1,0 +1,220 @@
+// greedy_place (placement.cpp:240-299, paper Alg. 3) on the compact flat activation, sm_100a.
+//
+// The reference walks the unanchored experts in (-total, id) order and puts each on the GPU with
+// headroom whose load in the expert's home row is lowest (strict <, lowest GPU first), then adds
+// the expert's activation column to that GPU.  On the flat activation an expert of layer l with
+// A > 0 has home row l and only changes row l; an expert with A = 0 (home row 0) changes nothing
+// and sorts after every positive expert.  So until some GPU reaches its cardinality cap m/g, the
+// walk decomposes into independent per-layer walks.  The kernel therefore
+//   A. runs every layer's walk in parallel (one thread per layer, loads in registers) ignoring
+//      the cap, recording each position's tentative GPU;
+//   B. finds s*, the first position in the global order whose tentative GPU would already be full
+//      (warp ballots over the running per-GPU counts);
+//   C. rebuilds the loads/counts at s* and finishes positions >= s* (including all A = 0 experts)
+//      with the exact sequential walk.
+// Positions before s* are provably identical to the sequential walk; the tail is exact by
+// construction, so the result is the reference's placement for every input.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxLayers = kThreads;  // layer-parallel phase needs one thread per layer
+
+__device__ __forceinline__ int key_expert(unsigned long long key) { return 0xffffff - (int)(key & 0xffffffull); }
+__device__ __forceinline__ unsigned long long key_total(unsigned long long key) { return key >> 24; }
+
+template <int G>
+__device__ __forceinline__ int argmin_first(const unsigned long long (&v)[G], const int (&cnt)[G], int cap) {
+  int best = -1;
+  unsigned long long bv = 0ull;
+#pragma unroll
+  for (int p = 0; p < G; ++p)
+    if (cnt[p] < cap && (best < 0 || v[p] < bv)) {
+      best = p;
+      bv = v[p];
+    }
+  return best;
+}
+
+// Sequential tail: positions [start, n_valid) with shared loads/counts (placement.cpp:286-297).
+__device__ void sequential_walk(int g, int cap, const unsigned long long* __restrict__ keys, int64_t start,
+                                int64_t n_valid, unsigned long long inv_ne, unsigned long long* load, int* counts,
+                                int32_t* __restrict__ out, uint8_t* __restrict__ out_u8) {
+  for (int64_t i = start; i < n_valid; ++i) {
+    const unsigned long long key = keys[i];
+    const int e = key_expert(key);
+    const unsigned long long a = key_total(key);
+    const int layer = (int)(((unsigned long long)e * inv_ne) >> 40);
+    const unsigned long long* lr = load + (a > 0 ? layer : 0) * g;
+    int best = -1;
+    unsigned long long bv = 0ull;
+    for (int p = 0; p < g; ++p) {
+      if (counts[p] >= cap) continue;
+      if (best < 0 || lr[p] < bv) {
+        best = p;
+        bv = lr[p];
+      }
+    }
+    out[e] = best;
+    if (out_u8) out_u8[e] = (uint8_t)best;
+    load[layer * g + best] += a;
+    counts[best] += 1;
+  }
+}
+
+template <int G>  // G = n_gpus (<= 32) for the layer-parallel path; 0 = fully sequential
+__global__ void __launch_bounds__(kThreads)
+    greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
+                       const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
+                       const unsigned long long* __restrict__ keys, int64_t n_keys, int32_t* __restrict__ out,
+                       uint8_t* __restrict__ out_u8, uint8_t* __restrict__ tent) {
+  extern __shared__ unsigned long long load[];  // [L][g] loads, then counts [g]
+  int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
+  __shared__ long long s_nvalid, s_npos, s_star;
+  const int64_t m = (int64_t)L * ne;
+  const int cap = (int)(m / g);
+  const unsigned long long inv_ne = ((1ull << 40) + (unsigned long long)ne - 1) / (unsigned long long)ne;
+  for (int64_t i = threadIdx.x; i < (int64_t)L * g; i += blockDim.x) load[i] = 0ull;
+  for (int p = threadIdx.x; p < g; p += blockDim.x) counts[p] = 0;
+  if (threadIdx.x == 0) {
+    s_nvalid = n_keys;
+    s_npos = n_keys;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nM; ++i) {  // placement.cpp:272-279: the strong-pair set on the anchor
+      const int e = M[i];
+      out[e] = anchor;
+      if (out_u8) out_u8[e] = (uint8_t)anchor;
+      load[(int64_t)(e / ne) * g + anchor] += A[e];
+      counts[anchor] += 1;
+    }
+  }
+  // boundaries of the sorted keys: [0, n_pos) positive totals, [n_pos, n_valid) zero totals
+  for (int64_t i = threadIdx.x; i < n_keys; i += blockDim.x) {
+    const unsigned long long k0 = keys[i];
+    const unsigned long long k1 = i + 1 < n_keys ? keys[i + 1] : 0ull;
+    if (k0 != 0ull && k1 == 0ull) s_nvalid = i + 1;
+    if (key_total(k0) > 0 && key_total(k1) == 0) s_npos = i + 1;
+    if (i == 0 && key_total(k0) == 0) s_npos = 0;
+    if (i == 0 && k0 == 0ull) s_nvalid = 0;
+  }
+  __syncthreads();
+  const int64_t n_valid = s_nvalid;
+  const int64_t n_pos = min((int64_t)s_npos, n_valid);
+
+  if constexpr (G > 0) {
+    // ---- A: per-layer walks, cap ignored (one thread per layer, its load row in registers) ----
+    if (threadIdx.x < L) {
+      const int l = threadIdx.x;
+      unsigned long long v[G];
+#pragma unroll
+      for (int p = 0; p < G; ++p) v[p] = load[l * G + p];
+      for (int64_t i = 0; i < n_pos; ++i) {
+        const unsigned long long key = __ldg(keys + i);  // same address across the warp: broadcast
+        const int e = key_expert(key);
+        if ((int)(((unsigned long long)e * inv_ne) >> 40) != l) continue;
+        int best = 0;
+#pragma unroll
+        for (int p = 1; p < G; ++p)
+          if (v[p] < v[best]) best = p;
+#pragma unroll
+        for (int p = 0; p < G; ++p) v[p] += (p == best) ? key_total(key) : 0ull;
+        tent[i] = (uint8_t)best;
+      }
+    }
+    __syncthreads();
+    // ---- B: first position whose tentative GPU is already at its cap ----
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int room = lane < G ? cap - counts[lane] : 0;  // lane p tracks GPU p's remaining headroom
+      long long star = n_pos;
+      for (int64_t base = 0; base < n_pos; base += 32) {
+        const int64_t i = base + lane;
+        const int p = i < n_pos ? tent[i] : -1;
+        int used_before = 0;  // earlier positions of this chunk on the same GPU
+        int taken = 0;        // lane q: positions of this chunk on GPU q
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          const unsigned b = __ballot_sync(0xffffffffu, p == q);
+          if (p == q) used_before = __popc(b & ((1u << lane) - 1u));
+          if (lane == q) taken = __popc(b);
+        }
+        const int room_p = __shfl_sync(0xffffffffu, room, p < 0 ? 0 : p);
+        const unsigned vb = __ballot_sync(0xffffffffu, p >= 0 && used_before >= room_p);
+        if (vb) {  // the earliest position whose GPU would already hold cap experts
+          star = base + __ffs(vb) - 1;
+          break;
+        }
+        room -= taken;
+      }
+      if (lane == 0) s_star = star;
+    }
+    __syncthreads();
+    const int64_t star = s_star;
+    // ---- C: state at s*: loads from each layer's positions < s*, counts from all of them ----
+    if (threadIdx.x < L) {
+      const int l = threadIdx.x;
+      unsigned long long v[G];
+#pragma unroll
+      for (int p = 0; p < G; ++p) v[p] = load[l * G + p];
+      int c[G];
+#pragma unroll
+      for (int p = 0; p < G; ++p) c[p] = 0;
+      for (int64_t i = 0; i < star; ++i) {
+        const unsigned long long key = __ldg(keys + i);
+        const int e = key_expert(key);
+        if ((int)(((unsigned long long)e * inv_ne) >> 40) != l) continue;
+        const int p = tent[i];
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+          v[q] += (q == p) ? key_total(key) : 0ull;
+          c[q] += (q == p);
+        }
+        out[e] = p;
+        if (out_u8) out_u8[e] = (uint8_t)p;
+      }
+#pragma unroll
+      for (int p = 0; p < G; ++p) {
+        load[l * G + p] = v[p];
+        atomicAdd(&counts[p], c[p]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sequential_walk(g, cap, keys, star, n_valid, inv_ne, load, counts, out, out_u8);
+  } else {
+    (void)tent;
+    __syncthreads();
+    if (threadIdx.x == 0) sequential_walk(g, cap, keys, 0, n_valid, inv_ne, load, counts, out, out_u8);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M, int32_t nM,
+                               int32_t anchor, const unsigned long long* keys, int64_t n_keys, int32_t* out,
+                               uint8_t* out_u8, uint8_t* tent_scratch, cudaStream_t s) {
+  const size_t smem = (size_t)L * g * 8 + (size_t)g * 4;
+  const bool parallel = L <= kMaxLayers && tent_scratch != nullptr;
+  auto kern = !parallel ? greedy_walk_kernel<0>
+            : g == 8    ? greedy_walk_kernel<8>
+            : g == 4    ? greedy_walk_kernel<4>
+            : g == 2    ? greedy_walk_kernel<2>
+            : g == 16   ? greedy_walk_kernel<16>
+            : g == 32   ? greedy_walk_kernel<32>
+                        : greedy_walk_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<1, kThreads, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8, tent_scratch);
+  return cudaGetLastError();
+}
+
+}  // namespace gimbal_gpu

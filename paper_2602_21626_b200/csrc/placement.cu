@@ -410,148 +410,6 @@ __global__ void greedy_keys_kernel(int64_t m, const unsigned long long* __restri
   }
 }
 
-constexpr int kGreedyKeyChunk = 8192;  // sorted keys staged per round (64 KB)
-
-template <int G>  // G = n_gpus when specialised, 0 = runtime
-__global__ void greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
-                                   const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
-                                   const unsigned long long* __restrict__ keys, int64_t n_keys,
-                                   int32_t* __restrict__ out, uint8_t* __restrict__ out_u8) {
-  extern __shared__ unsigned long long load[];  // [L][g], then counts [g], then staged keys
-  int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
-  const int64_t m = (int64_t)L * ne;
-  const int cap = (int)(m / g);
-  const unsigned long long inv_ne = ((1ull << 40) + (unsigned long long)ne - 1) / (unsigned long long)ne;
-  for (int64_t i = threadIdx.x; i < (int64_t)L * g; i += blockDim.x) load[i] = 0ull;
-  for (int p = threadIdx.x; p < g; p += blockDim.x) counts[p] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nM; ++i) {  // placement.cpp:272-279
-      const int e = M[i];
-      out[e] = anchor;
-      if (out_u8) out_u8[e] = (uint8_t)anchor;
-      load[(int64_t)(e / ne) * g + anchor] += A[e];
-      counts[anchor] += 1;
-    }
-  }
-  __syncthreads();
-  // The walk is inherently sequential (each choice reads the loads the previous ones wrote), so
-  // one thread walks while the CTA stages the sorted keys through shared memory ahead of it.
-  unsigned long long* kbuf = reinterpret_cast<unsigned long long*>(counts + ((g + 1) & ~1));
-  int gcnt[G > 0 ? G : 1];  // per-GPU cardinalities (thread 0, specialised walk)
-#pragma unroll
-  for (int p = 0; p < (G > 0 ? G : 1); ++p) gcnt[p] = G > 0 ? counts[p] : 0;
-  bool done = false;
-  for (int64_t base = 0; base < n_keys && !done; base += kGreedyKeyChunk) {
-    const int nk = (int)min((int64_t)kGreedyKeyChunk, n_keys - base);
-    for (int i = threadIdx.x; i < nk; i += blockDim.x) kbuf[i] = keys[base + i];
-    __syncthreads();
-    if constexpr (G > 0) {
-      // Pipelined walk: the next expert's home-row loads are issued before the current decision
-      // and patched if the current placement lands in that row, so steps do not serialise on
-      // the shared-memory store -> load round trip.  GPU cardinalities live in registers.
-      if (threadIdx.x == 0) {
-        auto decode = [&](unsigned long long key, int& e, unsigned long long& a, int& layer, int& row) {
-          e = 0xffffff - (int)(key & 0xffffffull);
-          a = key >> 24;
-          layer = (int)(((unsigned long long)e * inv_ne) >> 40);  // e / ne, exact for e < 2^24
-          row = a > 0 ? layer : 0;  // first argmax row of the flat column (row 0 if all zero)
-        };
-        unsigned long long key = nk > 0 ? kbuf[0] : 0ull;
-        int e = 0, layer = 0, row = 0;
-        unsigned long long a = 0ull;
-        unsigned long long v[G];
-        if (key != 0ull) {
-          decode(key, e, a, layer, row);
-#pragma unroll
-          for (int p = 0; p < G; ++p) v[p] = load[row * G + p];
-        }
-        for (int i = 0; i < nk; ++i) {
-          if (key == 0ull) {
-            done = true;
-            break;
-          }
-          const unsigned long long key_n = i + 1 < nk ? kbuf[i + 1] : 0ull;
-          int e_n = 0, layer_n = 0, row_n = 0;
-          unsigned long long a_n = 0ull, v_n[G];
-          if (key_n != 0ull) {
-            decode(key_n, e_n, a_n, layer_n, row_n);
-#pragma unroll
-            for (int p = 0; p < G; ++p) v_n[p] = load[row_n * G + p];
-          }
-          int best = -1;
-          unsigned long long bv = 0ull;
-#pragma unroll
-          for (int p = 0; p < G; ++p)  // placement.cpp:290-295: strict <, lowest p first
-            if (gcnt[p] < cap && (best < 0 || v[p] < bv)) {
-              best = p;
-              bv = v[p];
-            }
-          out[e] = best;
-          if (out_u8) out_u8[e] = (uint8_t)best;
-          load[layer * G + best] += a;
-#pragma unroll
-          for (int p = 0; p < G; ++p) {
-            gcnt[p] += (p == best);
-            if (row_n == layer) v_n[p] += (p == best) ? a : 0ull;  // forward the pending update
-          }
-          key = key_n;
-          e = e_n;
-          a = a_n;
-          layer = layer_n;
-          row = row_n;
-#pragma unroll
-          for (int p = 0; p < G; ++p) v[p] = v_n[p];
-        }
-      }
-    } else if (threadIdx.x == 0) {
-      for (int i = 0; i < nk; ++i) {
-        const unsigned long long key = kbuf[i];
-        if (key == 0ull) {
-          done = true;
-          break;
-        }
-        const int e = 0xffffff - (int)(key & 0xffffffull);
-        const unsigned long long a = key >> 24;
-        const int layer = (int)(((unsigned long long)e * inv_ne) >> 40);  // e / ne, exact for e < 2^24
-        // home = first argmax row of the flat column: its layer if A > 0, else row 0
-        const unsigned long long* lr = load + (a > 0 ? layer : 0) * g;
-        int best = -1;
-        unsigned long long bv = 0ull;
-        if constexpr (G > 0) {
-          unsigned long long v[G];
-          int cn[G];
-#pragma unroll
-          for (int p = 0; p < G; ++p) {  // issue all shared loads before the compare chain
-            v[p] = lr[p];
-            cn[p] = counts[p];
-          }
-#pragma unroll
-          for (int p = 0; p < G; ++p)  // placement.cpp:290-295: strict <, lowest p first
-            if (cn[p] < cap && (best < 0 || v[p] < bv)) {
-              best = p;
-              bv = v[p];
-            }
-        } else {
-          for (int p = 0; p < g; ++p) {
-            if (counts[p] >= cap) continue;
-            const unsigned long long v = lr[p];
-            if (best < 0 || v < bv) {
-              best = p;
-              bv = v;
-            }
-          }
-        }
-        out[e] = best;
-        if (out_u8) out_u8[e] = (uint8_t)best;
-        load[layer * g + best] += a;
-        counts[best] += 1;
-      }
-    }
-    done = __syncthreads_or(done);
-  }
-}
-
 // ---- bitonic sort (descending) of u64 keys, n a power of two ----
 
 __global__ void bitonic_local_kernel(unsigned long long* keys, int64_t n, int64_t k_start,
@@ -767,18 +625,6 @@ cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uin
                                cudaStream_t s) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(4 * 1184, (n_pad + 255) / 256));
   greedy_keys_kernel<<<grid, 256, 0, s>>>(m, A, anchored, keys, n_pad, flags);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M,
-                               int32_t nM, int32_t anchor, const unsigned long long* keys,
-                               int64_t n_keys, int32_t* out, uint8_t* out_u8, cudaStream_t s) {
-  const size_t smem = (size_t)L * g * 8 + (size_t)((g + 1) & ~1) * 4 + (size_t)kGreedyKeyChunk * 8;
-  auto kern = g == 8 ? greedy_walk_kernel<8> : g == 4 ? greedy_walk_kernel<4> : g == 2 ? greedy_walk_kernel<2>
-            : g == 16 ? greedy_walk_kernel<16> : greedy_walk_kernel<0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<1, 256, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8);
   return cudaGetLastError();
 }
 
