@@ -223,6 +223,13 @@ struct gimbal_stats_s {
 
   int count_device(const void* ids, int id_bytes, int64_t n) {
     const int L = topo.n_layers;
+    if (!use_mma && direct_u15_supported(lm8_plan, id_bytes, ids) && !std::getenv("GIMBAL_NO_DIRECT")) {
+      // every uint8 id is a valid expert at n_e = 256: no validation / transposition pass
+      GIMBAL_TRY(timing_begin());
+      GIMBAL_CUDA_TRY(launch_count_direct_u15(lm8_plan, static_cast<const uint8_t*>(ids), n, dE, stream));
+      GIMBAL_TRY(timing_end());
+      return GIMBAL_OK;
+    }
     if (lm8_supported(L, topo.n_experts, topo.top_k, id_bytes)) {
       // the transposition must see work already queued on `stream` (e.g. host staging)
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_order, stream));

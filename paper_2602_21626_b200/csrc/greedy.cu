@@ -112,24 +112,53 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t n_pos = min((int64_t)s_npos, n_valid);
 
   if constexpr (G > 0) {
+    // sorted keys and a per-position layer map staged in shared memory (the launcher only picks
+    // this path when they fit); layer 0xff marks padding
+    unsigned long long* skeys = reinterpret_cast<unsigned long long*>(counts + 4 * ((g + 3) / 4));
+    const int64_t n_pad = (n_pos + 15) & ~15ll;
+    uint8_t* lay = reinterpret_cast<uint8_t*>(skeys + n_pad);
+    tent = lay + n_pad;
+    for (int64_t i = threadIdx.x; i < n_pad; i += blockDim.x) {
+      const unsigned long long key = i < n_pos ? keys[i] : 0ull;
+      skeys[i] = key;
+      lay[i] = i < n_pos ? (uint8_t)(((unsigned long long)key_expert(key) * inv_ne) >> 40) : (uint8_t)0xff;
+    }
+    __syncthreads();
+    // visits this thread's layer positions in [0, end) in order: 16 layer bytes per shared load,
+    // exact zero-byte test on (word ^ layer) picks the matches
+    auto for_layer = [&](int l, int64_t end, auto&& body) {
+      const uint32_t lw = 0x01010101u * (uint32_t)l;
+      for (int64_t c = 0; c < end; c += 16) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(lay + c);
+        const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t x = ws[q] ^ lw;
+          uint32_t z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);  // 0x80 where byte == 0
+          while (z) {
+            const int64_t pos = c + q * 4 + ((__ffs(z) - 1) >> 3);
+            z &= z - 1;
+            if (pos < end) body(pos);
+          }
+        }
+      }
+    };
     // ---- A: per-layer walks, cap ignored (one thread per layer, its load row in registers) ----
     if (threadIdx.x < L) {
       const int l = threadIdx.x;
       unsigned long long v[G];
 #pragma unroll
       for (int p = 0; p < G; ++p) v[p] = load[l * G + p];
-      for (int64_t i = 0; i < n_pos; ++i) {
-        const unsigned long long key = __ldg(keys + i);  // same address across the warp: broadcast
-        const int e = key_expert(key);
-        if ((int)(((unsigned long long)e * inv_ne) >> 40) != l) continue;
+      for_layer(l, n_pos, [&](int64_t i) {
+        const unsigned long long a = key_total(skeys[i]);
         int best = 0;
 #pragma unroll
         for (int p = 1; p < G; ++p)
           if (v[p] < v[best]) best = p;
 #pragma unroll
-        for (int p = 0; p < G; ++p) v[p] += (p == best) ? key_total(key) : 0ull;
+        for (int p = 0; p < G; ++p) v[p] += (p == best) ? a : 0ull;
         tent[i] = (uint8_t)best;
-      }
+      });
     }
     __syncthreads();
     // ---- B: first position whose tentative GPU is already at its cap ----
@@ -160,6 +189,10 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
     const int64_t star = s_star;
+#ifdef GIMBAL_DEBUG_GREEDY
+    if (threadIdx.x == 0) printf("greedy: n_keys %lld n_valid %lld n_pos %lld star %lld\n", (long long)n_keys,
+                                 (long long)n_valid, (long long)n_pos, (long long)star);
+#endif
     // ---- C: state at s*: loads from each layer's positions < s*, counts from all of them ----
     if (threadIdx.x < L) {
       const int l = threadIdx.x;
@@ -169,10 +202,9 @@ __global__ void __launch_bounds__(kThreads)
       int c[G];
 #pragma unroll
       for (int p = 0; p < G; ++p) c[p] = 0;
-      for (int64_t i = 0; i < star; ++i) {
-        const unsigned long long key = __ldg(keys + i);
+      for_layer(l, star, [&](int64_t i) {
+        const unsigned long long key = skeys[i];
         const int e = key_expert(key);
-        if ((int)(((unsigned long long)e * inv_ne) >> 40) != l) continue;
         const int p = tent[i];
 #pragma unroll
         for (int q = 0; q < G; ++q) {
@@ -181,7 +213,7 @@ __global__ void __launch_bounds__(kThreads)
         }
         out[e] = p;
         if (out_u8) out_u8[e] = (uint8_t)p;
-      }
+      });
 #pragma unroll
       for (int p = 0; p < G; ++p) {
         load[l * G + p] = v[p];
@@ -202,8 +234,11 @@ __global__ void __launch_bounds__(kThreads)
 cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M, int32_t nM,
                                int32_t anchor, const unsigned long long* keys, int64_t n_keys, int32_t* out,
                                uint8_t* out_u8, uint8_t* tent_scratch, cudaStream_t s) {
-  const size_t smem = (size_t)L * g * 8 + (size_t)g * 4;
-  const bool parallel = L <= kMaxLayers && tent_scratch != nullptr;
+  const size_t base = (size_t)L * g * 8 + (size_t)4 * ((g + 3) / 4) * 4;
+  const size_t n_pad = (size_t)((n_keys + 15) & ~15ll);
+  const size_t staged = base + n_pad * 10;  // keys (8 B) + layer map + tentative GPU per position
+  const bool parallel = L <= kMaxLayers && L < 255 && tent_scratch != nullptr && staged <= 200 * 1024;
+  const size_t smem = parallel ? staged : base;
   auto kern = !parallel ? greedy_walk_kernel<0>
             : g == 8    ? greedy_walk_kernel<8>
             : g == 4    ? greedy_walk_kernel<4>

@@ -92,6 +92,10 @@ cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne,
                                  unsigned long long* X, int64_t ld, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, int64_t T, int64_t ld,
                              unsigned long long* E, cudaStream_t s);
+// n_e = 256, top_k = 8, uint8 ids (always in range): count straight from the token-major trace
+bool direct_u15_supported(const Lm8Plan& plan, int id_bytes, const void* ids);
+cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, int64_t T,
+                                    unsigned long long* E, cudaStream_t s);
 
 // tcgen05 int8 multi-hot contraction (mma_count.cu), n_e in [32, 128], top_k <= 8, on LM8 input.
 bool mma_count_supported(int L, int ne, int k);
