@@ -171,16 +171,21 @@ __global__ void __launch_bounds__(1024, 1)
     const unsigned long long* Xl = X + (int64_t)l * prm.ld;
     const unsigned long long* Xn = Xl + prm.ld;
     unsigned long long* El = E + (int64_t)l * ne * ne;
-    for (int64_t t = t_begin + threadIdx.x; t < t_end; t += blockDim.x) {
-      unsigned long long cur, nxt;
+    auto fetch = [&](int64_t t, unsigned long long& c, unsigned long long& n) {
       if constexpr (TM) {  // the other pairs' CTAs read the same rows: keep them cacheable
         const unsigned long long* row = X + t * prm.L + l;
-        cur = __ldg(row);
-        nxt = __ldg(row + 1);
+        c = __ldg(row);
+        n = __ldg(row + 1);
       } else {
-        cur = __ldcs(Xl + t);
-        nxt = __ldcs(Xn + t);
+        c = __ldcs(Xl + t);
+        n = __ldcs(Xn + t);
       }
+    };
+    unsigned long long cur = 0, nxt = 0, cur_n = 0, nxt_n = 0;
+    if (t_begin + threadIdx.x < t_end) fetch(t_begin + threadIdx.x, cur, nxt);
+    for (int64_t t = t_begin + threadIdx.x; t < t_end; t += blockDim.x) {
+      // the next token's ids are in flight while this token's 64 increments issue
+      if (t + blockDim.x < t_end) fetch(t + blockDim.x, cur_n, nxt_n);
 #pragma unroll
       for (int a = 0; a < K; ++a) {
         const uint32_t j = id_of(cur, a);
@@ -207,6 +212,8 @@ __global__ void __launch_bounds__(1024, 1)
           }
         }
       }
+      cur = cur_n;
+      nxt = nxt_n;
     }
     __syncthreads();
     for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) {
