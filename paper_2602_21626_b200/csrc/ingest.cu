@@ -21,7 +21,10 @@
 #include <cstdlib>
 #include <string>
 
+#include <cudaTypedefs.h>
+
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace gimbal_gpu {
 
@@ -145,6 +148,83 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// Balanced ("stream-K") split of the u15 kernels' work: the (chunk, pair, token) space is
+// linearised chunk-major and CTA b owns positions [b * per, (b + 1) * per), i.e. the tail of one
+// (chunk, pair) unit, some whole units and the head of another, so every CTA counts the same
+// number of token-pairs instead of the last wave of whole units running on a few SMs.
+// Neighbouring CTAs sit on neighbouring pairs of the same chunk at nearly the same token offset,
+// so a trace row fetched for one pair is still in L2 for the next.
+__device__ __forceinline__ void balanced_range(const Lm8Params& prm, int64_t& p, int64_t& p_end) {
+  const int64_t span = prm.n_units * prm.chunk_tokens;
+  const int64_t per = (span + gridDim.x - 1) / gridDim.x;
+  p = min(span, (int64_t)blockIdx.x * per);
+  p_end = min(span, p + per);
+}
+
+// Next non-empty segment [t0, t1) of pair l in [p, p_end); advances p.
+__device__ __forceinline__ bool next_segment(const Lm8Params& prm, int64_t& p, int64_t p_end, int& l,
+                                             int64_t& t0, int64_t& t1) {
+  const int pairs = prm.L - 1;
+  const int64_t CH = prm.chunk_tokens;
+  while (p < p_end) {
+    const int64_t u = p / CH;
+    const int64_t base = u * CH;
+    const int64_t off0 = p - base, off1 = min(CH, p_end - base);
+    p = base + off1;
+    const int64_t chunk = u / pairs;
+    l = (int)(u - chunk * pairs);
+    t0 = chunk * CH + off0;
+    t1 = min(prm.T, chunk * CH + off1);
+    if (t0 < t1) return true;
+  }
+  return false;
+}
+
+// The k x k increments of one token into a 15-bit-counter pair table (see below).
+template <int K>
+__device__ __forceinline__ void u15_count_token(uint32_t* cnt, int wpr, unsigned long long* El, int ne,
+                                                unsigned long long cur, unsigned long long nxt) {
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const uint32_t j = id_of(cur, a);
+    uint32_t* rowp = cnt + j * wpr;
+    const uint32_t sw = j & 31u;
+    uint32_t old[K];
+    bool full = false;
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const uint32_t k = id_of(nxt, b);
+      const uint32_t shift = (k & 1u) << 4;
+      old[b] = atomicAdd(rowp + ((k >> 1) ^ sw), 1u << shift);
+      full |= ((old[b] >> shift) & 0x7fffu) == 0x7fffu;  // this increment filled the half
+    }
+    if (full) {  // rare: one branch per row instead of one per increment
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const uint32_t k = id_of(nxt, b);
+        const uint32_t shift = (k & 1u) << 4;
+        if (((old[b] >> shift) & 0x7fffu) == 0x7fffu) {
+          atomicSub(rowp + ((k >> 1) ^ sw), 0x8000u << shift);
+          atomicAdd(El + (int64_t)j * ne + k, 32768ull);
+        }
+      }
+    }
+  }
+}
+
+// Add a 15-bit-counter pair table to the u64 tensor (caller synchronises around it).
+__device__ __forceinline__ void u15_flush(const uint32_t* cnt, int wpr, unsigned long long* El, int ne) {
+  for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) {
+    const uint32_t v = cnt[w];
+    if (v == 0u) continue;
+    const int j = w / wpr;
+    const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+    unsigned long long* rowE = El + (int64_t)j * ne;
+    if (v & 0xffffu) atomicAdd(rowE + k0, (unsigned long long)(v & 0xffffu));
+    if (v >> 16) atomicAdd(rowE + k0 + 1, (unsigned long long)(v >> 16));
+  }
+}
+
 // One whole layer pair per unit with 15-bit counters, two per 32-bit word (k even: bits 0-14,
 // k odd: bits 16-30; bits 15 and 31 are guards), so a 256 x 256 pair fits in 128 KB and no row
 // filter is needed.  An increment that carries a half into its guard bit (the half held 0x7FFF)
@@ -160,14 +240,13 @@ __global__ void __launch_bounds__(1024, 1)
   extern __shared__ uint32_t cnt[];
   const int ne = prm.ne;
   const int wpr = ne >> 1;  // words per row
-  const int pairs = prm.L - 1;
-  for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
-    const int64_t chunk = unit / pairs;
-    const int l = (int)(unit - chunk * pairs);
+  int64_t p, p_end;
+  balanced_range(prm, p, p_end);
+  int l;
+  int64_t t_begin, t_end;
+  while (next_segment(prm, p, p_end, l, t_begin, t_end)) {
     for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) cnt[w] = 0u;
     __syncthreads();
-    const int64_t t_begin = chunk * prm.chunk_tokens;
-    const int64_t t_end = min(prm.T, t_begin + prm.chunk_tokens);
     const unsigned long long* Xl = X + (int64_t)l * prm.ld;
     const unsigned long long* Xn = Xl + prm.ld;
     unsigned long long* El = E + (int64_t)l * ne * ne;
@@ -186,45 +265,86 @@ __global__ void __launch_bounds__(1024, 1)
     for (int64_t t = t_begin + threadIdx.x; t < t_end; t += blockDim.x) {
       // the next token's ids are in flight while this token's 64 increments issue
       if (t + blockDim.x < t_end) fetch(t + blockDim.x, cur_n, nxt_n);
-#pragma unroll
-      for (int a = 0; a < K; ++a) {
-        const uint32_t j = id_of(cur, a);
-        uint32_t* rowp = cnt + j * wpr;
-        const uint32_t sw = j & 31u;
-        uint32_t old[K];
-        bool full = false;
-#pragma unroll
-        for (int b = 0; b < K; ++b) {
-          const uint32_t k = id_of(nxt, b);
-          const uint32_t shift = (k & 1u) << 4;
-          old[b] = atomicAdd(rowp + ((k >> 1) ^ sw), 1u << shift);
-          full |= ((old[b] >> shift) & 0x7fffu) == 0x7fffu;  // this increment filled the half
-        }
-        if (full) {  // rare: one branch per row instead of one per increment
-#pragma unroll
-          for (int b = 0; b < K; ++b) {
-            const uint32_t k = id_of(nxt, b);
-            const uint32_t shift = (k & 1u) << 4;
-            if (((old[b] >> shift) & 0x7fffu) == 0x7fffu) {
-              atomicSub(rowp + ((k >> 1) ^ sw), 0x8000u << shift);
-              atomicAdd(El + (int64_t)j * ne + k, 32768ull);
-            }
-          }
-        }
-      }
+      u15_count_token<K>(cnt, wpr, El, ne, cur, nxt);
       cur = cur_n;
       nxt = nxt_n;
     }
     __syncthreads();
-    for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) {
-      const uint32_t v = cnt[w];
-      if (v == 0u) continue;
-      const int j = w / wpr;
-      const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
-      unsigned long long* rowE = El + (int64_t)j * ne;
-      if (v & 0xffffu) atomicAdd(rowE + k0, (unsigned long long)(v & 0xffffu));
-      if (v >> 16) atomicAdd(rowE + k0 + 1, (unsigned long long)(v >> 16));
+    u15_flush(cnt, wpr, El, ne);
+    __syncthreads();
+  }
+}
+
+// Direct token-major counting with the ids staged by the tensor memory accelerator: every
+// 1024-token block of the pair's two columns is one set of 2-D TMA boxes, so the SM's load/store
+// pipe serves only the shared-memory atomics and two short shared reads per token instead of two
+// 32-line gathers per warp.  A box must start 16-byte aligned in the row, so it spans the four
+// layers (l & ~1) .. (l & ~1) + 3 and the pair's words sit at offset l & 1 (columns past the last
+// layer are zero-filled and never read).  A 3-stage full/empty mbarrier ring keeps the next
+// blocks in flight while the current one is counted.
+constexpr int kTmaStages = 3;
+constexpr int kTmaBlock = 1024;  // tokens per stage = threads per CTA
+constexpr int kTmaBox = 256;     // rows per TMA box (hardware limit)
+constexpr int kTmaCols = 4;      // u64 words per row in a box (32 B)
+constexpr int kU15Bytes = 256 * 128 * 4;
+
+__global__ void __launch_bounds__(kTmaBlock, 1)
+    count_tm_u15_tma_kernel(const __grid_constant__ CUtensorMap tmap, Lm8Params prm,
+                            unsigned long long* __restrict__ E) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem_raw);
+  unsigned long long* stage = reinterpret_cast<unsigned long long*>(smem_raw + kU15Bytes);
+  __shared__ uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+  constexpr int ne = 256, wpr = 128;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kTmaBlock / 32);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t it = 0;  // stage uses so far (CTA-uniform)
+  int64_t p, p_end;
+  balanced_range(prm, p, p_end);
+  int l;
+  int64_t t_begin, t_end;
+  while (next_segment(prm, p, p_end, l, t_begin, t_end)) {
+    for (int w = tid; w < ne * wpr; w += kTmaBlock) cnt[w] = 0u;
+    const uint32_t nb = (uint32_t)((t_end - t_begin + kTmaBlock - 1) / kTmaBlock);
+    unsigned long long* El = E + (int64_t)l * ne * ne;
+    auto issue = [&](uint32_t blk, uint32_t g) {  // thread 0
+      const uint32_t s = g % kTmaStages;
+      if (g >= kTmaStages) mbar_wait(&empty_bar[s], (g / kTmaStages - 1) & 1u);
+      mbar_arrive_expect_tx(&full_bar[s], kTmaBlock * kTmaCols * 8);
+      const int64_t t0 = t_begin + (int64_t)blk * kTmaBlock;
+#pragma unroll
+      for (int q = 0; q < kTmaBlock / kTmaBox; ++q)
+        tma_load_2d(stage + (s * kTmaBlock + q * kTmaBox) * kTmaCols, &tmap, &full_bar[s], l & ~1,
+                    (int)(t0 + q * kTmaBox));
+    };
+    if (tid == 0)
+      for (uint32_t i = 0; i < min(nb, (uint32_t)kTmaStages); ++i) issue(i, it + i);
+    __syncthreads();  // counters zeroed
+    for (uint32_t i = 0; i < nb; ++i) {
+      const uint32_t g = it + i, s = g % kTmaStages;
+      mbar_wait(&full_bar[s], (g / kTmaStages) & 1u);
+      const unsigned long long* row = stage + (s * kTmaBlock + tid) * kTmaCols + (l & 1);
+      const unsigned long long cur = row[0], nxt = row[1];
+      if (t_begin + (int64_t)i * kTmaBlock + tid < t_end) u15_count_token<8>(cnt, wpr, El, ne, cur, nxt);
+      // release the stage only once its words have been consumed: a shared load can still sit
+      // in the queue behind this warp's atomics when an early arrive would let TMA overwrite it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[s]);
+      if (tid == 0 && i + kTmaStages < nb) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(i + kTmaStages, g + kTmaStages);
+      }
+    }
+    it += nb;
+    __syncthreads();
+    u15_flush(cnt, wpr, El, ne);
     __syncthreads();
   }
 }
@@ -404,6 +524,29 @@ cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne,
   }
 }
 
+// Tensor map over the token-major trace viewed as a [T][L] u64 matrix, box = 4 layers x 256
+// tokens.  Needs 16-byte row pitch (L even) and base; false = use the plain-load kernel.
+static bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode || (L & 1) || (reinterpret_cast<uintptr_t>(trace) & 15) || T >= (int64_t)INT32_MAX ||
+      std::getenv("GIMBAL_NO_TMA"))
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)L, (cuuint64_t)T};
+  const cuuint64_t strides[1] = {(cuuint64_t)L * 8};
+  const cuuint32_t box[2] = {kTmaCols, (cuuint32_t)kTmaBox};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(trace), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool direct_u15_supported(const Lm8Plan& plan, int id_bytes, const void* ids) {
   return plan.u15 && plan.k == 8 && plan.ne == 256 && id_bytes == 1 &&
          (reinterpret_cast<uintptr_t>(ids) & 7) == 0;
@@ -423,12 +566,25 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   prm.T = T;
   prm.ld = 0;
   const int64_t resident = plan.sms;
-  int64_t n_chunks = std::max<int64_t>(1, (8 * resident + plan.n_groups - 1) / plan.n_groups);
+  // chunks bound how far apart (in tokens) the CTAs counting different pairs of the same trace
+  // rows drift, i.e. the L2 footprint of the shared rows; the balanced split makes the count
+  // of chunks irrelevant to load balance
+  int64_t n_chunks = 21;
+  if (const char* e = std::getenv("GIMBAL_DIRECT_CHUNKS")) n_chunks = std::max(1, std::atoi(e));
   n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
   prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
   n_chunks = (T + prm.chunk_tokens - 1) / prm.chunk_tokens;
   prm.n_units = n_chunks * plan.n_groups;
-  const int grid = (int)std::min<int64_t>(prm.n_units, resident);
+  const int grid = (int)resident;
+  CUtensorMap tmap;
+  if (encode_trace_map(&tmap, trace, T, plan.L)) {
+    const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
+    cudaError_t e = cudaFuncSetAttribute(count_tm_u15_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    count_tm_u15_tma_kernel<<<grid, kTmaBlock, smem, s>>>(tmap, prm, E);
+    return cudaGetLastError();
+  }
   auto kern = count_lm8_u15_kernel<8, true>;
   const size_t smem = (size_t)plan.ne * plan.ne * 2;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -460,7 +616,8 @@ cudaError_t launch_count_lm8(const Lm8Plan& plan, const unsigned long long* X, i
   prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
   n_chunks = (T + prm.chunk_tokens - 1) / prm.chunk_tokens;
   prm.n_units = n_chunks * base_units;
-  const int grid = (int)std::min<int64_t>(prm.n_units, resident);
+  // the u15 kernel splits its work evenly over however many CTAs run it
+  const int grid = plan.u15 ? (int)resident : (int)std::min<int64_t>(prm.n_units, resident);
   switch (plan.k) {
     case 1: return launch_count_k<1>(plan, prm, X, E, s, grid);
     case 2: return launch_count_k<2>(plan, prm, X, E, s, grid);

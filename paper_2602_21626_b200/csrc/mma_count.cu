@@ -24,6 +24,7 @@
 #include <cstdint>
 
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace gimbal_gpu {
 
@@ -50,24 +51,6 @@ struct MmaParams {
   uint32_t idesc;
   const uint32_t* flags;  // kFlagDuplicates set by the transposition of this chunk
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
 
 // Shared-memory matrix descriptor: no swizzle, MN-major.  Core matrix = 8 K-rows of 16 bytes;
 // K-groups (8 tokens) are LBO = 1024 B apart, MN-groups (16 experts) SBO = 128 B apart.

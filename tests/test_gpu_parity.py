@@ -86,6 +86,22 @@ def test_stats_odd_shapes(G, orc, L, ne, k):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+@pytest.mark.parametrize("L,T,offset", [(58, 70001, 0), (58, 700, 0), (58, 3000, 8), (7, 5000, 0), (2, 1025, 0)])
+def test_direct_count_layouts(G, orc, L, T, offset):
+    """n_e = 256, top-8 uint8 traces are counted straight from the token-major rows: TMA-staged
+    when the row pitch and base are 16-byte aligned (L even), plain loads otherwise."""
+    ne, k = 256, 8
+    topo = G.MoeTopology(L, ne, k, 8)
+    rng = np.random.default_rng(T + L)
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    buf = torch.empty(T * L * k + offset, dtype=torch.uint8, device="cuda")
+    dev = buf[offset:].view(T, L, k)
+    dev.copy_(torch.from_numpy(ids))
+    _, (A, E, W) = _stats_gpu(G, topo, dev)
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
+
+
 @pytest.mark.parametrize("dup", [False, True])
 def test_counter_overflow_paths(G, dup):
     """Hot cells far beyond 2^15 / 2^16 per work unit (guarded 15-bit counters at n_e = 256,
