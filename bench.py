@@ -68,6 +68,29 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def peaks_all():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def count_kernel(ne, k):
+    """(kernel, engine) that counts E for this shape on a device-resident uint8 trace (capi.cu
+    count_device): the TMA-staged direct kernel at n_e = 256 / top-8, tcgen05 for n_e in (64, 128],
+    whole-pair shared tables below, 15-bit halves or row splits above."""
+    if ne == 256 and k == 8:
+        return "count_tm_u15_tma_kernel<true> (TMA-staged ids, 16-bit halves, drained)", "atomics"
+    if 64 < ne <= 128:
+        return "count_mma_kernel (tcgen05.mma kind::i8, TMEM accumulators)", "tensor"
+    if ne * ne * 4 <= 200 * 1024:
+        return "count_lm8_pairs_kernel", "atomics"
+    if ne % 64 == 0 and ne * ne * 2 <= 200 * 1024:
+        return "count_lm8_u15_kernel", "atomics"
+    return "count_lm8_split_kernel", "atomics"
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -295,18 +318,31 @@ def main():
         peak, peak_kind = peaks()
         achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
         upd = tok_per_launch * (L - 1) * k * k / (launch_ms * 1e-3)
-        split = ne * ne * 4 > 200 * 1024
+        kernel, engine = count_kernel(ne, k)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": (TRAFFIC[args.config]["bytes"] / TRAFFIC[args.config]["tokens_in_launch"] * tok_per_launch
                             if args.config in TRAFFIC else None),
                 "traffic_source": TRAFFIC.get(args.config, {}).get("source"),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                "kernel": "count_lm8_split_kernel" if split else "count_lm8_pairs_kernel",
+                "kernel": kernel,
                 "launch_ms": launch_ms, "launches_per_step": launches_per_step,
-                "algorithmic_bytes_per_launch": alg_bytes, "share_of_step": count_total_ms / args.steps / ms,
-                "atomic_ceiling": {"bound": "shared-memory atomics", "achieved": upd, "peak": ATOMS_RANDOM_PEAK,
-                                   "unit": "E pair-updates/s", "frac": upd / ATOMS_RANDOM_PEAK,
-                                   "peak_source": "profiles/r1_atoms_microbench.md (random-address ATOMS)"}}
+                "algorithmic_bytes_per_launch": alg_bytes, "share_of_step": count_total_ms / args.steps / ms}
+        if engine == "tensor":
+            # dense int8 multiply-adds the tcgen05 contraction issues (n_e rounded up to the MMA N)
+            n_mma = (ne + 15) // 16 * 16
+            ops = 2.0 * tok_per_launch * (L - 1) * 128 * n_mma / (launch_ms * 1e-3)
+            bf16 = peaks_all().get("bf16_tflops")
+            tpeak = 2.0 * bf16 * 1e12 if bf16 else 4.5e15
+            roof["tensor_ceiling"] = {
+                "bound": "tensor", "achieved": ops / 1e12, "peak": tpeak / 1e12, "unit": "TOP/s (dense int8)",
+                "frac": ops / tpeak,
+                "peak_source": ("2 x measured bf16 dense (MEASURED_PEAKS.json bf16_tflops; int8 dense = 2x bf16 "
+                                "on sm_100)" if bf16 else "B200_PROFILING.md fallback 4.5 POP/s"),
+                "useful_updates_per_s": upd}
+        else:
+            roof["atomic_ceiling"] = {"bound": "shared-memory atomics", "achieved": upd, "peak": ATOMS_RANDOM_PEAK,
+                                      "unit": "E pair-updates/s", "frac": upd / ATOMS_RANDOM_PEAK,
+                                      "peak_source": "profiles/r1_atoms_microbench.md (random-address ATOMS)"}
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None

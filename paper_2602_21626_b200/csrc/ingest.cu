@@ -148,29 +148,47 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
-// Balanced ("stream-K") split of the u15 kernels' work: the (chunk, pair, token) space is
-// linearised chunk-major and CTA b owns positions [b * per, (b + 1) * per), i.e. the tail of one
-// (chunk, pair) unit, some whole units and the head of another, so every CTA counts the same
-// number of token-pairs instead of the last wave of whole units running on a few SMs.
-// Neighbouring CTAs sit on neighbouring pairs of the same chunk at nearly the same token offset,
-// so a trace row fetched for one pair is still in L2 for the next.
-__device__ __forceinline__ void balanced_range(const Lm8Params& prm, int64_t& p, int64_t& p_end) {
-  const int64_t span = prm.n_units * prm.chunk_tokens;
+// Work split of the u15 kernels over the (chunk, pair) units, chunk-major (u = chunk * pairs +
+// pair): whole units round-robin (unit b + r * grid in round r, so the CTAs counting different
+// pairs of the same chunk start together and share its trace rows through L2), then the units
+// left over after the last full round are split evenly over all CTAs ("stream-K" tail: CTA b owns
+// positions [b * per, (b + 1) * per) of their token space), so no SM idles through a partial wave.
+struct WorkCursor {
+  int64_t round, rounds;  // whole-unit rounds done / total
+  int64_t p, p_end;       // tail positions (unit * chunk_tokens + token offset)
+};
+
+__device__ __forceinline__ WorkCursor work_begin(const Lm8Params& prm) {
+  WorkCursor c;
+  c.round = 0;
+  c.rounds = prm.n_units / gridDim.x;
+  const int64_t tail0 = c.rounds * gridDim.x * prm.chunk_tokens;
+  const int64_t span = prm.n_units * prm.chunk_tokens - tail0;
   const int64_t per = (span + gridDim.x - 1) / gridDim.x;
-  p = min(span, (int64_t)blockIdx.x * per);
-  p_end = min(span, p + per);
+  c.p = tail0 + min(span, (int64_t)blockIdx.x * per);
+  c.p_end = tail0 + min(span, (int64_t)(blockIdx.x + 1) * per);
+  return c;
 }
 
-// Next non-empty segment [t0, t1) of pair l in [p, p_end); advances p.
-__device__ __forceinline__ bool next_segment(const Lm8Params& prm, int64_t& p, int64_t p_end, int& l,
-                                             int64_t& t0, int64_t& t1) {
+// Next non-empty segment [t0, t1) of pair l; false when the CTA's work is done.
+__device__ __forceinline__ bool next_segment(const Lm8Params& prm, WorkCursor& c, int& l, int64_t& t0,
+                                             int64_t& t1) {
   const int pairs = prm.L - 1;
   const int64_t CH = prm.chunk_tokens;
-  while (p < p_end) {
-    const int64_t u = p / CH;
+  while (c.round < c.rounds) {
+    const int64_t u = c.round * gridDim.x + blockIdx.x;
+    ++c.round;
+    const int64_t chunk = u / pairs;
+    l = (int)(u - chunk * pairs);
+    t0 = chunk * CH;
+    t1 = min(prm.T, t0 + CH);
+    if (t0 < t1) return true;
+  }
+  while (c.p < c.p_end) {
+    const int64_t u = c.p / CH;
     const int64_t base = u * CH;
-    const int64_t off0 = p - base, off1 = min(CH, p_end - base);
-    p = base + off1;
+    const int64_t off0 = c.p - base, off1 = min(CH, c.p_end - base);
+    c.p = base + off1;
     const int64_t chunk = u / pairs;
     l = (int)(u - chunk * pairs);
     t0 = chunk * CH + off0;
@@ -240,11 +258,10 @@ __global__ void __launch_bounds__(1024, 1)
   extern __shared__ uint32_t cnt[];
   const int ne = prm.ne;
   const int wpr = ne >> 1;  // words per row
-  int64_t p, p_end;
-  balanced_range(prm, p, p_end);
+  WorkCursor wc = work_begin(prm);
   int l;
   int64_t t_begin, t_end;
-  while (next_segment(prm, p, p_end, l, t_begin, t_end)) {
+  while (next_segment(prm, wc, l, t_begin, t_end)) {
     for (int w = threadIdx.x; w < ne * wpr; w += blockDim.x) cnt[w] = 0u;
     __syncthreads();
     const unsigned long long* Xl = X + (int64_t)l * prm.ld;
@@ -288,6 +305,27 @@ constexpr int kTmaBox = 256;     // rows per TMA box (hardware limit)
 constexpr int kTmaCols = 4;      // u64 words per row in a box (32 B)
 constexpr int kU15Bytes = 256 * 128 * 4;
 
+constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tokens
+
+// true when two of the eight id bytes are equal (every pair compared once: within each half at
+// byte distance 1 and 2, across the halves at all four rotations; "has a zero byte" test)
+__device__ __forceinline__ bool has_dup8(unsigned long long x) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  auto z = [](uint32_t v) { return (v - 0x01010101u) & ~v & 0x80808080u; };
+  uint32_t acc = z(lo ^ __byte_perm(lo, 0, 0x0321)) | z(lo ^ __byte_perm(lo, 0, 0x1032));
+  acc |= z(hi ^ __byte_perm(hi, 0, 0x0321)) | z(hi ^ __byte_perm(hi, 0, 0x1032));
+  acc |= z(lo ^ hi) | z(lo ^ __byte_perm(hi, 0, 0x0321));
+  acc |= z(lo ^ __byte_perm(hi, 0, 0x1032)) | z(lo ^ __byte_perm(hi, 0, 0x2103));
+  return acc != 0u;
+}
+
+// U16 = full 16-bit halves, increments without return values, and a drain every kDrainBlocks
+// blocks: a token whose ids are distinct within each layer adds at most 1 to any cell, so after
+// a drain leaves every half below 32768 the next 32768 tokens cannot carry out of a half.  Tokens
+// with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor instead.
+// Without the return-value dependency a warp issues its 64 increments back to back.
+// !U16 = guarded 15-bit halves with per-increment overflow detection (u15_count_token).
+template <bool U16>
 __global__ void __launch_bounds__(kTmaBlock, 1)
     count_tm_u15_tma_kernel(const __grid_constant__ CUtensorMap tmap, Lm8Params prm,
                             unsigned long long* __restrict__ E) {
@@ -306,11 +344,10 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
   }
   __syncthreads();
   uint32_t it = 0;  // stage uses so far (CTA-uniform)
-  int64_t p, p_end;
-  balanced_range(prm, p, p_end);
+  WorkCursor wc = work_begin(prm);
   int l;
   int64_t t_begin, t_end;
-  while (next_segment(prm, p, p_end, l, t_begin, t_end)) {
+  while (next_segment(prm, wc, l, t_begin, t_end)) {
     for (int w = tid; w < ne * wpr; w += kTmaBlock) cnt[w] = 0u;
     const uint32_t nb = (uint32_t)((t_end - t_begin + kTmaBlock - 1) / kTmaBlock);
     unsigned long long* El = E + (int64_t)l * ne * ne;
@@ -332,7 +369,34 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
       mbar_wait(&full_bar[s], (g / kTmaStages) & 1u);
       const unsigned long long* row = stage + (s * kTmaBlock + tid) * kTmaCols + (l & 1);
       const unsigned long long cur = row[0], nxt = row[1];
-      if (t_begin + (int64_t)i * kTmaBlock + tid < t_end) u15_count_token<8>(cnt, wpr, El, ne, cur, nxt);
+      if (t_begin + (int64_t)i * kTmaBlock + tid < t_end) {
+        if constexpr (U16) {
+          if (!(has_dup8(cur) | has_dup8(nxt))) {
+            uint32_t col[8], inc[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+              const uint32_t k = id_of(nxt, b);
+              col[b] = k >> 1;
+              inc[b] = 1u << ((k & 1u) << 4);
+            }
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+              const uint32_t j = id_of(cur, a);
+              uint32_t* rowp = cnt + j * wpr;
+              const uint32_t sw = j & 31u;
+#pragma unroll
+              for (int b = 0; b < 8; ++b) atomicAdd(rowp + (col[b] ^ sw), inc[b]);
+            }
+          } else {
+#pragma unroll 1
+            for (int a = 0; a < 8; ++a)
+#pragma unroll 1
+              for (int b = 0; b < 8; ++b) atomicAdd(El + id_of(cur, a) * ne + id_of(nxt, b), 1ull);
+          }
+        } else {
+          u15_count_token<8>(cnt, wpr, El, ne, cur, nxt);
+        }
+      }
       // release the stage only once its words have been consumed: a shared load can still sit
       // in the queue behind this warp's atomics when an early arrive would let TMA overwrite it
       __syncwarp();
@@ -340,6 +404,20 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
       if (tid == 0 && i + kTmaStages < nb) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(i + kTmaStages, g + kTmaStages);
+      }
+      if (U16 && (i + 1) % kDrainBlocks == 0 && i + 1 < nb) {
+        __syncthreads();
+        for (int w = tid; w < ne * wpr; w += kTmaBlock) {
+          const uint32_t v = cnt[w];
+          if (v & 0x80008000u) {
+            const int j = w / wpr;
+            const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+            if (v & 0x8000u) atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
+            if (v & 0x80000000u) atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
+            cnt[w] = v & 0x7fff7fffu;
+          }
+        }
+        __syncthreads();
       }
     }
     it += nb;
@@ -538,12 +616,20 @@ static bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, 
   if (!encode || (L & 1) || (reinterpret_cast<uintptr_t>(trace) & 15) || T >= (int64_t)INT32_MAX ||
       std::getenv("GIMBAL_NO_TMA"))
     return false;
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  if (const char* e = std::getenv("GIMBAL_TMA_PROMO")) {
+    const int v = std::atoi(e);
+    promo = v >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+            : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+            : v >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                       : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }
   const cuuint64_t dims[2] = {(cuuint64_t)L, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)L * 8};
   const cuuint32_t box[2] = {kTmaCols, (cuuint32_t)kTmaBox};
   const cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(trace), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -569,7 +655,7 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   // chunks bound how far apart (in tokens) the CTAs counting different pairs of the same trace
   // rows drift, i.e. the L2 footprint of the shared rows; the balanced split makes the count
   // of chunks irrelevant to load balance
-  int64_t n_chunks = 21;
+  int64_t n_chunks = 96;
   if (const char* e = std::getenv("GIMBAL_DIRECT_CHUNKS")) n_chunks = std::max(1, std::atoi(e));
   n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
   prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
@@ -579,10 +665,11 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   CUtensorMap tmap;
   if (encode_trace_map(&tmap, trace, T, plan.L)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
-    cudaError_t e = cudaFuncSetAttribute(count_tm_u15_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    static const bool u16 = !(std::getenv("GIMBAL_TMA_MODE") && std::string(std::getenv("GIMBAL_TMA_MODE")) == "u15");
+    auto kern = u16 ? count_tm_u15_tma_kernel<true> : count_tm_u15_tma_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    count_tm_u15_tma_kernel<<<grid, kTmaBlock, smem, s>>>(tmap, prm, E);
+    kern<<<grid, kTmaBlock, smem, s>>>(tmap, prm, E);
     return cudaGetLastError();
   }
   auto kern = count_lm8_u15_kernel<8, true>;
