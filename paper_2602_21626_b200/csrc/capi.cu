@@ -230,6 +230,15 @@ struct gimbal_stats_s {
       GIMBAL_TRY(timing_end());
       return GIMBAL_OK;
     }
+    if (use_mma && id_bytes == 1 && topo.top_k == 8 && L % 2 == 0 && (reinterpret_cast<uintptr_t>(ids) & 15) == 0 &&
+        n < INT32_MAX && !std::getenv("GIMBAL_NO_DIRECT") && !std::getenv("GIMBAL_NO_TMA")) {
+      // tensor-core contraction straight from the token-major trace (TMA-mapped rows)
+      GIMBAL_TRY(timing_begin());
+      GIMBAL_CUDA_TRY(launch_count_mma_direct(L, topo.n_experts, sms, static_cast<const uint8_t*>(ids), n, dE,
+                                              dflags, stream));
+      GIMBAL_TRY(timing_end());
+      return GIMBAL_OK;
+    }
     if (lm8_supported(L, topo.n_experts, topo.top_k, id_bytes)) {
       // the transposition must see work already queued on `stream` (e.g. host staging)
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_order, stream));

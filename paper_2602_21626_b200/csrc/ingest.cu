@@ -307,18 +307,6 @@ constexpr int kU15Bytes = 256 * 128 * 4;
 
 constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tokens
 
-// true when two of the eight id bytes are equal (every pair compared once: within each half at
-// byte distance 1 and 2, across the halves at all four rotations; "has a zero byte" test)
-__device__ __forceinline__ bool has_dup8(unsigned long long x) {
-  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-  auto z = [](uint32_t v) { return (v - 0x01010101u) & ~v & 0x80808080u; };
-  uint32_t acc = z(lo ^ __byte_perm(lo, 0, 0x0321)) | z(lo ^ __byte_perm(lo, 0, 0x1032));
-  acc |= z(hi ^ __byte_perm(hi, 0, 0x0321)) | z(hi ^ __byte_perm(hi, 0, 0x1032));
-  acc |= z(lo ^ hi) | z(lo ^ __byte_perm(hi, 0, 0x0321));
-  acc |= z(lo ^ __byte_perm(hi, 0, 0x1032)) | z(lo ^ __byte_perm(hi, 0, 0x2103));
-  return acc != 0u;
-}
-
 // U16 = full 16-bit halves, increments without return values, and a drain every kDrainBlocks
 // blocks: a token whose ids are distinct within each layer adds at most 1 to any cell, so after
 // a drain leaves every half below 32768 the next 32768 tokens cannot carry out of a half.  Tokens
@@ -602,9 +590,9 @@ cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne,
   }
 }
 
-// Tensor map over the token-major trace viewed as a [T][L] u64 matrix, box = 4 layers x 256
-// tokens.  Needs 16-byte row pitch (L even) and base; false = use the plain-load kernel.
-static bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L) {
+// Tensor map over the token-major top-8 trace viewed as a [T][L] u64 matrix, box = cols layers x
+// rows tokens.  Needs a 16-byte row pitch (L even) and base; false = caller uses plain loads.
+bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L, int cols, int rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -626,7 +614,7 @@ static bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, 
   }
   const cuuint64_t dims[2] = {(cuuint64_t)L, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)L * 8};
-  const cuuint32_t box[2] = {kTmaCols, (cuuint32_t)kTmaBox};
+  const cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)rows};
   const cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint8_t*>(trace), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
@@ -653,8 +641,9 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   prm.ld = 0;
   const int64_t resident = plan.sms;
   // chunks bound how far apart (in tokens) the CTAs counting different pairs of the same trace
-  // rows drift, i.e. the L2 footprint of the shared rows; the balanced split makes the count
-  // of chunks irrelevant to load balance
+  // rows drift, i.e. the L2 footprint of the shared rows: at 64 Mi DS-V3 tokens 21 chunks read
+  // 101 GB from DRAM per launch, 96 chunks 53 GB (31 GB algorithmic), same time; the stream-K
+  // tail keeps the split balanced for any count
   int64_t n_chunks = 96;
   if (const char* e = std::getenv("GIMBAL_DIRECT_CHUNKS")) n_chunks = std::max(1, std::atoi(e));
   n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
@@ -663,7 +652,7 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   prm.n_units = n_chunks * plan.n_groups;
   const int grid = (int)resident;
   CUtensorMap tmap;
-  if (encode_trace_map(&tmap, trace, T, plan.L)) {
+  if (encode_trace_map(&tmap, trace, T, plan.L, kTmaCols, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
     static const bool u16 = !(std::getenv("GIMBAL_TMA_MODE") && std::string(std::getenv("GIMBAL_TMA_MODE")) == "u15");
     auto kern = u16 ? count_tm_u15_tma_kernel<true> : count_tm_u15_tma_kernel<false>;

@@ -1,6 +1,7 @@
 // Internal helpers shared by the sm_100a translation units of libgimbal_gpu.so.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -97,10 +98,18 @@ bool direct_u15_supported(const Lm8Plan& plan, int id_bytes, const void* ids);
 cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, int64_t T,
                                     unsigned long long* E, cudaStream_t s);
 
-// tcgen05 int8 multi-hot contraction (mma_count.cu), n_e in [32, 128], top_k <= 8, on LM8 input.
+// Tensor map over a token-major top-8 uint8 trace as a [T][L] u64 matrix (ingest.cu).
+bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L, int cols, int rows);
+
+// tcgen05 int8 multi-hot contraction (mma_count.cu), n_e in (64, 128], top_k <= 8, on LM8 input.
 bool mma_count_supported(int L, int ne, int k);
 cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
                              unsigned long long* E, const uint32_t* flags, cudaStream_t s);
+// Same contraction reading the token-major trace through TMA (top-8 uint8, L even, 16-byte
+// aligned base; ids range-checked and repeated ids detected in the kernel).  Returns
+// cudaErrorNotSupported when the trace cannot be mapped.
+cudaError_t launch_count_mma_direct(int L, int ne, int sms, const uint8_t* trace, int64_t T,
+                                    unsigned long long* E, uint32_t* flags, cudaStream_t s);
 
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);

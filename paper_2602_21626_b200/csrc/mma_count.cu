@@ -35,9 +35,10 @@ constexpr int kRows = 128;                 // experts per tile row block (MMA M,
 constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
 constexpr int kMaxPairs = 4;               // accumulators: 4 x 128 TMEM columns
 constexpr int kStages = 2;
-constexpr int kThreads = 512;
-constexpr int kIdSlots = 3;                                 // TMA ring of LM8 word tiles
-constexpr int kIdSlotWords = (kMaxPairs + 1) * kTok;        // 5 layers x 128 tokens
+constexpr int kThreads = (kMaxPairs + 1) * kTok;           // one token-layer row per thread
+constexpr int kIdSlots = 3;                                 // TMA ring of id word tiles
+constexpr int kIdCols = kMaxPairs + 2;                      // token-major box: 6 layers (16-B aligned start)
+constexpr int kIdSlotWords = kIdCols * kTok;                // >= 5 layers x 128 tokens (layer-major)
 constexpr int kSmemBytes = kStages * (kMaxPairs + 1) * kTileBytes + kIdSlots * kIdSlotWords * 8;
 constexpr int kStageBytes = (kMaxPairs + 1) * kTileBytes;
 
@@ -49,7 +50,7 @@ struct MmaParams {
   int64_t range_tokens;  // tokens per unit
   int64_t T, ld;
   uint32_t idesc;
-  const uint32_t* flags;  // kFlagDuplicates set by the transposition of this chunk
+  uint32_t* flags;  // LM8: kFlagDuplicates from the transposition; token-major: id errors raised here
 };
 
 // Shared-memory matrix descriptor: no swizzle, MN-major.  Core matrix = 8 K-rows of 16 bytes;
@@ -86,9 +87,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-template <int K>
+// TM = ids come from the token-major trace through a 2-D tensor map (box: kIdCols layers from
+// l0 & ~1 x 128 tokens; row tt of the box is token t0 + tt), with range and repeat checks done
+// per row here; otherwise from the layer-major LM8 buffer X by 1-D bulk copies.
+template <int K, bool TM>
 __global__ void __launch_bounds__(kThreads, 1)
-    count_mma_kernel(MmaParams prm, const unsigned long long* __restrict__ X, unsigned long long* __restrict__ E) {
+    count_mma_kernel(const __grid_constant__ CUtensorMap tmap, MmaParams prm,
+                     const unsigned long long* __restrict__ X, unsigned long long* __restrict__ E) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kStages + 1];
   __shared__ uint64_t id_bars[kIdSlots];
@@ -113,7 +118,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = tmem_slot;
 
   const int ne = prm.ne;
-  const bool dup = (*prm.flags & kFlagDuplicates) != 0;  // repeated ids: count, else set
+  const bool dup = !TM && (*prm.flags & kFlagDuplicates) != 0;  // repeated ids: count, else set
+  bool bad = false;
   uint32_t it_global = 0;        // tiles issued by this CTA (stage = it % 2, commit index = it / 2)
   uint32_t final_waits = 0;      // commits of the end-of-unit barrier
   for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
@@ -129,7 +135,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // bulk copies into a 3-slot ring, two tiles ahead of construction.
     auto fetch = [&](int it) {
       const uint32_t slot = fill_count % kIdSlots;
-      if (threadIdx.x == 0) {
+      if (TM && threadIdx.x == 0) {
+        const int64_t t0 = t_begin + (int64_t)it * kTok;
+        mbar_arrive_expect_tx(&id_bars[slot], kTok * kIdCols * 8);
+        tma_load_2d(ids + slot * kIdSlotWords, &tmap, &id_bars[slot], l0 & ~1, (int)t0);
+      } else if (threadIdx.x == 0) {
         const int64_t t0 = t_begin + (int64_t)it * kTok;
         const uint32_t bytes = (uint32_t)(((min((int64_t)kTok, t_end - t0) * 8) + 15) & ~15ll);
         const uint32_t bar = smem_u32(&id_bars[slot]);
@@ -165,12 +175,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(row + c * 128) = z;
         if (t0 + tt < t_end) {
-          const unsigned long long w = w_tile[q * kTok + tt];
+          const unsigned long long w =
+              TM ? w_tile[tt * kIdCols + (l0 & 1) + q] : w_tile[q * kTok + tt];
+          bool count = dup;
+          if constexpr (TM) {
+            if (has_ge8(w, (uint32_t)ne)) {  // out-of-range ids: flag, leave the row empty
+              bad = true;
+              continue;
+            }
+            count = has_dup8(w);
+          }
 #pragma unroll
           for (int a = 0; a < K; ++a) {
             const uint32_t e = (uint32_t)(w >> (8 * a)) & 0xffu;
             uint8_t* p = row + (e >> 4) * 128 + (e & 15);
-            *p = dup ? (uint8_t)(*p + 1) : (uint8_t)1;
+            *p = count ? (uint8_t)(*p + 1) : (uint8_t)1;
           }
         }
       }
@@ -214,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
   }
+  if (TM && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(prm.flags, (uint32_t)kFlagIdOutOfRange);
   // drain: every commit on the stage barriers has been waited for except the last one per stage
   if (it_global >= 1) mbar_wait(&bars[(it_global - 1) & 1], ((it_global - 1) >> 1) & 1);
   if (it_global >= 2) mbar_wait(&bars[(it_global - 2) & 1], ((it_global - 2) >> 1) & 1);
@@ -223,15 +243,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int K>
-cudaError_t launch_k(const MmaParams& prm, const unsigned long long* X, unsigned long long* E, cudaStream_t s,
-                     int grid) {
-  auto kern = count_mma_kernel<K>;
+template <int K, bool TM>
+cudaError_t launch_k(const CUtensorMap& tmap, const MmaParams& prm, const unsigned long long* X,
+                     unsigned long long* E, cudaStream_t s, int grid) {
+  auto kern = count_mma_kernel<K, TM>;
   const int smem = kSmemBytes;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kThreads, smem, s>>>(prm, X, E);
+  kern<<<grid, kThreads, smem, s>>>(tmap, prm, X, E);
   return cudaGetLastError();
+}
+
+// Units = (group of kMaxPairs pairs, token range): ranges so that groups x ranges fills the SMs;
+// s32 accumulators hold per-unit counts up to tokens * k^2 < 2^31.
+MmaParams make_params(int L, int ne, int k, int sms, int64_t T, int64_t ld, uint32_t* flags, int* grid) {
+  MmaParams prm;
+  prm.L = L;
+  prm.ne = ne;
+  prm.N = (ne + 15) / 16 * 16;
+  prm.P = kMaxPairs;
+  prm.n_groups = (L - 1 + prm.P - 1) / prm.P;
+  prm.T = T;
+  prm.ld = ld;
+  prm.flags = flags;
+  // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
+  prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+  int64_t ranges = std::max<int64_t>(1, sms / prm.n_groups);
+  const int64_t cap = ((int64_t)1 << 31) / ((int64_t)k * k) - kTok;
+  int64_t per = (T + ranges - 1) / ranges;
+  if (per > cap) per = cap;
+  per = (per + kTok - 1) / kTok * kTok;
+  ranges = (T + per - 1) / per;
+  prm.range_tokens = per;
+  prm.n_units = ranges * prm.n_groups;
+  *grid = (int)std::min<int64_t>(prm.n_units, sms);
+  return prm;
 }
 
 }  // namespace
@@ -244,39 +290,31 @@ bool mma_count_supported(int L, int ne, int k) { return L > 1 && k >= 1 && k <= 
 cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long long* X, int64_t T, int64_t ld,
                              unsigned long long* E, const uint32_t* flags, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  MmaParams prm;
-  prm.L = L;
-  prm.ne = ne;
-  prm.N = (ne + 15) / 16 * 16;
-  prm.P = kMaxPairs;
-  prm.n_groups = (L - 1 + prm.P - 1) / prm.P;
-  prm.T = T;
-  prm.ld = ld;
-  prm.flags = flags;
-  // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
-  prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
-  // one unit per CTA: token ranges so that groups x ranges fills the SMs; s32 accumulators hold
-  // per-unit counts up to tokens * k^2 < 2^31
-  int64_t ranges = std::max<int64_t>(1, sms / prm.n_groups);
-  const int64_t cap = ((int64_t)1 << 31) / ((int64_t)k * k) - kTok;
-  int64_t per = (T + ranges - 1) / ranges;
-  if (per > cap) per = cap;
-  per = (per + kTok - 1) / kTok * kTok;
-  ranges = (T + per - 1) / per;
-  prm.range_tokens = per;
-  prm.n_units = ranges * prm.n_groups;
-  const int grid = (int)std::min<int64_t>(prm.n_units, sms);
+  int grid = 0;
+  const MmaParams prm = make_params(L, ne, k, sms, T, ld, const_cast<uint32_t*>(flags), &grid);
+  CUtensorMap none{};
   switch (k) {
-    case 1: return launch_k<1>(prm, X, E, s, grid);
-    case 2: return launch_k<2>(prm, X, E, s, grid);
-    case 3: return launch_k<3>(prm, X, E, s, grid);
-    case 4: return launch_k<4>(prm, X, E, s, grid);
-    case 5: return launch_k<5>(prm, X, E, s, grid);
-    case 6: return launch_k<6>(prm, X, E, s, grid);
-    case 7: return launch_k<7>(prm, X, E, s, grid);
-    case 8: return launch_k<8>(prm, X, E, s, grid);
+    case 1: return launch_k<1, false>(none, prm, X, E, s, grid);
+    case 2: return launch_k<2, false>(none, prm, X, E, s, grid);
+    case 3: return launch_k<3, false>(none, prm, X, E, s, grid);
+    case 4: return launch_k<4, false>(none, prm, X, E, s, grid);
+    case 5: return launch_k<5, false>(none, prm, X, E, s, grid);
+    case 6: return launch_k<6, false>(none, prm, X, E, s, grid);
+    case 7: return launch_k<7, false>(none, prm, X, E, s, grid);
+    case 8: return launch_k<8, false>(none, prm, X, E, s, grid);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_count_mma_direct(int L, int ne, int sms, const uint8_t* trace, int64_t T,
+                                    unsigned long long* E, uint32_t* flags, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  CUtensorMap tmap;
+  if (!mma_count_supported(L, ne, 8) || !encode_trace_map(&tmap, trace, T, L, kIdCols, kTok))
+    return cudaErrorNotSupported;
+  int grid = 0;
+  const MmaParams prm = make_params(L, ne, 8, sms, T, 0, flags, &grid);
+  return launch_k<8, true>(tmap, prm, nullptr, E, s, grid);
 }
 
 }  // namespace gimbal_gpu

@@ -45,4 +45,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// ---- packed top-8 uint8 id words (one u64 per token-layer) ----
+
+__device__ __forceinline__ uint32_t id_byte(unsigned long long w, int a) {
+  return (uint32_t)(w >> (8 * a)) & 0xffu;
+}
+
+// true when two of the eight id bytes are equal (every pair compared once: within each half at
+// byte distance 1 and 2, across the halves at all four rotations; "has a zero byte" test)
+__device__ __forceinline__ bool has_dup8(unsigned long long x) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  auto z = [](uint32_t v) { return (v - 0x01010101u) & ~v & 0x80808080u; };
+  uint32_t acc = z(lo ^ __byte_perm(lo, 0, 0x0321)) | z(lo ^ __byte_perm(lo, 0, 0x1032));
+  acc |= z(hi ^ __byte_perm(hi, 0, 0x0321)) | z(hi ^ __byte_perm(hi, 0, 0x1032));
+  acc |= z(lo ^ hi) | z(lo ^ __byte_perm(hi, 0, 0x0321));
+  acc |= z(lo ^ __byte_perm(hi, 0, 0x1032)) | z(lo ^ __byte_perm(hi, 0, 0x2103));
+  return acc != 0u;
+}
+
+// true when some id byte is >= n (1 <= n <= 128): bytes below 128 gain bit 7 from + (128 - n)
+// exactly when they reach n, bytes from 128 up carry it already
+__device__ __forceinline__ bool has_ge8(unsigned long long w, uint32_t n) {
+  const unsigned long long add = (unsigned long long)(128u - n) * 0x0101010101010101ull;
+  return (((w & 0x7f7f7f7f7f7f7f7full) + add) | w) & 0x8080808080808080ull;
+}
+
 }  // namespace gimbal_gpu

@@ -102,6 +102,40 @@ def test_direct_count_layouts(G, orc, L, T, offset):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+@pytest.mark.parametrize("L,ne,T,offset,dup", [(48, 128, 70001, 0, False), (48, 128, 3000, 8, False),
+                                               (48, 128, 5000, 0, True), (10, 100, 9000, 0, True),
+                                               (9, 128, 4000, 0, False)])
+def test_mma_count_layouts(G, orc, L, ne, T, offset, dup):
+    """n_e in (64, 128], top-8 uint8 traces go through the tcgen05 contraction: straight from the
+    token-major rows by TMA when L is even and the base 16-byte aligned (ids range-checked and
+    repeats detected per row in the kernel), through the layer-major transposition otherwise."""
+    k = 8
+    topo = G.MoeTopology(L, ne, k, 4)
+    rng = np.random.default_rng(T + ne)
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    if dup:
+        ids[::7, :, 1] = ids[::7, :, 0]  # every 7th token repeats its first id
+    buf = torch.empty(T * L * k + offset, dtype=torch.uint8, device="cuda")
+    dev = buf[offset:].view(T, L, k)
+    dev.copy_(torch.from_numpy(ids))
+    _, (A, E, W) = _stats_gpu(G, topo, dev)
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
+
+
+@pytest.mark.parametrize("ne,bad", [(128, 128), (128, 255), (100, 100)])
+def test_mma_direct_out_of_range(G, ne, bad):
+    L, k = 6, 8
+    topo = G.MoeTopology(L, ne, k, 4)
+    ids = np.zeros((1000, L, k), np.uint8)
+    ids[:, :, :] = np.arange(k, dtype=np.uint8)
+    ids[777, 3, 5] = bad
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(torch.from_numpy(ids).cuda())
+    with pytest.raises(IndexError):
+        s.read()
+
+
 @pytest.mark.parametrize("dup", [False, True])
 def test_counter_overflow_paths(G, dup):
     """Hot cells far beyond 2^15 / 2^16 per work unit (guarded 15-bit counters at n_e = 256,
