@@ -51,9 +51,7 @@ ATOMS_RANDOM_PEAK = 2.553e12
 TRAFFIC = {"dsv3": {"bytes": 62.633288e9 + 1.774051e9, "tokens_in_launch": 67108864,
                     "source": "profiles/r1b_ncu_count_dsv3.md"},
            "qwen3": {"bytes": 19.263587e9 + 5.747456e6, "tokens_in_launch": 33554432,
-                     "source": "profiles/r1b_ncu_count_qwen3.md"},
-           "dsv2lite": {"bytes": 3.627678e9 + 4.321024e6, "tokens_in_launch": 16777216,
-                        "source": "profiles/r1b_ncu_count_dsv2lite.md"}}
+                     "source": "profiles/r1b_ncu_count_qwen3.md"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 REASON_BITS = {
@@ -86,6 +84,8 @@ def count_kernel(ne, k):
     whole-pair shared tables below, 15-bit halves or row splits above."""
     if ne == 256 and k == 8:
         return "count_tm_u15_tma_kernel<true> (TMA-staged ids, 16-bit halves, drained)", "atomics"
+    if ne == 64 and k <= 8:
+        return "count_mma_stack_kernel (tcgen05.mma kind::i8, two 64-expert layers per 128-row operand)", "tensor"
     if 64 < ne <= 128:
         return "count_mma_kernel (tcgen05.mma kind::i8, TMEM accumulators)", "tensor"
     if ne * ne * 4 <= 200 * 1024:
@@ -333,8 +333,14 @@ def main():
                 "algorithmic_bytes_per_launch": alg_bytes, "share_of_step": count_total_ms / args.steps / ms}
         if engine == "tensor":
             # dense int8 multiply-adds the tcgen05 contraction issues (n_e rounded up to the MMA N)
-            n_mma = (ne + 15) // 16 * 16
-            ops = 2.0 * tok_per_launch * (L - 1) * 128 * n_mma / (launch_ms * 1e-3)
+            if ne == 64:  # stacked: M = 128 (layers l, l+2) x N = 64 per two pairs (mma_stack.cu groups)
+                groups = -(-(L - 1) // 16)
+                ppg = -(-(L - 1) // groups)
+                n_ins = sum((min(ppg, L - 1 - g0) + 1) // 2 for g0 in range(0, L - 1, ppg))
+                ops = 2.0 * tok_per_launch * n_ins * 128 * 64 / (launch_ms * 1e-3)
+            else:
+                n_mma = (ne + 15) // 16 * 16
+                ops = 2.0 * tok_per_launch * (L - 1) * 128 * n_mma / (launch_ms * 1e-3)
             bf16 = peaks_all().get("bf16_tflops")
             tpeak = 2.0 * bf16 * 1e12 if bf16 else 4.5e15
             roof["tensor_ceiling"] = {

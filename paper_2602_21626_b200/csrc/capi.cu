@@ -99,6 +99,7 @@ struct gimbal_stats_s {
   gimbal_topology topo{};
   int device = 0;
   int sms = 148;
+  int smem_optin = 0;
   StatsPlan plan;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
@@ -123,6 +124,7 @@ struct gimbal_stats_s {
   static constexpr int64_t kLm8BufferBytes = (int64_t)4 << 30;
   Lm8Plan lm8_plan;
   bool use_mma = false;  // tcgen05 contraction instead of shared-memory counting (n_e <= 128)
+  bool use_stack = false;  // tcgen05 contraction with two 64-expert layers per operand
   cudaStream_t t_stream = nullptr;
   unsigned long long* lm8[kStages] = {nullptr, nullptr};
   int64_t lm8_tokens = 0;
@@ -223,6 +225,19 @@ struct gimbal_stats_s {
 
   int count_device(const void* ids, int id_bytes, int64_t n) {
     const int L = topo.n_layers;
+    if (use_stack && mma_stack_supported(L, topo.n_experts, topo.top_k, id_bytes, ids) &&
+        !std::getenv("GIMBAL_NO_DIRECT")) {
+      // 64-expert layers: two layers per 128-row tensor-core operand, straight from the trace
+      GIMBAL_TRY(timing_begin());
+      const cudaError_t e = launch_count_mma_stack(L, topo.n_experts, topo.top_k, sms, smem_optin,
+                                                   static_cast<const uint8_t*>(ids), n, dE, dflags, stream);
+      if (e != cudaErrorNotSupported) {
+        GIMBAL_CUDA_TRY(e);
+        GIMBAL_TRY(timing_end());
+        return GIMBAL_OK;
+      }
+      cudaGetLastError();  // shape does not fit the stacked kernel: fall through (timing slot reused)
+    }
     if (!use_mma && direct_u15_supported(lm8_plan, id_bytes, ids) && !std::getenv("GIMBAL_NO_DIRECT")) {
       // every uint8 id is a valid expert at n_e = 256: no validation / transposition pass
       GIMBAL_TRY(timing_begin());
@@ -353,7 +368,9 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
     const char* path = std::getenv("GIMBAL_COUNT_PATH");
     const bool want_mma = !(path && std::string(path) == "atomic");
     h->use_mma = want_mma && mma_count_supported(topo->n_layers, topo->n_experts, topo->top_k);
+    h->use_stack = want_mma && !(path && std::string(path) == "lm8");
   }
+  h->smem_optin = optin;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->t_stream, cudaStreamNonBlocking) != cudaSuccess ||

@@ -111,6 +111,13 @@ cudaError_t launch_count_mma(int L, int ne, int k, int sms, const unsigned long 
 cudaError_t launch_count_mma_direct(int L, int ne, int sms, const uint8_t* trace, int64_t T,
                                     unsigned long long* E, uint32_t* flags, cudaStream_t s);
 
+// Same contraction for 64-expert layers with two layers stacked per 128-row operand, reading the
+// token-major uint8 trace (16-byte aligned) by bulk copies (mma_stack.cu).  cudaErrorNotSupported
+// when the shape does not fit.
+bool mma_stack_supported(int L, int ne, int k, int id_bytes, const void* ids);
+cudaError_t launch_count_mma_stack(int L, int ne, int k, int sms, int max_smem, const uint8_t* trace, int64_t T,
+                                   unsigned long long* E, uint32_t* flags, cudaStream_t s);
+
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_count_activation(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,

@@ -123,6 +123,42 @@ def test_mma_count_layouts(G, orc, L, ne, T, offset, dup):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+@pytest.mark.parametrize("L,k,T,offset,dup", [(26, 6, 70001, 0, False), (26, 6, 1, 0, False), (26, 6, 65, 0, True),
+                                              (2, 8, 5000, 0, False), (3, 1, 4097, 0, False), (17, 6, 3000, 0, False),
+                                              (18, 5, 3000, 0, True), (34, 3, 9000, 0, False),
+                                              (64, 8, 2000, 0, False), (26, 6, 3000, 8, False)])
+def test_mma_stack_layouts(G, orc, L, k, T, offset, dup):
+    """64-expert uint8 traces go through the stacked tcgen05 contraction (two layers per 128-row
+    operand, rows bulk-copied from the token-major trace): odd and even pair counts per group,
+    several groups, ragged tails shorter than one 16-byte copy unit, repeated ids; a base that is
+    not 16-byte aligned falls back to the shared-memory counters."""
+    ne = 64
+    topo = G.MoeTopology(L, ne, k, 8)
+    rng = np.random.default_rng(T * 7 + L)
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    if dup and k > 1:
+        ids[::5, :, 1] = ids[::5, :, 0]
+    buf = torch.empty(T * L * k + offset, dtype=torch.uint8, device="cuda")
+    dev = buf[offset:].view(T, L, k)
+    dev.copy_(torch.from_numpy(ids))
+    _, (A, E, W) = _stats_gpu(G, topo, dev)
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
+
+
+@pytest.mark.parametrize("bad", [64, 255])
+def test_mma_stack_out_of_range(G, bad):
+    L, ne, k = 26, 64, 6
+    topo = G.MoeTopology(L, ne, k, 8)
+    ids = np.zeros((3000, L, k), np.uint8)
+    ids[:, :, :] = np.arange(k, dtype=np.uint8)
+    ids[2999, 25, 5] = bad
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(torch.from_numpy(ids).cuda())
+    with pytest.raises(IndexError):
+        s.read()
+
+
 @pytest.mark.parametrize("ne,bad", [(128, 128), (128, 255), (100, 100)])
 def test_mma_direct_out_of_range(G, ne, bad):
     L, k = 6, 8
