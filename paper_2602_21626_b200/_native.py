@@ -10,7 +10,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgimbal_gpu.so")
+# GIMBAL_LIB selects another build of the same library (A/B kernel experiments on the GPU box)
+LIB_PATH = os.environ.get("GIMBAL_LIB") or os.path.join(HERE, "lib", "libgimbal_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "gimbal_gpu.h")
 
 OK, INVALID_ARGUMENT, CUDA_ERROR, NCCL_ERROR, OVERFLOW, OUT_OF_RANGE, NOT_SUPPORTED = range(7)
