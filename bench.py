@@ -87,7 +87,7 @@ def count_kernel(ne, k):
     if ne == 64 and k <= 8:
         return "count_mma_stack_kernel (tcgen05.mma kind::i8, two 64-expert layers per 128-row operand)", "tensor"
     if 64 < ne <= 128:
-        return "count_mma_kernel (tcgen05.mma kind::i8, M=128 x N=256 per two pairs, TMEM accumulators)", "tensor"
+        return "count_mma_kernel (tcgen05.mma kind::i8, TMEM accumulators)", "tensor"
     if ne * ne * 4 <= 200 * 1024:
         return "count_lm8_pairs_kernel", "atomics"
     if ne % 64 == 0 and ne * ne * 2 <= 200 * 1024:
@@ -338,9 +338,9 @@ def main():
                 ppg = -(-(L - 1) // groups)
                 n_ins = sum((min(ppg, L - 1 - g0) + 1) // 2 for g0 in range(0, L - 1, ppg))
                 ops = 2.0 * tok_per_launch * n_ins * 128 * 64 / (launch_ms * 1e-3)
-            else:  # M = 128 (odd layer) x N = 256 (two even layers) per two pairs, groups of 4 pairs
-                n_ins = sum((min(4, L - 1 - g0) + 1) // 2 for g0 in range(0, L - 1, 4))
-                ops = 2.0 * tok_per_launch * n_ins * 128 * 256 / (launch_ms * 1e-3)
+            else:  # M = 128 (experts of layer l, padded) x N = n_e rounded to 16, per pair
+                n_mma = (ne + 15) // 16 * 16
+                ops = 2.0 * tok_per_launch * (L - 1) * 128 * n_mma / (launch_ms * 1e-3)
             bf16 = peaks_all().get("bf16_tflops")
             tpeak = 2.0 * bf16 * 1e12 if bf16 else 4.5e15
             roof["tensor_ceiling"] = {
