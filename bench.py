@@ -78,11 +78,13 @@ def peaks_all():
         return {}
 
 
-def count_kernel(ne, k):
+def count_kernel(ne, k, L=58):
     """(kernel, engine) that counts E for this shape on a device-resident uint8 trace (capi.cu
     count_device): the TMA-staged direct kernel at n_e = 256 / top-8, tcgen05 for n_e in (64, 128],
     whole-pair shared tables below, 15-bit halves or row splits above."""
     if ne == 256 and k == 8:
+        if os.environ.get("GIMBAL_COUNT_PATH") == "fp4" and L % 2 == 0:
+            return "count_fp4_kernel (tcgen05.mma kind::mxf4 block-scaled FP4, K-major nibble operands)", "tensor_fp4"
         return "count_tm_u15_tma_kernel<true> (TMA-staged ids, 16-bit halves, drained)", "atomics"
     if ne == 64 and k <= 8:
         return "count_mma_stack_kernel (tcgen05.mma kind::i8, two 64-expert layers per 128-row operand)", "tensor"
@@ -322,7 +324,7 @@ def main():
         peak, peak_kind = peaks()
         achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
         upd = tok_per_launch * (L - 1) * k * k / (launch_ms * 1e-3)
-        kernel, engine = count_kernel(ne, k)
+        kernel, engine = count_kernel(ne, k, L)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": (TRAFFIC[args.config]["bytes"] / TRAFFIC[args.config]["tokens_in_launch"] * tok_per_launch
                             if args.config in TRAFFIC else None),
@@ -331,7 +333,18 @@ def main():
                 "kernel": kernel,
                 "launch_ms": launch_ms, "launches_per_step": launches_per_step,
                 "algorithmic_bytes_per_launch": alg_bytes, "share_of_step": count_total_ms / args.steps / ms}
-        if engine == "tensor":
+        if engine == "tensor_fp4":
+            # dense FP4 multiply-adds issued: per pair and token, 2 halves x M = 128 x N = 256
+            ops = 2.0 * tok_per_launch * (L - 1) * 256 * 256 / (launch_ms * 1e-3)
+            bf16 = peaks_all().get("bf16_tflops")
+            tpeak = 4.0 * bf16 * 1e12 if bf16 else 9.0e15
+            roof["tensor_ceiling"] = {
+                "bound": "tensor", "achieved": ops / 1e12, "peak": tpeak / 1e12, "unit": "TFLOP/s (dense FP4)",
+                "frac": ops / tpeak,
+                "peak_source": ("4 x measured bf16 dense (MEASURED_PEAKS.json bf16_tflops; dense FP4 = 4x bf16 "
+                                "on sm_100)" if bf16 else "B200_PROFILING.md fallback 9 PFLOP/s"),
+                "useful_updates_per_s": upd}
+        elif engine == "tensor":
             # dense int8 multiply-adds the tcgen05 contraction issues (n_e rounded up to the MMA N)
             if ne == 64:  # stacked: M = 128 (layers l, l+2) x N = 64 per two pairs (mma_stack.cu groups)
                 groups = -(-(L - 1) // 16)

@@ -125,6 +125,7 @@ struct gimbal_stats_s {
   Lm8Plan lm8_plan;
   bool use_mma = false;  // tcgen05 contraction instead of shared-memory counting (n_e <= 128)
   bool use_stack = false;  // tcgen05 contraction with two 64-expert layers per operand
+  bool use_fp4 = false;    // block-scaled FP4 tcgen05 contraction (256 experts, top-8)
   cudaStream_t t_stream = nullptr;
   unsigned long long* lm8[kStages] = {nullptr, nullptr};
   int64_t lm8_tokens = 0;
@@ -237,6 +238,18 @@ struct gimbal_stats_s {
         return GIMBAL_OK;
       }
       cudaGetLastError();  // shape does not fit the stacked kernel: fall through (timing slot reused)
+    }
+    if (use_fp4 && fp4_count_supported(L, topo.n_experts, topo.top_k, id_bytes, ids, n) &&
+        !std::getenv("GIMBAL_NO_DIRECT")) {
+      // 256 experts, top-8: block-scaled FP4 tensor-core contraction straight from the trace
+      GIMBAL_TRY(timing_begin());
+      const cudaError_t e = launch_count_fp4(L, sms, static_cast<const uint8_t*>(ids), n, dE, stream);
+      if (e != cudaErrorNotSupported) {
+        GIMBAL_CUDA_TRY(e);
+        GIMBAL_TRY(timing_end());
+        return GIMBAL_OK;
+      }
+      cudaGetLastError();  // not mappable: fall through (timing slot reused)
     }
     if (!use_mma && direct_u15_supported(lm8_plan, id_bytes, ids) && !std::getenv("GIMBAL_NO_DIRECT")) {
       // every uint8 id is a valid expert at n_e = 256: no validation / transposition pass
@@ -364,11 +377,13 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
   };
   h->lm8_plan = make_lm8_plan(topo->n_layers, topo->n_experts, topo->top_k, h->sms, optin);
   {
-    // GIMBAL_COUNT_PATH=atomic|mma overrides the default (tensor cores where supported)
+    // GIMBAL_COUNT_PATH=atomic|lm8|split|fp4 overrides the default (tensor cores where supported)
     const char* path = std::getenv("GIMBAL_COUNT_PATH");
     const bool want_mma = !(path && std::string(path) == "atomic");
     h->use_mma = want_mma && mma_count_supported(topo->n_layers, topo->n_experts, topo->top_k);
     h->use_stack = want_mma && !(path && std::string(path) == "lm8");
+    // opt-in: measured slower than the atomic u15 kernel at DS-V3 (fp4_count.cu header)
+    h->use_fp4 = path && std::string(path) == "fp4";
   }
   h->smem_optin = optin;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||

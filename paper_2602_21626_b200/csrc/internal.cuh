@@ -118,6 +118,12 @@ bool mma_stack_supported(int L, int ne, int k, int id_bytes, const void* ids);
 cudaError_t launch_count_mma_stack(int L, int ne, int k, int sms, int max_smem, const uint8_t* trace, int64_t T,
                                    unsigned long long* E, uint32_t* flags, cudaStream_t s);
 
+// Block-scaled FP4 tensor-core contraction for 256-expert top-8 uint8 traces (fp4_count.cu):
+// L even, 16-byte aligned base, T < 2^31.  cudaErrorNotSupported when the trace cannot be mapped.
+bool fp4_count_supported(int L, int ne, int k, int id_bytes, const void* ids, int64_t T);
+cudaError_t launch_count_fp4(int L, int sms, const uint8_t* trace, int64_t T, unsigned long long* E,
+                             cudaStream_t s);
+
 cudaError_t launch_count_pairs(const StatsPlan& plan, const void* ids, int id_bytes, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_count_activation(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,

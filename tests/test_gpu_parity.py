@@ -146,6 +146,22 @@ def test_mma_stack_layouts(G, orc, L, k, T, offset, dup):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+@pytest.mark.parametrize("L,T,dup", [(58, 70001, False), (58, 129, False), (2, 5000, False), (58, 5000, True)])
+def test_fp4_count_path(G, orc, monkeypatch, L, T, dup):
+    """The opt-in block-scaled FP4 tensor-core contraction (GIMBAL_COUNT_PATH=fp4, 256 experts,
+    top-8) is bit-exact too, repeated ids included (those tokens go straight to the u64 tensor)."""
+    monkeypatch.setenv("GIMBAL_COUNT_PATH", "fp4")
+    ne, k = 256, 8
+    topo = G.MoeTopology(L, ne, k, 8)
+    rng = np.random.default_rng(T + L)
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    if dup:
+        ids[::3, :, 1] = ids[::3, :, 0]
+    _, (A, E, W) = _stats_gpu(G, topo, torch.from_numpy(ids).cuda())
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
+
+
 @pytest.mark.parametrize("bad", [64, 255])
 def test_mma_stack_out_of_range(G, bad):
     L, ne, k = 26, 64, 6
