@@ -260,6 +260,11 @@ def main():
     torch.cuda.set_device(local)
     dist_on = world > 1 or args.dist_path
     if dist_on:
+        if world == 1:  # --dist-path without torchrun: a one-rank group on 127.0.0.1
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L, ne, k, g, T, C, desc = CONFIGS[args.config]
     if args.tokens:

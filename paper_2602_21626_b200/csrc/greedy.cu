@@ -5,15 +5,16 @@
 // the expert's activation column to that GPU.  On the flat activation an expert of layer l with
 // A > 0 has home row l and only changes row l; an expert with A = 0 (home row 0) changes nothing
 // and sorts after every positive expert.  So until some GPU reaches its cardinality cap m/g, the
-// walk decomposes into independent per-layer walks.  The kernel therefore
-//   A. runs every layer's walk in parallel (one thread per layer, loads in registers) ignoring
-//      the cap, recording each position's tentative GPU;
-//   B. finds s*, the first position in the global order whose tentative GPU would already be full
-//      (warp ballots over the running per-GPU counts);
-//   C. rebuilds the loads/counts at s* and finishes positions >= s* (including all A = 0 experts)
-//      with the exact sequential walk.
-// Positions before s* are provably identical to the sequential walk; the tail is exact by
-// construction, so the result is the reference's placement for every input.
+// walk decomposes into independent per-layer walks, and after that it does again for as long as
+// the set of full GPUs stays the same.  The kernel groups the positions by layer once, then runs
+// rounds, each from the first unplaced position with the current full set F:
+//   A. every layer's walk in parallel (one thread per layer, its load row in registers) over the
+//      GPUs outside F, cap ignored, recording each position's tentative GPU;
+//   B. s*, the first position whose tentative GPU would already be full (each warp counts a
+//      segment per GPU with ballots, then scans it with the headroom the earlier segments leave);
+//   C. commits positions before s*; the GPU at s* is now full.
+// At most g rounds; positions before each s* are provably identical to the sequential walk.  The
+// A = 0 experts (no load change, sorted last) finish with the exact sequential walk.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -112,23 +113,41 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t n_pos = min((int64_t)s_npos, n_valid);
 
   if constexpr (G > 0) {
-    // sorted keys and a per-position layer map staged in shared memory (the launcher only picks
-    // this path when they fit); layer 0xff marks padding
+    // sorted keys, each position's layer, its tentative GPU, and per-layer position lists staged
+    // in shared memory (the launcher only picks this path when they fit)
     unsigned long long* skeys = reinterpret_cast<unsigned long long*>(counts + 4 * ((g + 3) / 4));
     const int64_t n_pad = (n_pos + 15) & ~15ll;
-    uint8_t* lay = reinterpret_cast<uint8_t*>(skeys + n_pad);
+    uint16_t* list = reinterpret_cast<uint16_t*>(skeys + n_pad);  // positions grouped by layer, ascending
+    uint8_t* lay = reinterpret_cast<uint8_t*>(list + n_pad);
     tent = lay + n_pad;
+    __shared__ int l_start[kMaxLayers + 1];
+    __shared__ long long w_star[kThreads / 32];
+    __shared__ int w_cnt[kThreads / 32][32];
+    __shared__ uint32_t s_full;
+    for (int l = threadIdx.x; l <= L; l += blockDim.x) l_start[l] = 0;
+    __syncthreads();
     for (int64_t i = threadIdx.x; i < n_pad; i += blockDim.x) {
       const unsigned long long key = i < n_pos ? keys[i] : 0ull;
       skeys[i] = key;
-      lay[i] = i < n_pos ? (uint8_t)(((unsigned long long)key_expert(key) * inv_ne) >> 40) : (uint8_t)0xff;
+      const int l = i < n_pos ? (int)(((unsigned long long)key_expert(key) * inv_ne) >> 40) : 0xff;
+      lay[i] = (uint8_t)l;
+      if (i < n_pos) atomicAdd(&l_start[l + 1], 1);
     }
     __syncthreads();
-    // visits this thread's layer positions in [0, end) in order: 16 layer bytes per shared load,
-    // exact zero-byte test on (word ^ layer) picks the matches
-    auto for_layer = [&](int l, int64_t end, auto&& body) {
+    if (threadIdx.x == 0) {
+      for (int l = 0; l < L; ++l) l_start[l + 1] += l_start[l];
+      uint32_t f = 0;
+      for (int p = 0; p < G; ++p) f |= (counts[p] >= cap ? 1u : 0u) << p;
+      s_full = f;
+    }
+    __syncthreads();
+    // one pass per layer thread over the layer map (16 layer bytes per shared load, exact
+    // zero-byte test on word ^ layer) writes its positions in ascending order
+    if (threadIdx.x < L) {
+      const int l = threadIdx.x;
       const uint32_t lw = 0x01010101u * (uint32_t)l;
-      for (int64_t c = 0; c < end; c += 16) {
+      int w = l_start[l];
+      for (int64_t c = 0; c < n_pos; c += 16) {
         const uint4 w4 = *reinterpret_cast<const uint4*>(lay + c);
         const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
@@ -136,92 +155,140 @@ __global__ void __launch_bounds__(kThreads)
           const uint32_t x = ws[q] ^ lw;
           uint32_t z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);  // 0x80 where byte == 0
           while (z) {
-            const int64_t pos = c + q * 4 + ((__ffs(z) - 1) >> 3);
+            list[w++] = (uint16_t)(c + q * 4 + ((__ffs(z) - 1) >> 3));
             z &= z - 1;
-            if (pos < end) body(pos);
           }
         }
       }
-    };
-    // ---- A: per-layer walks, cap ignored (one thread per layer, its load row in registers) ----
-    if (threadIdx.x < L) {
-      const int l = threadIdx.x;
-      unsigned long long v[G];
-#pragma unroll
-      for (int p = 0; p < G; ++p) v[p] = load[l * G + p];
-      for_layer(l, n_pos, [&](int64_t i) {
-        const unsigned long long a = key_total(skeys[i]);
-        int best = 0;
-#pragma unroll
-        for (int p = 1; p < G; ++p)
-          if (v[p] < v[best]) best = p;
-#pragma unroll
-        for (int p = 0; p < G; ++p) v[p] += (p == best) ? a : 0ull;
-        tent[i] = (uint8_t)best;
-      });
     }
     __syncthreads();
-    // ---- B: first position whose tentative GPU is already at its cap ----
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      int room = lane < G ? cap - counts[lane] : 0;  // lane p tracks GPU p's remaining headroom
+    // Rounds: with the set F of full GPUs fixed, every other GPU has room, so the walk is again a
+    // set of independent per-layer walks.  A round runs them from the first unplaced position,
+    // finds the first position whose GPU would overflow and commits everything before it; that
+    // GPU is then full, so there are at most g rounds and every committed position is exact.
+    const int l_me = threadIdx.x;
+    int cursor = l_me < L ? l_start[l_me] : 0;  // first uncommitted entry of this layer's list
+    const int l_end = l_me < L ? l_start[l_me + 1] : 0;
+    int64_t pos = 0;
+    while (pos < n_pos) {
+      const uint32_t full = s_full;
+      // ---- A: per-layer walks over the GPUs outside F (cap ignored), tentative GPUs ----
+      if (l_me < L) {
+        unsigned long long v[G];
+#pragma unroll
+        for (int p = 0; p < G; ++p) v[p] = load[l_me * G + p];
+        for (int idx = cursor; idx < l_end; ++idx) {
+          const int i = list[idx];
+          const unsigned long long a = key_total(skeys[i]);
+          int best = -1;
+          unsigned long long bv = 0ull;
+#pragma unroll
+          for (int p = 0; p < G; ++p)
+            if (!((full >> p) & 1u) && (best < 0 || v[p] < bv)) {
+              best = p;
+              bv = v[p];
+            }
+#pragma unroll
+          for (int p = 0; p < G; ++p) v[p] += (p == best) ? a : 0ull;
+          tent[i] = (uint8_t)best;
+        }
+      }
+      __syncthreads();
+      // ---- B: first position >= pos whose tentative GPU is already at its cap.  Each warp
+      // counts its segment's positions per GPU, then scans the segment with the headroom left
+      // by the segments before it; the earliest overflow over all warps is the round's end ----
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      const int n_warps = blockDim.x >> 5;
+      const int64_t seg = ((n_pos - pos + n_warps - 1) / n_warps + 31) & ~31ll;
+      const int64_t s_lo = min(n_pos, pos + warp * seg), s_hi = min(n_pos, s_lo + seg);
+      {
+        int taken = 0;  // lane q: positions of this segment on GPU q
+        for (int64_t base = s_lo; base < s_hi; base += 32) {
+          const int64_t i = base + lane;
+          const int p = i < s_hi ? tent[i] : -1;
+#pragma unroll
+          for (int q = 0; q < G; ++q) {
+            const unsigned b = __ballot_sync(0xffffffffu, p == q);
+            if (lane == q) taken += __popc(b);
+          }
+        }
+        w_cnt[warp][lane] = taken;
+      }
+      __syncthreads();
+      {
+        int room = 0;  // lane p: GPU p's headroom at the start of this segment
+        if (lane < G) {
+          room = cap - counts[lane];
+          for (int w2 = 0; w2 < warp; ++w2) room -= w_cnt[w2][lane];
+        }
+        long long star = n_pos;
+        for (int64_t base = s_lo; base < s_hi; base += 32) {
+          const int64_t i = base + lane;
+          const int p = i < s_hi ? tent[i] : -1;
+          int used_before = 0;  // earlier positions of this chunk on the same GPU
+          int taken = 0;        // lane q: positions of this chunk on GPU q
+#pragma unroll
+          for (int q = 0; q < G; ++q) {
+            const unsigned b = __ballot_sync(0xffffffffu, p == q);
+            if (p == q) used_before = __popc(b & ((1u << lane) - 1u));
+            if (lane == q) taken = __popc(b);
+          }
+          const int room_p = __shfl_sync(0xffffffffu, room, p < 0 ? 0 : p);
+          const unsigned vb = __ballot_sync(0xffffffffu, p >= 0 && used_before >= room_p);
+          if (vb) {  // the earliest position of this segment whose GPU would hold cap experts
+            star = base + __ffs(vb) - 1;
+            break;
+          }
+          room -= taken;
+        }
+        if (lane == 0) w_star[warp] = star;
+      }
+      __syncthreads();
       long long star = n_pos;
-      for (int64_t base = 0; base < n_pos; base += 32) {
-        const int64_t i = base + lane;
-        const int p = i < n_pos ? tent[i] : -1;
-        int used_before = 0;  // earlier positions of this chunk on the same GPU
-        int taken = 0;        // lane q: positions of this chunk on GPU q
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-          const unsigned b = __ballot_sync(0xffffffffu, p == q);
-          if (p == q) used_before = __popc(b & ((1u << lane) - 1u));
-          if (lane == q) taken = __popc(b);
-        }
-        const int room_p = __shfl_sync(0xffffffffu, room, p < 0 ? 0 : p);
-        const unsigned vb = __ballot_sync(0xffffffffu, p >= 0 && used_before >= room_p);
-        if (vb) {  // the earliest position whose GPU would already hold cap experts
-          star = base + __ffs(vb) - 1;
-          break;
-        }
-        room -= taken;
-      }
-      if (lane == 0) s_star = star;
-    }
-    __syncthreads();
-    const int64_t star = s_star;
+      for (int w2 = 0; w2 < n_warps; ++w2) star = min(star, w_star[w2]);
 #ifdef GIMBAL_DEBUG_GREEDY
-    if (threadIdx.x == 0) printf("greedy: n_keys %lld n_valid %lld n_pos %lld star %lld\n", (long long)n_keys,
-                                 (long long)n_valid, (long long)n_pos, (long long)star);
+      if (threadIdx.x == 0) printf("greedy round: pos %lld star %lld n_pos %lld full %x\n", (long long)pos,
+                                   (long long)star, (long long)n_pos, full);
 #endif
-    // ---- C: state at s*: loads from each layer's positions < s*, counts from all of them ----
-    if (threadIdx.x < L) {
-      const int l = threadIdx.x;
-      unsigned long long v[G];
+      // ---- C: commit [pos, star): loads per layer, counts per GPU, output ----
+      if (l_me < L) {
+        unsigned long long v[G];
 #pragma unroll
-      for (int p = 0; p < G; ++p) v[p] = load[l * G + p];
-      int c[G];
+        for (int p = 0; p < G; ++p) v[p] = load[l_me * G + p];
+        int c[G];
 #pragma unroll
-      for (int p = 0; p < G; ++p) c[p] = 0;
-      for_layer(l, star, [&](int64_t i) {
-        const unsigned long long key = skeys[i];
-        const int e = key_expert(key);
-        const int p = tent[i];
+        for (int p = 0; p < G; ++p) c[p] = 0;
+        for (; cursor < l_end; ++cursor) {
+          const int i = list[cursor];
+          if (i >= star) break;
+          const unsigned long long key = skeys[i];
+          const int e = key_expert(key);
+          const int p = tent[i];
 #pragma unroll
-        for (int q = 0; q < G; ++q) {
-          v[q] += (q == p) ? key_total(key) : 0ull;
-          c[q] += (q == p);
+          for (int q = 0; q < G; ++q) {
+            v[q] += (q == p) ? key_total(key) : 0ull;
+            c[q] += (q == p);
+          }
+          out[e] = p;
+          if (out_u8) out_u8[e] = (uint8_t)p;
         }
-        out[e] = p;
-        if (out_u8) out_u8[e] = (uint8_t)p;
-      });
 #pragma unroll
-      for (int p = 0; p < G; ++p) {
-        load[l * G + p] = v[p];
-        atomicAdd(&counts[p], c[p]);
+        for (int p = 0; p < G; ++p) {
+          load[l_me * G + p] = v[p];
+          if (c[p]) atomicAdd(&counts[p], c[p]);
+        }
       }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t f = 0;
+        for (int p = 0; p < G; ++p) f |= (counts[p] >= cap ? 1u : 0u) << p;
+        s_full = f;
+      }
+      __syncthreads();
+      pos = star;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) sequential_walk(g, cap, keys, star, n_valid, inv_ne, load, counts, out, out_u8);
+    // experts with zero activation (home row 0, no load change) after every positive one
+    if (threadIdx.x == 0) sequential_walk(g, cap, keys, n_pos, n_valid, inv_ne, load, counts, out, out_u8);
   } else {
     (void)tent;
     __syncthreads();
@@ -236,8 +303,9 @@ cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A
                                uint8_t* out_u8, uint8_t* tent_scratch, cudaStream_t s) {
   const size_t base = (size_t)L * g * 8 + (size_t)4 * ((g + 3) / 4) * 4;
   const size_t n_pad = (size_t)((n_keys + 15) & ~15ll);
-  const size_t staged = base + n_pad * 10;  // keys (8 B) + layer map + tentative GPU per position
-  const bool parallel = L <= kMaxLayers && L < 255 && tent_scratch != nullptr && staged <= 200 * 1024;
+  const size_t staged = base + n_pad * 12;  // key (8 B) + list entry (2) + layer + tentative GPU per position
+  const bool parallel =
+      L <= kMaxLayers && L < 255 && tent_scratch != nullptr && n_pad < 65536 && staged <= 200 * 1024;
   const size_t smem = parallel ? staged : base;
   auto kern = !parallel ? greedy_walk_kernel<0>
             : g == 8    ? greedy_walk_kernel<8>
