@@ -648,6 +648,13 @@ int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, in
     dobj = dcut + C;
   }
   darg = reinterpret_cast<long long*>(h->dout.as<double>() + 3 * C);
+  if (h->max_tokens != h->tokens &&
+      (unsigned long long)h->tokens * (unsigned long long)(k * k) < (1ull << 27)) {
+    // every cell is at most tokens * k^2 (a token pairs each of its k slots with each of the next
+    // layer's k): small enough for 32-bit partial sums without looking
+    h->small_cells = true;
+    h->max_tokens = h->tokens;
+  }
   if (h->max_tokens != h->tokens) {
     // cells < 2^27 lets the evaluator keep 32-bit partial sums (one host sync per new count state)
     unsigned long long mx = 0;

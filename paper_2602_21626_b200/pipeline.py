@@ -19,7 +19,7 @@ from typing import Optional
 import numpy as np
 
 from .moe import MoeTopology, RoutingStats
-from .placement import AffinitySet, build_affinity_set, eval_costs, greedy_place
+from .placement import AffinitySet, build_affinity_set, eval_costs, greedy_place, greedy_place_array
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -134,19 +134,39 @@ class HotPath:
         """Tumbling-window re-placement (config 5; sim.cpp:149-165 semantics per window: the window
         is counted from zero, greedy re-places with the fixed anchor set, all candidates are
         scored, and `moved` counts experts whose GPU changed against the previous choice).
-        ``windows``: iterable of CUDA uint8 [T_w][L][k] traces.  Returns per-window
-        (argmin, moved, greedy placement)."""
+        ``windows``: sequence of CUDA uint8 [T_w][L][k] traces.  Returns per-window
+        (argmin, moved, greedy placement as an int32 numpy array).
+
+        Windows alternate between this handle and a twin (its own stats state and stream), and
+        window w+1 is queued for counting before window w's greedy/scoring reads its results back,
+        so the next window's counting overlaps this window's host round trips."""
+        windows = list(windows)
         out = []
-        prev = previous
-        for w in windows:
-            self.stats.reset()
-            self.stats.add_tokens(w)
-            res = self.place_with(M, candidates)
-            moved = (sum(1 for a, b in zip(prev, res.greedy) if a != b) if prev is not None
-                     and len(prev) == len(res.greedy) else len(res.greedy))
-            out.append((res.argmin, moved, res.greedy))
-            prev = res.greedy
+        if not windows:
+            return out
+        pair = (self, self._twin())
+        prev = None if previous is None else np.asarray(previous, np.int32)
+        pair[0].stats.reset()
+        pair[0].stats.add_tokens(windows[0])
+        for i in range(len(windows)):
+            cur = pair[i % 2]
+            if i + 1 < len(windows):
+                nxt = pair[(i + 1) % 2]
+                nxt.stats.reset()
+                nxt.stats.add_tokens(windows[i + 1])
+            gp = greedy_place_array(cur.stats, M, self.topo.n_gpus, out_u8_device=candidates[0])
+            _, am = eval_costs(cur.stats, candidates, self.alpha, self.beta, out=cur._scores(candidates.shape[0]))
+            moved = int(np.count_nonzero(prev != gp)) if prev is not None and prev.shape == gp.shape else len(gp)
+            out.append((am, moved, gp))
+            prev = gp
         return out
+
+    def _twin(self) -> "HotPath":
+        """A second handle with the same topology and parameters (stream double-buffering)."""
+        if getattr(self, "_twin_hp", None) is None:
+            self._twin_hp = HotPath(self.topo, device=self.device, alpha=self.alpha, beta=self.beta,
+                                    threshold=self.threshold, top_e=self.top_e, anchor_gpu=self.anchor_gpu)
+        return self._twin_hp
 
     def stream_distributed(self, window_shards, candidates_shard, cand_offset: int, n_candidates: int,
                            M: AffinitySet, group=None, previous=None):

@@ -140,23 +140,29 @@ def greedy_place(activation, affinity: AffinitySet, g: int, out_u8_device=None) 
     """placement.cpp:240-299.  ``activation`` is a dense [rows][m] matrix (reference form) or a
     RoutingStats (flat activation on the device).  ``out_u8_device`` optionally receives the
     result as uint8 (e.g. row 0 of a candidate batch)."""
-    M = _i32(affinity.experts)
     if isinstance(activation, RoutingStats):
-        if g != activation.topo.n_gpus:
-            raise ValueError("greedy_place: g must equal the topology's n_gpus for device stats")
-        m = activation.topo.total_experts()
-        out = np.zeros(m, np.int32)
-        N.check(N.lib().gimbal_greedy_place(activation.handle, M.ctypes.data if M.size else None, M.size,
-                                            affinity.anchor_gpu, out.ctypes.data, N.MEM_HOST,
-                                            C.c_void_p(out_u8_device.data_ptr()) if out_u8_device is not None
-                                            else None), "greedy_place")
-        return Placement(assign=[int(x) for x in out])
+        return Placement(assign=greedy_place_array(activation, affinity, g, out_u8_device).tolist())
+    M = _i32(affinity.experts)
     A = np.ascontiguousarray(np.atleast_2d(np.asarray(activation, np.float64)))
     out = np.zeros(A.shape[1], np.int32)
     N.check(N.lib().gimbal_greedy_place_dense(A.shape[0], A.shape[1], A.ctypes.data,
                                               M.ctypes.data if M.size else None, M.size, affinity.anchor_gpu, g,
                                               out.ctypes.data), "greedy_place")
     return Placement(assign=[int(x) for x in out])
+
+
+def greedy_place_array(stats: RoutingStats, affinity: AffinitySet, g: int, out_u8_device=None) -> np.ndarray:
+    """greedy_place on device stats, returned as an int32 numpy array (no per-element Python
+    objects: the streaming loop compares successive placements vectorised)."""
+    if g != stats.topo.n_gpus:
+        raise ValueError("greedy_place: g must equal the topology's n_gpus for device stats")
+    M = _i32(affinity.experts)
+    out = np.zeros(stats.topo.total_experts(), np.int32)
+    N.check(N.lib().gimbal_greedy_place(stats.handle, M.ctypes.data if M.size else None, M.size,
+                                        affinity.anchor_gpu, out.ctypes.data, N.MEM_HOST,
+                                        C.c_void_p(out_u8_device.data_ptr()) if out_u8_device is not None
+                                        else None), "greedy_place")
+    return out
 
 
 def maybe_relocate(step_count: int, tau: int, affinity: AffinitySet, recent_activation, g: int,

@@ -250,6 +250,36 @@ def test_placement_pipeline_matches_oracle(G, orc, shape):
     assert res.argmin == am
 
 
+@pytest.mark.parametrize("shape", ["dsv2lite", "dsv3"])
+def test_stream_windows_match_oracle(G, orc, shape):
+    """Config 5 (tumbling windows, sim.cpp:149-165): M fixed from a calibration window, each window
+    counted from zero, greedy with M, all candidates scored; the two-handle overlapped loop gives
+    the oracle's greedy placement, argmin and moved count for every window."""
+    L, ne, k, g = SHAPES[shape]
+    topo = G.MoeTopology(L, ne, k, g)
+    C, T_w = 40, 6001
+    calib = G.generate_trace(topo, 20000, model_seed=1, stream_seed=3, drift=0.05, drift_epoch=0, device=0)
+    wins = [G.generate_trace(topo, T_w, model_seed=1, stream_seed=2, first_token=w * T_w, drift=0.05,
+                             drift_epoch=w + 1, device=0) for w in range(5)]
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 77, C)).cuda()
+    hp = G.HotPath(topo, 0)
+    M = hp.calibrate(calib)
+    cA, cE, _ = orc.stats(L, ne, k, calib.cpu().numpy())
+    assert M.experts == list(orc.affinity_set(L, ne, g, cE, 0.0, 4))
+    out = hp.stream(wins, cands, M)
+    prev = None
+    for w, (am, moved, gp) in zip(wins, out):
+        oA, oE, _ = orc.stats(L, ne, k, w.cpu().numpy())
+        ogp = np.asarray(orc.greedy_place(L, ne, g, oA, M.experts, 0), np.int32)
+        assert np.array_equal(gp, ogp)
+        hc = cands.cpu().numpy()
+        hc[0] = ogp.astype(np.uint8)  # the loop scores the window's greedy as candidate 0
+        _, _, _, oam = orc.eval_costs(L, ne, g, oA, oE, hc)
+        assert am == oam
+        assert moved == (len(ogp) if prev is None else int(np.count_nonzero(prev != ogp)))
+        prev = ogp
+
+
 @pytest.mark.parametrize("threshold,top_e,cap", [(0.0, 4, None), (0.0, -1, None), (50.0, 16, 7), (1e12, 4, None),
                                                  (0.0, 0, None), (0.0, 64, 3), (3.0, 1000, None)])
 def test_affinity_set_variants(G, orc, threshold, top_e, cap):
