@@ -295,14 +295,15 @@ __global__ void __launch_bounds__(1024, 1)
 // Direct token-major counting with the ids staged by the tensor memory accelerator: every
 // 1024-token block of the pair's two columns is one set of 2-D TMA boxes, so the SM's load/store
 // pipe serves only the shared-memory atomics and two short shared reads per token instead of two
-// 32-line gathers per warp.  A box must start 16-byte aligned in the row, so it spans the four
-// layers (l & ~1) .. (l & ~1) + 3 and the pair's words sit at offset l & 1 (columns past the last
-// layer are zero-filled and never read).  A 3-stage full/empty mbarrier ring keeps the next
+// 32-line gathers per warp.  A box must start 16-byte aligned in the row, so boxes hold two
+// layers: (l, l+1) for even l, read as one 16-byte load per token; (l-1, l) and (l+1, l+2) for
+// odd l, read as two 8-byte loads at a 16-byte stride (conflict-free); columns past the last
+// layer are zero-filled and never read.  A 3-stage full/empty mbarrier ring keeps the next
 // blocks in flight while the current one is counted.
 constexpr int kTmaStages = 3;
 constexpr int kTmaBlock = 1024;  // tokens per stage = threads per CTA
 constexpr int kTmaBox = 256;     // rows per TMA box (hardware limit)
-constexpr int kTmaCols = 4;      // u64 words per row in a box (32 B)
+constexpr int kTmaCols = 4;      // u64 words per token in a stage (two 2-layer boxes of 16 B)
 constexpr int kU15Bytes = 256 * 128 * 4;
 
 constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tokens
@@ -342,12 +343,16 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
     auto issue = [&](uint32_t blk, uint32_t g) {  // thread 0
       const uint32_t s = g % kTmaStages;
       if (g >= kTmaStages) mbar_wait(&empty_bar[s], (g / kTmaStages - 1) & 1u);
-      mbar_arrive_expect_tx(&full_bar[s], kTmaBlock * kTmaCols * 8);
+      // boxes of two layers (16 B per token, 16-byte aligned in the row): layers l, l+1 when l
+      // is even; layers l-1, l and l+1, l+2 (two half-stages) when l is odd
+      mbar_arrive_expect_tx(&full_bar[s], kTmaBlock * 16 * ((l & 1) + 1));
       const int64_t t0 = t_begin + (int64_t)blk * kTmaBlock;
 #pragma unroll
-      for (int q = 0; q < kTmaBlock / kTmaBox; ++q)
-        tma_load_2d(stage + (s * kTmaBlock + q * kTmaBox) * kTmaCols, &tmap, &full_bar[s], l & ~1,
-                    (int)(t0 + q * kTmaBox));
+      for (int q = 0; q < kTmaBlock / kTmaBox; ++q) {
+        unsigned long long* dst = stage + (s * kTmaBlock + q * kTmaBox) * kTmaCols;
+        tma_load_2d(dst, &tmap, &full_bar[s], l & ~1, (int)(t0 + q * kTmaBox));
+        if (l & 1) tma_load_2d(dst + kTmaBox * 2, &tmap, &full_bar[s], l + 1, (int)(t0 + q * kTmaBox));
+      }
     };
     if (tid == 0)
       for (uint32_t i = 0; i < min(nb, (uint32_t)kTmaStages); ++i) issue(i, it + i);
@@ -355,8 +360,18 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
     for (uint32_t i = 0; i < nb; ++i) {
       const uint32_t g = it + i, s = g % kTmaStages;
       mbar_wait(&full_bar[s], (g / kTmaStages) & 1u);
-      const unsigned long long* row = stage + (s * kTmaBlock + tid) * kTmaCols + (l & 1);
-      const unsigned long long cur = row[0], nxt = row[1];
+      // per 256-token box: [256][2] words of layers (l & ~1, +1), then (odd l) [256][2] of l+1, l+2
+      const unsigned long long* box = stage + (s * kTmaBlock + (tid & ~(kTmaBox - 1))) * kTmaCols;
+      const int r = tid & (kTmaBox - 1);
+      unsigned long long cur, nxt;
+      if (l & 1) {  // 16-byte row stride: conflict-free 8-byte loads
+        cur = box[r * 2 + 1];
+        nxt = box[kTmaBox * 2 + r * 2];
+      } else {      // one 16-byte load
+        const ulonglong2 v = reinterpret_cast<const ulonglong2*>(box)[r];
+        cur = v.x;
+        nxt = v.y;
+      }
       if (t_begin + (int64_t)i * kTmaBlock + tid < t_end) {
         if constexpr (U16) {
           if (!(has_dup8(cur) | has_dup8(nxt))) {
@@ -652,7 +667,7 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   prm.n_units = n_chunks * plan.n_groups;
   const int grid = (int)resident;
   CUtensorMap tmap;
-  if (encode_trace_map(&tmap, trace, T, plan.L, kTmaCols, kTmaBox)) {
+  if (encode_trace_map(&tmap, trace, T, plan.L, 2, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
     static const bool u16 = !(std::getenv("GIMBAL_TMA_MODE") && std::string(std::getenv("GIMBAL_TMA_MODE")) == "u15");
     auto kern = u16 ? count_tm_u15_tma_kernel<true> : count_tm_u15_tma_kernel<false>;
