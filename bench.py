@@ -47,11 +47,13 @@ METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
 # atomic increments to random addresses of a 128 KB table, 148 CTAs x 1024 threads.
 ATOMS_RANDOM_PEAK = 2.553e12
 # dram__bytes_read.sum + dram__bytes_write.sum per counting launch from one `ncu --set full`
-# capture (profiles/r1b_ncu_count_<config>.md), bytes / launch, with the tokens of that launch.
-TRAFFIC = {"dsv3": {"bytes": 62.633288e9 + 1.774051e9, "tokens_in_launch": 67108864,
-                    "source": "profiles/r1b_ncu_count_dsv3.md"},
-           "qwen3": {"bytes": 19.263587e9 + 5.747456e6, "tokens_in_launch": 33554432,
-                     "source": "profiles/r1b_ncu_count_qwen3.md"}}
+# capture (profiles/r1c_ncu_count_<config>.md), bytes / launch, with the tokens of that launch.
+TRAFFIC = {"dsv3": {"bytes": 51.768141e9 + 1.372393e9, "tokens_in_launch": 67108864,
+                    "source": "profiles/r1c_ncu_count_dsv3.md"},
+           "qwen3": {"bytes": 18.002675e9 + 9.890816e6, "tokens_in_launch": 33554432,
+                     "source": "profiles/r1c_ncu_count_qwen3.md"},
+           "dsv2lite": {"bytes": 4.356829e9 + 7.6224e6, "tokens_in_launch": 16777216,
+                        "source": "profiles/r1c_ncu_count_dsv2lite.md"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 REASON_BITS = {
