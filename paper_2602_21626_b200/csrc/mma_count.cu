@@ -33,7 +33,12 @@ namespace {
 constexpr int kTok = 128;                  // tokens per tile (MMA K, 4 instructions of 32)
 constexpr int kRows = 128;                 // experts per tile row block (MMA M, N <= 128)
 constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
-constexpr int kMaxPairs = 4;               // accumulators: 4 x 128 TMEM columns
+#ifndef GIMBAL_MMA_PAIRS
+#define GIMBAL_MMA_PAIRS 2  // 2 pairs x 128 TMEM columns, 2 CTAs per SM: 29.1 vs 30.1 ms at Qwen3 (4 pairs, 1 CTA)
+#endif
+constexpr int kMaxPairs = GIMBAL_MMA_PAIRS;  // accumulators: kMaxPairs x 128 TMEM columns
+constexpr int kTmemCols = kMaxPairs <= 2 ? 256 : 512;
+constexpr int kCtasPerSm = kMaxPairs <= 2 ? 2 : 1;  // two CTAs (TMEM halves) overlap barrier stalls
 constexpr int kStages = 2;
 constexpr int kThreads = (kMaxPairs + 1) * kTok;           // one token-layer row per thread
 constexpr int kIdSlots = 3;                                 // TMA ring of id word tiles
@@ -91,7 +96,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // l0 & ~1 x 128 tokens; row tt of the box is token t0 + tt), with range and repeat checks done
 // per row here; otherwise from the layer-major LM8 buffer X by 1-D bulk copies.
 template <int K, bool TM>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     count_mma_kernel(const __grid_constant__ CUtensorMap tmap, MmaParams prm,
                      const unsigned long long* __restrict__ X, unsigned long long* __restrict__ E) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "r"(512));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (it_global >= 2) mbar_wait(&bars[(it_global - 2) & 1], ((it_global - 2) >> 1) & 1);
   __syncthreads();
   if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -268,7 +273,7 @@ MmaParams make_params(int L, int ne, int k, int sms, int64_t T, int64_t ld, uint
   prm.flags = flags;
   // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
   prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
-  int64_t ranges = std::max<int64_t>(1, sms / prm.n_groups);
+  int64_t ranges = std::max<int64_t>(1, kCtasPerSm * sms / prm.n_groups);
   const int64_t cap = ((int64_t)1 << 31) / ((int64_t)k * k) - kTok;
   int64_t per = (T + ranges - 1) / ranges;
   if (per > cap) per = cap;
@@ -276,7 +281,7 @@ MmaParams make_params(int L, int ne, int k, int sms, int64_t T, int64_t ld, uint
   ranges = (T + per - 1) / per;
   prm.range_tokens = per;
   prm.n_units = ranges * prm.n_groups;
-  *grid = (int)std::min<int64_t>(prm.n_units, sms);
+  *grid = (int)std::min<int64_t>(prm.n_units, (int64_t)kCtasPerSm * sms);
   return prm;
 }
 
