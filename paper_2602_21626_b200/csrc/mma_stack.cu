@@ -36,8 +36,13 @@ namespace {
 constexpr int kNe = 64;              // experts per layer (one half of the M = 128 operand)
 constexpr int kTok = 64;             // tokens per tile (two K = 32 MMA steps)
 constexpr int kSlotBytes = 512;      // one layer's 64 experts x 8 tokens (4 core matrices)
-constexpr int kMaxPairs = 16;        // 8 accumulators of 64 TMEM columns
-constexpr int kStages = 3;
+#ifndef GIMBAL_STACK_CTAS
+#define GIMBAL_STACK_CTAS 1  // 2 (half the pairs per group, 2 stages): 4.95 vs 4.75 ms at DS-V2-Lite
+#endif
+constexpr int kCtasPerSm = GIMBAL_STACK_CTAS;             // CTAs per SM (TMEM and smem split)
+constexpr int kMaxPairs = 16 / kCtasPerSm;               // 8 / kCtasPerSm accumulators of 64 TMEM columns
+constexpr int kTmemCols = 512 / kCtasPerSm;
+constexpr int kStages = kCtasPerSm > 1 ? 2 : 3;
 constexpr int kIdSlots = 3;
 constexpr int kThreads = 512;
 
@@ -84,7 +89,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
     count_mma_stack_kernel(StackParams prm, const uint8_t* __restrict__ trace, unsigned long long* __restrict__ E) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bars[kStages + 1];
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "r"(512));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&bars[g % kStages], (g / kStages) & 1);
   }
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
 bool make_params(int L, int k, int sms, int max_smem, int64_t T, uint32_t* flags, StackParams* prm, int* grid,
@@ -263,7 +268,7 @@ bool make_params(int L, int k, int sms, int max_smem, int64_t T, uint32_t* flags
     prm->odd_slots = (prm->ppg + 1) / 2;
     prm->stage_bytes = (prm->even_slots + prm->odd_slots) * (kTok / 8) * kSlotBytes;
     *smem = (size_t)kStages * prm->stage_bytes + (size_t)kIdSlots * prm->id_slot_bytes;
-    if (*smem <= (size_t)max_smem - 1024) break;
+    if (*smem <= (size_t)(max_smem / kCtasPerSm) - 2048) break;
   }
   prm->T = T;
   prm->flags = flags;
@@ -279,7 +284,7 @@ bool make_params(int L, int k, int sms, int max_smem, int64_t T, uint32_t* flags
   ranges = (T + per - 1) / per;
   prm->range_tokens = per;
   prm->n_units = ranges * prm->n_groups;
-  *grid = (int)std::min<int64_t>(prm->n_units, sms);
+  *grid = (int)std::min<int64_t>(prm->n_units, (int64_t)kCtasPerSm * sms);
   return true;
 }
 
