@@ -130,6 +130,23 @@ int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32
 int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t n_M, int32_t anchor_gpu,
                         int32_t* out, int out_mem, uint8_t* out_u8_device);
 
+/* One tumbling window of streaming re-placement (MoeSubsystem::on_forward_step, sim.cpp:149-165,
+ * with the strong-pair set fixed after calibration, sim.cpp:94-104), queued on the handle's stream
+ * with NO host synchronisation: greedy_place (placement.cpp:240-299) with M anchored on
+ * anchor_gpu -> `placement` (m int32, device) and row 0 of `candidates` (uint8 [C][m], device),
+ * then eval_cost of all C candidates (placement.cpp:58-85) -> `scores` (device f64 [3][C]: D, cut,
+ * objective) and `argmin` (device int64, lowest index on ties).  M is validated (reference
+ * messages) and uploaded only when it differs from the previous call's.  Device-side errors
+ * (infeasible candidate, overflow) are deferred: the next gimbal_stats_sync reports them.  With
+ * two handles a caller pipelines window w+1's counting behind window w's placement. */
+int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t n_M, int32_t anchor_gpu,
+                              uint8_t* candidates_device, int64_t n_candidates, double alpha, double beta,
+                              double* scores_device, int64_t* argmin_device, int32_t* placement_device);
+
+/* Counting kernels of this handle run on n_sms SMs (default: all).  Leaving SMs free lets a
+ * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */
+int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms);
+
 /* ---- the reference's general dense forms (PlacementProblem with arbitrary A / W) ---- */
 
 /* eval_cost (placement.cpp:58-85) on dense A [rows][m] and W [m][m] doubles (host). */

@@ -157,6 +157,11 @@ struct gimbal_stats_s {
   // scratch
   DevBuf cand, same, dout, keys, misc, ints;
   std::mutex mu;
+  // strong-pair set resident in `ints` for the asynchronous window path (streaming windows keep
+  // M fixed, sim.cpp:94-104, so it is uploaded once): valid while ints.p == m_cached_buf
+  std::vector<int32_t> m_cached;
+  int32_t m_cached_anchor = -1;
+  void* m_cached_buf = nullptr;
 
   int64_t m() const { return (int64_t)topo.n_layers * topo.n_experts; }
   int64_t nE() const { return (int64_t)(topo.n_layers - 1) * topo.n_experts * topo.n_experts; }
@@ -409,6 +414,11 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
     return fail(GIMBAL_CUDA_ERROR);
   }
   *out = h;
+  if (cudaMemset(h->dflags, 0, 64) != cudaSuccess) {
+    *out = nullptr;
+    set_error("gimbal_stats_create: flag init failed");
+    return fail(GIMBAL_CUDA_ERROR);
+  }
   int st = gimbal_stats_reset(h);
   if (st != GIMBAL_OK) {
     *out = nullptr;
@@ -462,7 +472,7 @@ int gimbal_stats_reset(gimbal_stats_t h) {
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dE, 0, std::max<int64_t>(h->nE(), 1) * 8, h->stream));
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dA, 0, nA * 8, h->stream));
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dW, 0, nW * 8, h->stream));
-  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 64, h->stream));
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 4, h->stream));  // word 1 (deferred) survives
   h->tokens = 0;
   h->max_tokens = -1;
   h->derived = true;
@@ -499,7 +509,17 @@ int gimbal_stats_sync(gimbal_stats_t h) {
   GIMBAL_TRY(check_handle(h));
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
-  return h->check_flags();
+  uint32_t f[2] = {0, 0};
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(f, h->dflags, sizeof(f), cudaMemcpyDeviceToHost, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (f[1]) {  // deferred evaluator flags of gimbal_window_place_async: report once, then clear
+    GIMBAL_CUDA_TRY(cudaMemset(h->dflags + 1, 0, 4));
+    if (f[1] & kFlagInfeasible)
+      return invalid("placement: a queued candidate batch is infeasible (ids must be in [0, g) with exactly "
+                     "m/g experts per GPU)");
+    GIMBAL_TRY(flags_to_status(f[1]));
+  }
+  return flags_to_status(f[0] & (kFlagIdOutOfRange | kFlagOverflow));
 }
 
 int gimbal_stats_read(gimbal_stats_t h, uint64_t* A, uint64_t* E, uint64_t* W, int mem) {
@@ -615,39 +635,15 @@ int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
   return GIMBAL_OK;
 }
 
-int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, int cand_mem,
-                      double alpha, double beta, double* deviation, double* cut, double* objective,
-                      int64_t* argmin, int out_mem) {
-  GIMBAL_TRY(check_handle(h));
-  if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
-  if (C < 0) return invalid("eval_costs: negative candidate count");
-  if (C == 0) {
-    if (argmin) *argmin = -1;
-    return GIMBAL_OK;
-  }
-  if (!candidates || !deviation || !cut || !objective) return invalid("eval_costs: null argument");
-  if (h->topo.n_gpus > 255) return invalid("eval_costs: uint8 candidates need n_gpus <= 255");
-  std::lock_guard<std::mutex> lk(h->mu);
-  DeviceGuard g(h->device);
-  GIMBAL_TRY(h->derive());
+namespace {
+
+// Queues the batch evaluator (eval_same + eval_dev + eval_finish) for C device candidates on the
+// handle's stream.  The only host synchronisation is the one-off max-cell probe when the token
+// count alone cannot bound every E cell below 2^27.
+int enqueue_eval(gimbal_stats_t h, const uint8_t* dc, int64_t C, double alpha, double beta, double* dD,
+                 double* dcut, double* dobj, long long* darg, uint32_t* flags) {
   const int L = h->topo.n_layers, ne = h->topo.n_experts, gg = h->topo.n_gpus, k = h->topo.top_k;
-  const int64_t m = h->m();
-  const uint8_t* dc = candidates;
-  if (cand_mem != GIMBAL_MEM_DEVICE) {
-    GIMBAL_TRY(h->cand.ensure((size_t)C * m));
-    GIMBAL_CUDA_TRY(cudaMemcpyAsync(h->cand.p, candidates, (size_t)C * m, cudaMemcpyHostToDevice, h->stream));
-    dc = h->cand.as<uint8_t>();
-  }
   GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
-  double *dD = deviation, *dcut = cut, *dobj = objective;
-  long long* darg = nullptr;
-  GIMBAL_TRY(h->dout.ensure((size_t)C * 24 + 16));
-  if (out_mem != GIMBAL_MEM_DEVICE) {
-    dD = h->dout.as<double>();
-    dcut = dD + C;
-    dobj = dcut + C;
-  }
-  darg = reinterpret_cast<long long*>(h->dout.as<double>() + 3 * C);
   if (h->max_tokens != h->tokens &&
       (unsigned long long)h->tokens * (unsigned long long)(k * k) < (1ull << 27)) {
     // every cell is at most tokens * k^2 (a token pairs each of its k slots with each of the next
@@ -667,11 +663,47 @@ int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, in
   }
   GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
                                     h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
-                                    h->dflags, h->small_cells, h->stream));
+                                    flags, h->small_cells, h->stream));
   const unsigned long long total =
       (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
   GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
-                                     dobj, darg, h->dflags, h->stream));
+                                     dobj, darg, flags, h->stream));
+  return GIMBAL_OK;
+}
+
+}  // namespace
+
+int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, int cand_mem,
+                      double alpha, double beta, double* deviation, double* cut, double* objective,
+                      int64_t* argmin, int out_mem) {
+  GIMBAL_TRY(check_handle(h));
+  if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
+  if (C < 0) return invalid("eval_costs: negative candidate count");
+  if (C == 0) {
+    if (argmin) *argmin = -1;
+    return GIMBAL_OK;
+  }
+  if (!candidates || !deviation || !cut || !objective) return invalid("eval_costs: null argument");
+  if (h->topo.n_gpus > 255) return invalid("eval_costs: uint8 candidates need n_gpus <= 255");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->derive());
+  const int64_t m = h->m();
+  const uint8_t* dc = candidates;
+  if (cand_mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(h->cand.ensure((size_t)C * m));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(h->cand.p, candidates, (size_t)C * m, cudaMemcpyHostToDevice, h->stream));
+    dc = h->cand.as<uint8_t>();
+  }
+  double *dD = deviation, *dcut = cut, *dobj = objective;
+  GIMBAL_TRY(h->dout.ensure((size_t)C * 24 + 16));
+  if (out_mem != GIMBAL_MEM_DEVICE) {
+    dD = h->dout.as<double>();
+    dcut = dD + C;
+    dobj = dcut + C;
+  }
+  long long* darg = reinterpret_cast<long long*>(h->dout.as<double>() + 3 * C);
+  GIMBAL_TRY(enqueue_eval(h, dc, C, alpha, beta, dD, dcut, dobj, darg, h->dflags));
   uint32_t f = 0;
   long long bad = 0, am = -1;
   GIMBAL_CUDA_TRY(cudaMemcpyAsync(&f, h->dflags, 4, cudaMemcpyDeviceToHost, h->stream));
@@ -769,15 +801,51 @@ static int validate_greedy(int64_t m, int g, const int32_t* M, int32_t nM, int32
   return GIMBAL_OK;
 }
 
+namespace {
+
+// Scratch layout in h->ints for greedy: [anchored bits][M][result m int32][tent m bytes].
+struct GreedyScratch {
+  uint32_t* bits;
+  int32_t* M;
+  int32_t* res;
+  uint8_t* tent;
+};
+
+int greedy_scratch(gimbal_stats_t h, size_t words, int32_t nM, GreedyScratch& g) {
+  const int64_t m = h->m();
+  GIMBAL_TRY(h->keys.ensure((size_t)next_pow2(m) * 8));
+  GIMBAL_TRY(h->ints.ensure(words * 4 + (size_t)std::max(nM, 1) * 4 + (size_t)m * 4 + (size_t)m + 64));
+  g.bits = h->ints.as<uint32_t>();
+  g.M = reinterpret_cast<int32_t*>(g.bits + words);
+  g.res = g.M + std::max(nM, 1);
+  g.tent = reinterpret_cast<uint8_t*>(g.res + m);  // per-position scratch
+  return GIMBAL_OK;
+}
+
+// greedy_keys -> sort -> walk on the handle's stream (anchored bits and M already on the device).
+int enqueue_greedy(gimbal_stats_t h, const GreedyScratch& gs, int32_t nM, int32_t anchor, int32_t* dres,
+                   uint8_t* out_u8) {
+  const int L = h->topo.n_layers, ne = h->topo.n_experts, g = h->topo.n_gpus;
+  const int64_t m = h->m();
+  const int64_t n_pad = next_pow2(m);
+  GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, gs.bits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
+                                     h->stream));
+  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+  GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, gs.M, nM, anchor, h->keys.as<unsigned long long>(),
+                                     m, dres, out_u8, gs.tent, h->stream));
+  return GIMBAL_OK;
+}
+
+}  // namespace
+
 int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t anchor, int32_t* out,
                         int out_mem, uint8_t* out_u8) {
   GIMBAL_TRY(check_handle(h));
   if (!out && !out_u8) return invalid("greedy_place: null output");
   if (nM < 0 || (nM > 0 && !M)) return invalid("greedy_place: bad affinity set");
-  const int L = h->topo.n_layers, ne = h->topo.n_experts, g = h->topo.n_gpus;
   const int64_t m = h->m();
   std::vector<uint32_t> bits;
-  GIMBAL_TRY(validate_greedy(m, g, M, nM, anchor, bits));
+  GIMBAL_TRY(validate_greedy(m, h->topo.n_gpus, M, nM, anchor, bits));
   if (m >= (1ll << 24)) {
     set_error("greedy_place: m must be < 2^24");
     return GIMBAL_NOT_SUPPORTED;
@@ -785,25 +853,69 @@ int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t 
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard dg(h->device);
   GIMBAL_TRY(h->derive());
-  const int64_t n_pad = next_pow2(m);
-  GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
-  const size_t words = bits.size();
-  GIMBAL_TRY(h->ints.ensure(words * 4 + (size_t)std::max(nM, 1) * 4 + (size_t)m * 4 + (size_t)m + 64));
-  uint32_t* dbits = h->ints.as<uint32_t>();
-  int32_t* dM = reinterpret_cast<int32_t*>(dbits + words);
-  int32_t* dres = dM + std::max(nM, 1);
-  if (out && out_mem == GIMBAL_MEM_DEVICE) dres = out;
-  GIMBAL_CUDA_TRY(cudaMemcpyAsync(dbits, bits.data(), words * 4, cudaMemcpyHostToDevice, h->stream));
-  if (nM > 0) GIMBAL_CUDA_TRY(cudaMemcpyAsync(dM, M, (size_t)nM * 4, cudaMemcpyHostToDevice, h->stream));
-  GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, dbits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
-                                     h->stream));
-  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
-  uint8_t* tent = reinterpret_cast<uint8_t*>(dM + std::max(nM, 1) + m);  // per-position scratch
-  GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, dM, nM, anchor, h->keys.as<unsigned long long>(),
-                                     m, dres, out_u8, tent, h->stream));
+  GreedyScratch gs{};
+  GIMBAL_TRY(greedy_scratch(h, bits.size(), nM, gs));
+  h->m_cached_buf = nullptr;  // this call overwrites the resident strong-pair set
+  int32_t* dres = (out && out_mem == GIMBAL_MEM_DEVICE) ? out : gs.res;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(gs.bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, h->stream));
+  if (nM > 0) GIMBAL_CUDA_TRY(cudaMemcpyAsync(gs.M, M, (size_t)nM * 4, cudaMemcpyHostToDevice, h->stream));
+  GIMBAL_TRY(enqueue_greedy(h, gs, nM, anchor, dres, out_u8));
   if (out && out_mem != GIMBAL_MEM_DEVICE)
     GIMBAL_CUDA_TRY(cudaMemcpyAsync(out, dres, (size_t)m * 4, cudaMemcpyDeviceToHost, h->stream));
   return h->check_flags();
+}
+
+int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t nM, int32_t anchor,
+                              uint8_t* candidates, int64_t C, double alpha, double beta, double* scores,
+                              int64_t* argmin, int32_t* placement) {
+  GIMBAL_TRY(check_handle(h));
+  if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
+  if (C < 1 || !candidates || !scores || !argmin || !placement)
+    return invalid("window_place: needs C >= 1 device candidates and device outputs");
+  if (nM < 0 || (nM > 0 && !M)) return invalid("greedy_place: bad affinity set");
+  if (h->topo.n_gpus > 255) return invalid("eval_costs: uint8 candidates need n_gpus <= 255");
+  const int64_t m = h->m();
+  if (m >= (1ll << 24)) {
+    set_error("greedy_place: m must be < 2^24");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  const int64_t words = (m + 31) / 32;
+  GreedyScratch gs{};
+  GIMBAL_TRY(greedy_scratch(h, (size_t)words, nM, gs));
+  const bool same_set = h->m_cached_buf == h->ints.p && h->m_cached_anchor == anchor &&
+                        h->m_cached.size() == (size_t)nM &&
+                        std::equal(M, M + nM, h->m_cached.begin());
+  if (!same_set) {
+    std::vector<uint32_t> bits;
+    GIMBAL_TRY(validate_greedy(m, h->topo.n_gpus, M, nM, anchor, bits));
+    // a new set is rare (once per stream): upload synchronously so the host vectors may go
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    GIMBAL_CUDA_TRY(cudaMemcpy(gs.bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice));
+    if (nM > 0) GIMBAL_CUDA_TRY(cudaMemcpy(gs.M, M, (size_t)nM * 4, cudaMemcpyHostToDevice));
+    h->m_cached.assign(M, M + nM);
+    h->m_cached_anchor = anchor;
+    h->m_cached_buf = h->ints.p;
+  }
+  GIMBAL_TRY(h->derive());
+  GIMBAL_TRY(enqueue_greedy(h, gs, nM, anchor, placement, candidates));
+  // evaluator flags go to the deferred word (dflags[1]): reset() clears only the count-state word,
+  // so an infeasible candidate in any queued window is still reported by gimbal_stats_sync
+  return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
+                      reinterpret_cast<long long*>(argmin), h->dflags + 1);
+}
+
+int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms) {
+  GIMBAL_TRY(check_handle(h));
+  std::lock_guard<std::mutex> lk(h->mu);
+  int dev_sms = 0;
+  GIMBAL_CUDA_TRY(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
+  if (n_sms < 1 || n_sms > dev_sms) return invalid("set_count_sms: n_sms must be in [1, SM count]");
+  h->sms = n_sms;
+  h->plan = make_stats_plan(h->topo.n_layers, h->topo.n_experts, h->topo.top_k, n_sms, h->smem_optin);
+  h->lm8_plan = make_lm8_plan(h->topo.n_layers, h->topo.n_experts, h->topo.top_k, n_sms, h->smem_optin);
+  return GIMBAL_OK;
 }
 
 int gimbal_static_placement(const gimbal_topology* topo, int32_t* out) {

@@ -221,6 +221,10 @@ class RoutingStats:
     def mark_reduced(self, global_tokens: int) -> None:
         N.check(N.lib().gimbal_stats_mark_reduced(self._h, int(global_tokens)), "mark_reduced")
 
+    def set_count_sms(self, n_sms: int) -> None:
+        """Counting kernels use n_sms SMs (the rest stay free for another stream's kernels)."""
+        N.check(N.lib().gimbal_stats_set_count_sms(self._h, int(n_sms)), "set_count_sms")
+
     def sync(self) -> None:
         self._flush()
         N.check(N.lib().gimbal_stats_sync(self._h), "sync")

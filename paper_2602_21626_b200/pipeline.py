@@ -13,11 +13,13 @@ are all-gathered for a global argmin with the lowest index winning ties (SURVEY.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
 
+from . import _native as N
 from .moe import MoeTopology, RoutingStats
 from .placement import AffinitySet, build_affinity_set, eval_costs, greedy_place, greedy_place_array
 
@@ -130,34 +132,75 @@ class HotPath:
         return build_affinity_set(self.stats, topo, self.threshold, self.top_e,
                                   topo.total_experts() // topo.n_gpus, self.anchor_gpu)
 
-    def stream(self, windows, candidates, M: AffinitySet, previous=None):
+    def stream(self, windows, candidates, M: AffinitySet, previous=None, reserve_sms: int = 2):
         """Tumbling-window re-placement (config 5; sim.cpp:149-165 semantics per window: the window
         is counted from zero, greedy re-places with the fixed anchor set, all candidates are
         scored, and `moved` counts experts whose GPU changed against the previous choice).
-        ``windows``: sequence of CUDA uint8 [T_w][L][k] traces.  Returns per-window
+        ``windows``: sequence of CUDA uint8 [T_w][L][k] traces; ``candidates``: CUDA uint8 [C][m]
+        (row 0 is replaced by each window's greedy placement).  Returns per-window
         (argmin, moved, greedy placement as an int32 numpy array).
 
-        Windows alternate between this handle and a twin (its own stats state and stream), and
-        window w+1 is queued for counting before window w's greedy/scoring reads its results back,
-        so the next window's counting overlaps this window's host round trips."""
+        The whole stream is queued without host synchronisation.  Windows alternate between this
+        handle and a twin (own counts, own stream, own copy of the candidate batch), so window
+        w+1 is counted while window w is placed and scored; counting leaves ``reserve_sms`` SMs
+        free, where window w's latency-bound greedy walk runs alongside.  Each window's greedy
+        placement, scores and argmin stay on the device until the end
+        (gimbal_window_place_async); device-side errors surface at the final sync."""
+        import torch
+
         windows = list(windows)
-        out = []
         if not windows:
-            return out
+            return []
+        n, (n_c, m) = len(windows), tuple(candidates.shape)
+        dev = torch.device("cuda", self.device)
         pair = (self, self._twin())
+        scores = torch.empty((n, 3, n_c), dtype=torch.float64, device=dev)
+        argmins = torch.empty((n,), dtype=torch.int64, device=dev)
+        places = torch.empty((n, m), dtype=torch.int32, device=dev)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        for hp in pair:
+            if getattr(hp, "_wcands", None) is None or tuple(hp._wcands.shape) != (n_c, m):
+                hp._wcands = torch.empty_like(candidates)
+            hp._wcands.copy_(candidates)
+            hp.stats._after_torch(places)  # outputs and candidate copies are ready before use
+            hp.stats.set_count_sms(max(1, sms - max(0, reserve_sms)))
+        Mi = np.ascontiguousarray(np.asarray(M.experts, np.int32))
+        lib = N.lib()
+        try:
+            pair[0].stats.reset()
+            pair[0].stats.add_tokens(windows[0])
+            for i in range(n):
+                cur = pair[i % 2]
+                if i + 1 < n:
+                    nxt = pair[(i + 1) % 2]
+                    nxt.stats.reset()
+                    nxt.stats.add_tokens(windows[i + 1])
+                N.check(lib.gimbal_window_place_async(
+                    cur.stats.handle, Mi.ctypes.data if Mi.size else None, Mi.size, M.anchor_gpu,
+                    C.c_void_p(cur._wcands.data_ptr()), int(n_c), self.alpha, self.beta,
+                    C.c_void_p(scores[i].data_ptr()), C.c_void_p(argmins[i].data_ptr()),
+                    C.c_void_p(places[i].data_ptr())), "window_place")
+        finally:
+            for hp in pair:
+                hp.stats.set_count_sms(sms)
+        errors = []
+        for hp in pair:  # every handle's deferred flags are read (and cleared) before raising
+            try:
+                hp.stats.sync()
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+        if errors:
+            raise errors[0]
+        candidates[0].copy_(pair[(n - 1) % 2]._wcands[0])
+        self._window_scores = scores
+        am = argmins.cpu().numpy()
+        pl = places.cpu().numpy()
         prev = None if previous is None else np.asarray(previous, np.int32)
-        pair[0].stats.reset()
-        pair[0].stats.add_tokens(windows[0])
-        for i in range(len(windows)):
-            cur = pair[i % 2]
-            if i + 1 < len(windows):
-                nxt = pair[(i + 1) % 2]
-                nxt.stats.reset()
-                nxt.stats.add_tokens(windows[i + 1])
-            gp = greedy_place_array(cur.stats, M, self.topo.n_gpus, out_u8_device=candidates[0])
-            _, am = eval_costs(cur.stats, candidates, self.alpha, self.beta, out=cur._scores(candidates.shape[0]))
+        out = []
+        for i in range(n):
+            gp = pl[i]
             moved = int(np.count_nonzero(prev != gp)) if prev is not None and prev.shape == gp.shape else len(gp)
-            out.append((am, moved, gp))
+            out.append((int(am[i]), moved, gp))
             prev = gp
         return out
 

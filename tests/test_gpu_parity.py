@@ -267,17 +267,44 @@ def test_stream_windows_match_oracle(G, orc, shape):
     cA, cE, _ = orc.stats(L, ne, k, calib.cpu().numpy())
     assert M.experts == list(orc.affinity_set(L, ne, g, cE, 0.0, 4))
     out = hp.stream(wins, cands, M)
+    scores = hp._window_scores.cpu().numpy()
     prev = None
-    for w, (am, moved, gp) in zip(wins, out):
+    for i, (w, (am, moved, gp)) in enumerate(zip(wins, out)):
         oA, oE, _ = orc.stats(L, ne, k, w.cpu().numpy())
         ogp = np.asarray(orc.greedy_place(L, ne, g, oA, M.experts, 0), np.int32)
         assert np.array_equal(gp, ogp)
         hc = cands.cpu().numpy()
         hc[0] = ogp.astype(np.uint8)  # the loop scores the window's greedy as candidate 0
-        _, _, _, oam = orc.eval_costs(L, ne, g, oA, oE, hc)
+        D, cut, obj, oam = orc.eval_costs(L, ne, g, oA, oE, hc)
         assert am == oam
+        assert np.array_equal(scores[i][0], D) and np.array_equal(scores[i][1], cut)
+        assert np.array_equal(scores[i][2], obj)
         assert moved == (len(ogp) if prev is None else int(np.count_nonzero(prev != ogp)))
         prev = ogp
+    # the queued path leaves the handles usable by the synchronous API
+    hp.stats.reset()
+    hp.stats.add_tokens(wins[-1])
+    res = hp.place_with(M, cands)
+    assert res.greedy == list(out[-1][2])
+
+
+def test_stream_infeasible_candidate_reported_at_sync(G):
+    """gimbal_window_place_async defers device-side errors: an infeasible candidate row in the
+    queued windows raises (like check_feasible, placement.cpp:30-50) when the stream syncs, and
+    the flag is cleared afterwards."""
+    L, ne, k, g = SHAPES["dsv2lite"]
+    topo = G.MoeTopology(L, ne, k, g)
+    wins = [G.generate_trace(topo, 3000, model_seed=1, stream_seed=2, first_token=w * 3000, device=0)
+            for w in range(3)]
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 5, 8)).cuda()
+    cands[5, 3] = (int(cands[5, 3]) + 1) % g  # one GPU over, one under its m/g share
+    hp = G.HotPath(topo, 0)
+    M = hp.calibrate(wins[0])
+    with pytest.raises(ValueError, match="infeasible"):
+        hp.stream(wins, cands, M)
+    cands[5, 3] = (int(cands[5, 3]) - 1) % g
+    out = hp.stream(wins, cands, M)
+    assert len(out) == 3
 
 
 @pytest.mark.parametrize("threshold,top_e,cap", [(0.0, 4, None), (0.0, -1, None), (50.0, 16, 7), (1e12, 4, None),
