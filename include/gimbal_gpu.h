@@ -143,6 +143,18 @@ int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t n_M, i
                               uint8_t* candidates_device, int64_t n_candidates, double alpha, double beta,
                               double* scores_device, int64_t* argmin_device, int32_t* placement_device);
 
+/* The whole placement half of the north-star pass queued on the handle's stream with NO host
+ * synchronisation: build_affinity_set (placement.cpp:186-238; members -> `members` [m] and
+ * `n_members` [1], device int32) -> greedy_place with that set on anchor_gpu (placement.cpp:240-299;
+ * -> `placement` [m] int32 and row 0 of `candidates`) -> eval_cost of all C candidates ->
+ * `scores` [3][C] f64 and `argmin` [1] int64 (device).  capacity must be <= m/g (the reference's
+ * greedy_place would reject a larger set).  Device-side errors are reported by the next
+ * gimbal_stats_sync. */
+int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity, int32_t anchor_gpu,
+                      uint8_t* candidates_device, int64_t n_candidates, double alpha, double beta,
+                      double* scores_device, int64_t* argmin_device, int32_t* placement_device,
+                      int32_t* members_device, int32_t* n_members_device);
+
 /* Counting kernels of this handle run on n_sms SMs (default: all).  Leaving SMs free lets a
  * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms);

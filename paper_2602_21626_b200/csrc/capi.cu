@@ -730,31 +730,16 @@ int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t C, in
   return GIMBAL_OK;
 }
 
-int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity,
-                        int32_t anchor_gpu, int32_t* out, int32_t* n_out) {
-  GIMBAL_TRY(check_handle(h));
-  if (!out || !n_out) return invalid("build_affinity_set: null output");
-  if (anchor_gpu < 0 || anchor_gpu >= h->topo.n_gpus)
-    return invalid("build_affinity_set: anchor_gpu out of range");
-  std::lock_guard<std::mutex> lk(h->mu);
-  DeviceGuard g(h->device);
+namespace {
+
+// Queues build_affinity_set on the handle's E: member bitmask `bits` (m bits), sorted member ids
+// `dout` and their count `dn` (device), no host synchronisation.  L >= 2, (L-1)*n_e^2 < 2^24.
+int enqueue_affinity(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity, uint32_t* bits,
+                     int32_t* dout, int32_t* dn) {
   const int L = h->topo.n_layers, ne = h->topo.n_experts;
-  if (L < 2) {
-    *n_out = 0;
-    return h->check_flags();
-  }
   const int64_t n = h->nE();
-  if (n >= (1ll << 24)) {
-    set_error("build_affinity_set: (L-1)*n_experts^2 must be < 2^24");
-    return GIMBAL_NOT_SUPPORTED;
-  }
   const int64_t n_pad = next_pow2(n);
-  const int64_t m = h->m();
   GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
-  GIMBAL_TRY(h->misc.ensure((size_t)((m + 31) / 32) * 4 + (size_t)m * 4 + 16));
-  uint32_t* bits = h->misc.as<uint32_t>();
-  int32_t* dout = reinterpret_cast<int32_t*>(bits + (m + 31) / 32);
-  int32_t* dn = dout + m;
   if (top_e >= 1 && top_e <= kTopkMax) {
     // only the top_e heaviest pairs can survive truncation: segment top-K, no full sort
     unsigned long long* ka = h->keys.as<unsigned long long>();
@@ -774,6 +759,33 @@ int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32
     GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, h->keys.as<unsigned long long>(), n, top_e, capacity, bits,
                                            dout, dn, h->stream));
   }
+  return GIMBAL_OK;
+}
+
+}  // namespace
+
+int gimbal_affinity_set(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity,
+                        int32_t anchor_gpu, int32_t* out, int32_t* n_out) {
+  GIMBAL_TRY(check_handle(h));
+  if (!out || !n_out) return invalid("build_affinity_set: null output");
+  if (anchor_gpu < 0 || anchor_gpu >= h->topo.n_gpus)
+    return invalid("build_affinity_set: anchor_gpu out of range");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  if (h->topo.n_layers < 2) {
+    *n_out = 0;
+    return h->check_flags();
+  }
+  if (h->nE() >= (1ll << 24)) {
+    set_error("build_affinity_set: (L-1)*n_experts^2 must be < 2^24");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  const int64_t m = h->m();
+  GIMBAL_TRY(h->misc.ensure((size_t)((m + 31) / 32) * 4 + (size_t)m * 4 + 16));
+  uint32_t* bits = h->misc.as<uint32_t>();
+  int32_t* dout = reinterpret_cast<int32_t*>(bits + (m + 31) / 32);
+  int32_t* dn = dout + m;
+  GIMBAL_TRY(enqueue_affinity(h, threshold, top_e, capacity, bits, dout, dn));
   int32_t cnt = 0;
   GIMBAL_CUDA_TRY(cudaMemcpyAsync(&cnt, dn, 4, cudaMemcpyDeviceToHost, h->stream));
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -902,6 +914,49 @@ int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t nM, in
   GIMBAL_TRY(enqueue_greedy(h, gs, nM, anchor, placement, candidates));
   // evaluator flags go to the deferred word (dflags[1]): reset() clears only the count-state word,
   // so an infeasible candidate in any queued window is still reported by gimbal_stats_sync
+  return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
+                      reinterpret_cast<long long*>(argmin), h->dflags + 1);
+}
+
+int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity, int32_t anchor,
+                      uint8_t* candidates, int64_t C, double alpha, double beta, double* scores, int64_t* argmin,
+                      int32_t* placement, int32_t* members, int32_t* n_members) {
+  GIMBAL_TRY(check_handle(h));
+  if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
+  if (anchor < 0 || anchor >= h->topo.n_gpus) return invalid("build_affinity_set: anchor_gpu out of range");
+  if (C < 1 || !candidates || !scores || !argmin || !placement || !members || !n_members)
+    return invalid("pass: needs C >= 1 device candidates and device outputs");
+  if (h->topo.n_gpus > 255) return invalid("eval_costs: uint8 candidates need n_gpus <= 255");
+  const int64_t m = h->m();
+  // greedy_place rejects |M| > m/g (placement.cpp:252); with capacity <= m/g that cannot happen,
+  // so the whole pass can be queued without looking at |M|
+  if (capacity > m / h->topo.n_gpus) return invalid("pass: capacity must be <= m/g (greedy_place anchor capacity)");
+  if (m >= (1ll << 24) || h->nE() >= (1ll << 24)) {
+    set_error("pass: m and (L-1)*n_experts^2 must be < 2^24");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  GIMBAL_TRY(h->derive());
+  // scratch sized before anything is queued (a regrown buffer is freed, not stream-ordered)
+  GreedyScratch gs{};
+  GIMBAL_TRY(greedy_scratch(h, 0, 1, gs));  // only the walk's per-position scratch is used
+  h->m_cached_buf = nullptr;
+  GIMBAL_TRY(h->misc.ensure((size_t)((m + 31) / 32) * 4 + 64));
+  uint32_t* bits = h->misc.as<uint32_t>();
+  if (h->topo.n_layers < 2) {
+    GIMBAL_CUDA_TRY(cudaMemsetAsync(bits, 0, (size_t)((m + 31) / 32) * 4, h->stream));
+    GIMBAL_CUDA_TRY(cudaMemsetAsync(n_members, 0, 4, h->stream));
+  } else {
+    GIMBAL_TRY(enqueue_affinity(h, threshold, top_e, capacity, bits, members, n_members));
+  }
+  const int L = h->topo.n_layers, ne = h->topo.n_experts, g = h->topo.n_gpus;
+  const int64_t n_pad = next_pow2(m);
+  GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, bits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
+                                     h->stream));
+  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
+  GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, members, -1, anchor, h->keys.as<unsigned long long>(), m,
+                                     placement, candidates, gs.tent, h->stream, n_members));
   return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
                       reinterpret_cast<long long*>(argmin), h->dflags + 1);
 }

@@ -74,9 +74,9 @@ __device__ void sequential_walk(int g, int cap, const unsigned long long* __rest
 template <int G>  // G = n_gpus (<= 32) for the layer-parallel path; 0 = fully sequential
 __global__ void __launch_bounds__(kThreads)
     greedy_walk_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
-                       const int32_t* __restrict__ M, int32_t nM, int32_t anchor,
-                       const unsigned long long* __restrict__ keys, int64_t n_keys, int32_t* __restrict__ out,
-                       uint8_t* __restrict__ out_u8, uint8_t* __restrict__ tent) {
+                       const int32_t* __restrict__ M, int32_t nM, const int32_t* __restrict__ nM_dev,
+                       int32_t anchor, const unsigned long long* __restrict__ keys, int64_t n_keys,
+                       int32_t* __restrict__ out, uint8_t* __restrict__ out_u8, uint8_t* __restrict__ tent) {
   extern __shared__ unsigned long long load[];  // [L][g] loads, then counts [g]
   int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
   __shared__ long long s_nvalid, s_npos, s_star;
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(kThreads)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int i = 0; i < nM; ++i) {  // placement.cpp:272-279: the strong-pair set on the anchor
+    const int32_t n_set = nM >= 0 ? nM : *nM_dev;  // device count: set built by affinity_select
+    for (int i = 0; i < n_set; ++i) {  // placement.cpp:272-279: the strong-pair set on the anchor
       const int e = M[i];
       out[e] = anchor;
       if (out_u8) out_u8[e] = (uint8_t)anchor;
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(kThreads)
 
 cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M, int32_t nM,
                                int32_t anchor, const unsigned long long* keys, int64_t n_keys, int32_t* out,
-                               uint8_t* out_u8, uint8_t* tent_scratch, cudaStream_t s) {
+                               uint8_t* out_u8, uint8_t* tent_scratch, cudaStream_t s, const int32_t* nM_dev) {
   const size_t base = (size_t)L * g * 8 + (size_t)4 * ((g + 3) / 4) * 4;
   const size_t n_pad = (size_t)((n_keys + 15) & ~15ll);
   const size_t staged = base + n_pad * 12;  // key (8 B) + list entry (2) + layer + tentative GPU per position
@@ -316,7 +317,7 @@ cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A
                         : greedy_walk_kernel<0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<1, kThreads, smem, s>>>(L, ne, g, A, M, nM, anchor, keys, n_keys, out, out_u8, tent_scratch);
+  kern<<<1, kThreads, smem, s>>>(L, ne, g, A, M, nM, nM_dev, anchor, keys, n_keys, out, out_u8, tent_scratch);
   return cudaGetLastError();
 }
 

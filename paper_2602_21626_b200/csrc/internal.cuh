@@ -169,7 +169,7 @@ cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uin
 cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A, const int32_t* M,
                                int32_t nM, int32_t anchor, const unsigned long long* keys,
                                int64_t n_keys, int32_t* out, uint8_t* out_u8, uint8_t* tent_scratch,
-                               cudaStream_t s);
+                               cudaStream_t s, const int32_t* nM_dev = nullptr);  // nM < 0: read *nM_dev
 
 // Sort uint64 keys descending in place (bitonic; n must be a power of two).
 cudaError_t sort_u64_desc(unsigned long long* keys, int64_t n, cudaStream_t s);

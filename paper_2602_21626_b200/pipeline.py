@@ -105,11 +105,47 @@ class HotPath:
         """Stats already counted: M -> greedy (written into candidates[0] if greedy_row) ->
         scores -> argmin.  candidates: CUDA uint8 tensor [C][m]."""
         topo = self.topo
+        if (greedy_row and getattr(candidates, "is_cuda", False) and candidates.shape[0] > 0
+                and topo.n_gpus <= 255):
+            return self._place_queued(candidates)
         M = build_affinity_set(self.stats, topo, self.threshold, self.top_e,
                                topo.total_experts() // topo.n_gpus, self.anchor_gpu)
         gp = greedy_place(self.stats, M, topo.n_gpus, out_u8_device=candidates[0] if greedy_row else None)
         out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
         return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
+
+    def _place_queued(self, candidates) -> HotPathResult:
+        """place() as one queued device chain (gimbal_pass_async: strong-pair set, greedy, scores,
+        argmin), then a single read-back of [argmin | |M| | M | greedy] and one stream sync."""
+        import torch
+
+        topo = self.topo
+        m, C_ = topo.total_experts(), int(candidates.shape[0])
+        dev = torch.device("cuda", self.device)
+        if getattr(self, "_pk", None) is None:
+            # int32 words: [0:2] argmin (int64), [2] |M|, [3] pad, [4:4+m] M, [4+m:4+2m] greedy
+            self._pk = torch.zeros(4 + 2 * m, dtype=torch.int32, device=dev)
+            self._pk_host = torch.empty(4 + 2 * m, dtype=torch.int32).pin_memory()
+            self._hstream = torch.cuda.ExternalStream(self.stats.device_buffers()[2], device=dev)
+        scores = self._scores(C_)
+        self.stats._after_torch(candidates)
+        base = self._pk.data_ptr()
+        N.check(N.lib().gimbal_pass_async(
+            self.stats.handle, self.threshold, self.top_e, m // topo.n_gpus, self.anchor_gpu,
+            C.c_void_p(candidates.data_ptr()), C_, self.alpha, self.beta, C.c_void_p(scores.data_ptr()),
+            C.c_void_p(base), C.c_void_p(base + 16 + 4 * m), C.c_void_p(base + 16), C.c_void_p(base + 8)),
+            "pass")
+        # the read-back runs on torch's stream behind the handle's (a pinned block used on the
+        # handle's own stream would outlive it in torch's host allocator)
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_stream(self._hstream)
+        self._pk_host.copy_(self._pk, non_blocking=True)
+        self.stats.sync()  # raises deferred device-side errors
+        cur.synchronize()
+        h = self._pk_host.numpy()
+        n = int(h[2])
+        return HotPathResult(affinity=AffinitySet(experts=h[4:4 + n].tolist(), anchor_gpu=self.anchor_gpu),
+                             greedy=h[4 + m:4 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
 
     def place_with(self, M: AffinitySet, candidates, greedy_row: bool = True) -> HotPathResult:
         """Stats already counted, strong-pair set fixed (sim.cpp:94-104 computes M once from a
