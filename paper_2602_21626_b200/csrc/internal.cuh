@@ -147,6 +147,10 @@ size_t eval_scratch_bytes(int64_t C);
 // max over E cells (for choosing 32-bit partial sums in the evaluator)
 cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s);
 
+// tensor-core same-GPU weights (eval_mma.cu): n_e in {128, 256}, g in {4, 8, 16}, cells < 2^27
+bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C);
+cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, const uint8_t* cands, int64_t C,
+                            unsigned long long* same, cudaStream_t s);
 cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
                                const unsigned long long* same, const double* D, double* cut,
                                double* obj, long long* argmin, uint32_t* flags, cudaStream_t s);

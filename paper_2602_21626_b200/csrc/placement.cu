@@ -523,7 +523,11 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
   e = cudaMemcpyAsync(bad_index, &init, sizeof(init), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   const bool fast = small_cells && ne % 32 == 0 && 256 % ne == 0;
-  if (L > 1 && fast) {
+  if (small_cells && eval_mma_supported(L, ne, g, cands, C)) {
+    // tensor cores: E byte planes x one-hot assignment (eval_mma.cu)
+    e = launch_eval_mma(L, ne, g, E, cands, C, scratch_same, s);
+    if (e != cudaSuccess) return e;
+  } else if (L > 1 && fast) {
     const int64_t rows = (int64_t)(L - 1) * ne;
     const int rows_per_cta = kEvalCellsPerCta / ne;
     const int64_t ctas = (rows + rows_per_cta - 1) / rows_per_cta;

@@ -485,3 +485,26 @@ def test_bench_scale_properties(G):
     for assign in (G.static_placement(topo).assign, list(G.shuffled_candidates(L * ne, g, 5, 1)[0])):
         _, cut, _, _ = G.eval_costs(s, np.asarray([assign], np.uint8))
         assert cut[0] == float(G.comm_cost(stream, assign))
+
+
+@pytest.mark.parametrize("L,ne,k,g,C", [(58, 256, 8, 8, 70), (48, 128, 8, 8, 33), (12, 256, 8, 4, 41),
+                                        (9, 128, 4, 16, 17), (58, 256, 8, 16, 129), (3, 128, 8, 4, 1)])
+def test_eval_tensor_core_path_matches_oracle(G, orc, monkeypatch, L, ne, k, g, C):
+    """eval_mma.cu (E byte planes x one-hot assignment on tcgen05 kind::i8) gives exactly the
+    oracle's D / cut / objective / argmin (placement.cpp:58-85), like the integer-ALU evaluator,
+    on ragged candidate counts (partial groups) and every supported g."""
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 20011, model_seed=2, stream_seed=5, device=0)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(trace)
+    oA, oE, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+    cands = G.shuffled_candidates(L * ne, g, 31, C)
+    want = orc.eval_costs(L, ne, g, oA, oE, cands, 2.0, 0.5)
+    got = G.eval_costs(s, torch.from_numpy(cands).cuda(), 2.0, 0.5)
+    for a, b in zip(got[:3], want[:3]):
+        assert np.array_equal(a, b)
+    assert got[3] == want[3]
+    monkeypatch.setenv("GIMBAL_EVAL_ALU", "1")  # the integer-ALU evaluator agrees
+    alu = G.eval_costs(s, torch.from_numpy(cands).cuda(), 2.0, 0.5)
+    for a, b in zip(alu[:3], want[:3]):
+        assert np.array_equal(a, b)
