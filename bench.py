@@ -92,6 +92,8 @@ def count_kernel(ne, k, L=58):
         return "count_mma_stack_kernel (tcgen05.mma kind::i8, two 64-expert layers per 128-row operand)", "tensor"
     if 64 < ne <= 128:
         return "count_mma_kernel (tcgen05.mma kind::i8, TMEM accumulators)", "tensor"
+    if (L - 1) * ne * ne * 4 <= 48 * 1024 and k <= 8 and not os.environ.get("GIMBAL_NO_SMALL"):
+        return "count_small_tm_kernel (whole E in shared memory, token-major trace, one pass)", "atomics"
     if ne * ne * 4 <= 200 * 1024:
         return "count_lm8_pairs_kernel", "atomics"
     if ne % 64 == 0 and ne * ne * 2 <= 200 * 1024:

@@ -272,6 +272,14 @@ struct gimbal_stats_s {
       GIMBAL_TRY(timing_end());
       return GIMBAL_OK;
     }
+    if (small_count_supported(L, topo.n_experts, topo.top_k, id_bytes, n) && !std::getenv("GIMBAL_NO_SMALL")) {
+      // the whole E fits every CTA's shared memory (Mixtral class): one pass, no transposition
+      GIMBAL_TRY(timing_begin());
+      GIMBAL_CUDA_TRY(launch_count_small(L, topo.n_experts, topo.top_k, sms, static_cast<const uint8_t*>(ids), n,
+                                         dE, dflags, stream));
+      GIMBAL_TRY(timing_end());
+      return GIMBAL_OK;
+    }
     if (lm8_supported(L, topo.n_experts, topo.top_k, id_bytes)) {
       // the transposition must see work already queued on `stream` (e.g. host staging)
       GIMBAL_CUDA_TRY(cudaEventRecord(ev_order, stream));

@@ -88,6 +88,10 @@ struct Lm8Plan {
   int P = 1, R = 0, n_groups = 0, n_parts = 1;
 };
 bool lm8_supported(int L, int ne, int k, int id_bytes);
+// whole-E-in-shared-memory counting straight from the token-major uint8 trace (small_count.cu)
+bool small_count_supported(int L, int ne, int k, int id_bytes, int64_t T);
+cudaError_t launch_count_small(int L, int ne, int k, int sms, const uint8_t* trace, int64_t T,
+                               unsigned long long* E, uint32_t* flags, cudaStream_t s);
 Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin);
 cudaError_t launch_transpose_lm8(const uint8_t* trace, int64_t T, int L, int ne, int k,
                                  unsigned long long* X, int64_t ld, uint32_t* flags, cudaStream_t s);
