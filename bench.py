@@ -217,8 +217,10 @@ def extrapolated_rate(r, sT, sC, T, C):
     return T / total
 
 
-def cpu_baseline(config, T, C):
-    """Rank 0, N = 1: the reference's own code (oracle/_ref) on host cores, bounded sample."""
+def cpu_baseline(config, T, C, windows=1):
+    """Rank 0, N = 1: the reference's own code (oracle/_ref) on host cores, bounded sample.  With
+    `windows` > 1 (streaming) the placement stages run once per window: stats scale with T, strong-
+    pair set + greedy + C eval_cost calls with the window count."""
     import oracle
 
     L, ne, k, g, _, _, _ = CONFIGS[config]
@@ -229,11 +231,14 @@ def cpu_baseline(config, T, C):
     cores = os.cpu_count() or 1
     r = oracle.Ref().pipeline(L, ne, k, g, ids, cands, n_threads=cores)
     rate = extrapolated_rate(r, sT, sC, T, C)
+    if windows > 1:
+        rate = T / (r["t_stats"] / sT * T + windows * (r["t_place"] + r["t_eval"] / max(sC, 1) * C))
     return {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference",
             "sample": f"{sT} tokens (add_token over {cores} RoutingStats shards + affinity/flat forms + "
                       f"build_affinity_set + greedy_place) and {sC} eval_cost calls on the reference's own "
                       f"moe.cpp/placement.cpp; stage times {r['t_stats']:.3f}/{r['t_place']:.3f}/{r['t_eval']:.3f} s, "
-                      f"extrapolated linearly to {T} tokens, {C} candidates"}
+                      f"extrapolated linearly to {T} tokens, {C} candidates"
+                      + (f" per window x {windows} windows" if windows > 1 else "")}
 
 
 def main():
@@ -322,8 +327,42 @@ def main():
         ms = float(tt.item())
     value = world * T / (ms * 1e-3)
 
-    # roofline of the dominant kernel (E counting): algorithmic bytes per launch = the launch's
-    # trace bytes (tokens * L * k uint8) + one u64 write of E; duration = average launch time
+    roof = make_roofline(args, topo, T, count_total_ms, count_launches, ms)
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(G, topo, trace, cands_host, T, args, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(args.config, T, C)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
+            "data": "synthetic (Zipf-skewed RoutingModel-semantics trace generated on the GPU)",
+            "config": {"workload": desc, "tokens_per_gpu": T, "candidates": C, "g": g,
+                       "parallelism": f"token-shard dp{world}",
+                       "l2": f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": kernel_launches_per_step(topo, count_launches / args.steps) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def make_roofline(args, topo, T, count_total_ms, count_launches, ms, traffic=True):
+    """Roofline of the dominant kernel (E counting) over `args.steps` steps of T tokens: algorithmic
+    bytes per launch = the launch's trace bytes (tokens * L * k uint8) + one u64 write of E; duration
+    = average launch time (CUDA events on the counting stream)."""
+    L, ne, k = topo.n_layers, topo.n_experts, topo.top_k
     roof = None
     if count_launches:
         launch_ms = count_total_ms / count_launches
@@ -336,7 +375,7 @@ def main():
         kernel, engine = count_kernel(ne, k, L)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": (TRAFFIC[args.config]["bytes"] / TRAFFIC[args.config]["tokens_in_launch"] * tok_per_launch
-                            if args.config in TRAFFIC else None),
+                            if traffic and args.config in TRAFFIC else None),
                 "traffic_source": TRAFFIC.get(args.config, {}).get("source"),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
                 "kernel": kernel,
@@ -375,34 +414,7 @@ def main():
             roof["atomic_ceiling"] = {"bound": "shared-memory atomics", "achieved": upd, "peak": ATOMS_RANDOM_PEAK,
                                       "unit": "E pair-updates/s", "frac": upd / ATOMS_RANDOM_PEAK,
                                       "peak_source": "profiles/r1_atoms_microbench.md (random-address ATOMS)"}
-
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
-    e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(G, topo, trace, cands_host, T, args, local)
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            cpu = cpu_baseline(args.config, T, C)
-        except Exception as ex:  # reported, not fatal
-            cpu = {"error": str(ex)}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
-            "data": "synthetic (Zipf-skewed RoutingModel-semantics trace generated on the GPU)",
-            "config": {"workload": desc, "tokens_per_gpu": T, "candidates": C, "g": g,
-                       "parallelism": f"token-shard dp{world}",
-                       "l2": f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": kernel_launches_per_step(topo, count_launches / args.steps) * args.steps,
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    return roof
 
 
 def kernel_launches_per_step(topo, count_launches_per_step, top_e=4):
@@ -480,6 +492,9 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local).start() if rank == 0 else None
+    handles = [hp.stats] + ([hp._twin().stats] if getattr(hp, "_twin_hp", None) is not None else [])
+    for h in handles:
+        h.count_timing(True)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -491,11 +506,25 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
         dist.barrier()
     ms = t0.elapsed_time(t1) / args.steps
     clk = clocks.stop() if clocks else None
+    count_ms, count_launches = 0.0, 0
+    for h in handles:
+        a, b = h.count_timing(False)
+        count_ms, count_launches = count_ms + a, count_launches + b
     if world > 1:
         tt = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     tokens = world * per_rank * n_win
+    roof = make_roofline(args, topo, per_rank * n_win, count_ms, count_launches, ms, traffic=False)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_stream_e2e(G, topo, windows, cands.cpu(), M, args, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline("dsv3", per_rank * n_win, C, windows=n_win)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"error": str(ex)}
     if rank == 0:
         moved = [r[1] for r in res]
         line = {
@@ -507,12 +536,75 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
                        "parallelism": f"token-shard dp{world} per window",
                        "strong_pair_set": M.experts, "mean_moved_per_window": float(np.mean(moved[1:])) if len(moved) > 1
                        else None},
-            "roofline": None, "cpu_baseline": None, "e2e": None, "clocks": clk,
-            "gpu_launches": None,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": stream_launches(topo, n_win, count_launches / args.steps) * args.steps,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
+
+
+def stream_launches(topo, n_win, count_launches_per_step):
+    """Our kernels per streaming step: per window the counting launch(es) (measured), derive A + W,
+    greedy (keys + bitonic sort + walk) and the evaluator (same + dev + finish)."""
+    def sort_launches(n):
+        p = 1
+        while p < n:
+            p <<= 1
+        if p <= 2048:
+            return 1
+        c, kk = 1, 4096
+        while kk <= p:
+            j = kk // 2
+            while j >= 2048:
+                c += 1
+                j //= 2
+            c += 1
+            kk *= 2
+        return c
+
+    per_window = 2 + 1 + sort_launches(topo.total_experts()) + 1 + 3
+    return int(round(count_launches_per_step + n_win * per_window))
+
+
+def run_stream_e2e(G, topo, windows, cands_host, M, args, local):
+    """The streaming step through the public API from pinned host memory: every window's ids and
+    the candidate batch cross PCIe inside the timed region (counted while copied, double-buffered
+    per handle), each window's greedy placement and argmin come back at the end."""
+    import torch
+
+    try:
+        host = [torch.empty(tuple(w.shape), dtype=torch.uint8, pin_memory=True) for w in windows]
+        for h, w in zip(host, windows):
+            h.copy_(w)
+        ch = cands_host.pin_memory()
+    except Exception as ex:
+        return {"error": f"pinned host buffers unavailable: {ex}"}
+    hp = G.HotPath(topo, device=local)
+    stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", local))
+
+    def step():
+        dcands = ch.to(f"cuda:{local}", non_blocking=True)
+        return hp.stream(host, dcands, M)
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    n = max(1, min(args.steps, 2))
+    for _ in range(n):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    wall = (time.perf_counter() - t0) / n * 1e3
+    T = sum(int(w.shape[0]) for w in windows)
+    m, L, k = topo.total_experts(), topo.n_layers, topo.top_k
+    return {"value": T / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": int(T * L * k + ch.numel()),
+            "d2h_bytes_per_step": int(len(windows) * (m * 4 + 8)), "ms_per_step": ms, "wall_ms_per_step": wall,
+            "steps": n}
 
 
 def run_e2e(G, topo, trace, cands_host, T, args, local):
