@@ -8,14 +8,19 @@
 // E cells are < 2^27 on this path (the host's small-cell test), so E_l is split into four u8 byte
 // planes and each plane is an exact u8 x u8 -> s32 product (<= 255 * n_e per accumulator).
 //
-// CTA work unit = (pair l, block of 128 rows j, candidate range).  The unit's four A planes
-// (128 rows x n_e, K-major: core matrix = 8 rows x 16 bytes) are built once from the u64 E; then
-// per group of 128/g candidates the B tile H = [(candidate, gpu) x k] one-hot (K-major, built with
-// __vcmpeq4 from four GPU ids at a time) is staged in a 2-deep ring while the previous group's MMAs
-// run, and one thread issues 4 planes x n_e/32 instructions (M = 128 rows, N = 128 (c, p) columns,
-// K = 32) into four 128-column s32 accumulators (all 512 TMEM columns).  Four warps read their
-// rows back with tcgen05.ld, pick column P_c(l, j) per candidate, recombine the planes
-// (sum v_b << 8b) and reduce the rows of the block into same[c] (u64 atomics).
+// CTA work unit = (pair l, block of 128 rows j, candidate range).  Warp roles (288 threads):
+//  * warps 4-7 (producers) build the unit's four A planes once (128 rows x n_e, K-major: core
+//    matrix = 8 rows x 16 bytes) from the u64 E, then per group of 64/g candidates the one-hot
+//    B tile H = [(candidate, gpu) x k] (K-major, __vcmpeq4 on four GPU ids at a time);
+//  * warp 8 (issuer) bulk-copies each group's candidate id rows (cp.async.bulk, one copy per lane)
+//    two groups ahead into a 4-slot ring, and one lane issues 4 planes x n_e/32 instructions
+//    (M = 128 rows, N = 64 (c, p) columns, K = 32) into one of two TMEM buffers (4 planes x 64
+//    columns each) and commits them;
+//  * warps 0-3 (epilogue) read the finished buffer back with tcgen05.ld (lane = row j), pick the
+//    candidate's column P_c(l, j), recombine the planes (sum v_b << 8b), release the buffer and
+//    reduce-scatter the rows over the warp into same[c] (u64 atomics),
+// so a group's epilogue overlaps the next groups' one-hot builds and MMAs.  mbarriers: ids full
+// (TMA tx), B full (4 producer warps), MMA done (tcgen05.commit), TMEM free (4 epilogue warps).
 //
 // Work per candidate is 4 x (L-1) x n_e^2 x g MACs on the tensor pipe instead of (L-1) x n_e^2
 // compare-and-adds on the integer pipe (eval_same_fast_kernel, placement.cu).
@@ -33,15 +38,16 @@ namespace gimbal_gpu {
 namespace {
 
 constexpr int kRowsBlk = 128;  // MMA M: rows j of one layer-l block
-constexpr int kN = 128;        // MMA N: (candidate, gpu) columns per group
+constexpr int kN = 64;         // MMA N: (candidate, gpu) columns per group
 constexpr int kPlanes = 4;     // byte planes of a cell < 2^27
-constexpr int kThreads = 256;
-constexpr int kBStages = 2;
-constexpr int kIdSlots = 3;  // candidate-id ring, filled two groups ahead
+constexpr int kThreads = 288;  // warps 0-3 epilogue, warps 4-7 producers, warp 8 issuer
+constexpr int kBStages = 2;    // one-hot tiles = TMEM buffers
+constexpr int kIdSlots = 4;    // candidate-id ring, filled two groups ahead
+constexpr int kIssuerWarp = 8;
 
 struct EvalMmaParams {
-  int L, ne, g, cpg;  // cpg = candidates per group (kN / g)
-  int n_jb, n_cr;     // row blocks per pair, candidate ranges
+  int L, ne, g;
+  int n_jb, n_cr;  // row blocks per pair, candidate ranges
   int64_t C, m, range_cands, n_units;
   uint32_t idesc;
 };
@@ -55,6 +61,27 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr, uint32_t sbo) {
   d |= (uint64_t)((sbo >> 4) & 0x3fffu) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
   return d;
+}
+
+// r = c ? a : b as a real select (a plain ?: chain over v[p] is turned into an indexed local-memory
+// load of the accumulator row by the compiler)
+__device__ __forceinline__ uint32_t selp(uint32_t c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tselp.b32 %0, %2, %3, q;\n\t}" : "=r"(r) : "r"(c), "r"(a), "r"(b));
+  return r;
+}
+
+// v[o + p] for p < G by a binary select tree on the bits of p
+template <int G>
+__device__ __forceinline__ uint32_t pick(const uint32_t* v, uint32_t p) {
+  uint32_t t[G];
+#pragma unroll
+  for (int i = 0; i < G; ++i) t[i] = v[i];
+#pragma unroll
+  for (int w = G / 2, bit = 1; w >= 1; w >>= 1, bit <<= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] = selp(p & (uint32_t)bit, t[2 * i + 1], t[2 * i]);
+  return t[0];
 }
 
 __device__ __forceinline__ uint32_t kmajor_off(int row, int k, uint32_t sbo) {
@@ -88,19 +115,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // matrix (lane = row-in-core * 4 + word), so a warp's stores cover 128 contiguous bytes.
 template <int G>
 __device__ __forceinline__ void build_onehot(uint8_t* B, const uint8_t* ids, int ids_stride, int ne, int n_live,
-                                             uint32_t sbo) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kcs = ne >> 4;
-  for (int cm = warp; cm < (kN / 8) * kcs; cm += kThreads / 32) {
-    const int ng = cm / kcs, kc = cm - ng * kcs;
-    const int n = ng * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-    const int ci = n / G, p = n - ci * G;
-    uint32_t w = 0u;
-    if (ci < n_live) {
-      const uint32_t v = *reinterpret_cast<const uint32_t*>(ids + ci * ids_stride + k);
-      w = __vcmpeq4(v, (uint32_t)p * 0x01010101u) & 0x01010101u;
+                                             uint32_t sbo, int pwarp, int lane) {
+  // warp w covers 8-row groups ng = w, w + 4, ...; a lane's row n and candidate/GPU (ci, p) are
+  // fixed per row group, so the k loop is shifts and adds only
+#pragma unroll
+  for (int ng = pwarp; ng < kN / 8; ng += 4) {
+    const int n = ng * 8 + (lane >> 2);
+    const int ci = n / G, p = n % G;
+    const uint32_t pat = (uint32_t)p * 0x01010101u;
+    const bool on = ci < n_live;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(ids + ci * ids_stride) + (lane & 3);
+    uint8_t* dst = B + (uint32_t)ng * sbo + (uint32_t)(lane >> 2) * 16u + (uint32_t)(lane & 3) * 4u;
+    for (int kc = 0; kc < (ne >> 4); ++kc) {
+      const uint32_t w = on ? (__vcmpeq4(src[kc * 4], pat) & 0x01010101u) : 0u;
+      *reinterpret_cast<uint32_t*>(dst + kc * 128) = w;
     }
-    *reinterpret_cast<uint32_t*>(B + kmajor_off(n, k, sbo)) = w;
   }
 }
 
@@ -109,19 +138,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     eval_mma_kernel(EvalMmaParams prm, const unsigned long long* __restrict__ E, const uint8_t* __restrict__ cands,
                     unsigned long long* __restrict__ same) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[kBStages], id_bars[kIdSlots];
+  __shared__ uint64_t mma_done[kBStages], tmem_free[kBStages], b_full[kBStages], id_full[kIdSlots];
   __shared__ uint32_t tmem_slot;
-  constexpr int kCpg = kN / G;
+  constexpr int kCpg = kN / G;  // candidates per group
   const int ne = prm.ne;
   const int64_t m = prm.m;
   const uint32_t sbo = (uint32_t)(ne >> 4) * 128u;
   const int plane_bytes = kRowsBlk * ne;
   const int b_bytes = kN * ne;
   const int ids_stride = ne + kRowsBlk;  // per candidate: P_c(l+1, 0..n_e) then P_c(l, j0..j0+128)
+  const int ids_bytes = kCpg * ids_stride;
   uint8_t* A = smem;
   uint8_t* Bst = smem + kPlanes * plane_bytes;
-  uint8_t* idst = Bst + kBStages * b_bytes;  // kIdSlots slots of kCpg * ids_stride bytes
-  const int ids_bytes = kCpg * ids_stride;
+  uint8_t* idst = Bst + kBStages * b_bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0) {
@@ -130,8 +159,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kBStages; ++s) mbar_init(&bars[s], 1);
-    for (int s = 0; s < kIdSlots; ++s) mbar_init(&id_bars[s], 1);
+    for (int s = 0; s < kBStages; ++s) {
+      mbar_init(&mma_done[s], 1);
+      mbar_init(&tmem_free[s], 4);  // one arrival per epilogue warp
+      mbar_init(&b_full[s], 4);     // one arrival per producer warp
+    }
+    for (int s = 0; s < kIdSlots; ++s) mbar_init(&id_full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -139,28 +172,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_slot;
 
-  // thread 0: bulk-copy the GPU ids one group needs into id slot `slot` (16-byte aligned rows)
+  // issuer warp: bulk-copy the GPU ids one group needs into id slot `slot` (16-byte aligned
+  // rows), one copy per lane (candidate ci = lane / 2, lane & 1 = layer l+1 row / layer l slice)
   auto fetch_ids = [&](uint32_t slot, int l, int j0, int64_t c0, int n_live) {
     uint8_t* dst = idst + slot * ids_bytes;
-    const uint32_t bar = smem_u32(&id_bars[slot]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                 "r"((uint32_t)(n_live * (ne + kRowsBlk)))
-                 : "memory");
-    for (int ci = 0; ci < n_live; ++ci) {
-      const uint8_t* row = cands + (c0 + ci) * m;
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(dst + ci * ids_stride)),
-                   "l"(row + (int64_t)(l + 1) * ne), "r"(ne), "r"(bar)
+    const uint32_t bar = smem_u32(&id_full[slot]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)(n_live * (ne + kRowsBlk)))
                    : "memory");
+    __syncwarp();
+    for (int i = lane; i < 2 * n_live; i += 32) {
+      const int ci = i >> 1;
+      const uint8_t* row = cands + (c0 + ci) * m;
+      const bool lo = (i & 1) == 0;
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_u32(dst + ci * ids_stride + ne)),
-                   "l"(row + (int64_t)l * ne + j0), "r"(kRowsBlk), "r"(bar)
+                       smem_u32(dst + ci * ids_stride + (lo ? 0 : ne))),
+                   "l"(lo ? row + (int64_t)(l + 1) * ne : row + (int64_t)l * ne + j0), "r"(lo ? ne : kRowsBlk),
+                   "r"(bar)
                    : "memory");
     }
   };
 
-  // groups of this CTA so far: B stage = & 1 (MMA barrier phase (>> 1) & 1); id slot = % 3 (phase (/ 3) & 1)
-  uint32_t grp_global = 0;
+  // Both roles walk the same (unit, group) sequence; G_ counts this CTA's groups: B stage / TMEM
+  // buffer = G & 1 (barrier parity (G >> 1) & 1), id slot = G & 3 (parity (G >> 2) & 1).
+  uint32_t G_ = 0;
   for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
     const int cr = (int)(unit % prm.n_cr);
     const int64_t rest = unit / prm.n_cr;
@@ -172,80 +208,90 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (c_begin >= c_end) continue;
     const int n_groups = (int)((c_end - c_begin + kCpg - 1) / kCpg);
     auto live = [&](int gi) { return (int)min((int64_t)kCpg, c_end - c_begin - (int64_t)gi * kCpg); };
-    if (threadIdx.x == 0) {
-      fetch_ids(grp_global % kIdSlots, l, j0, c_begin, live(0));
-      if (n_groups > 1) fetch_ids((grp_global + 1) % kIdSlots, l, j0, c_begin + kCpg, live(1));
-    }
-    // A planes: byte b of the 128 x n_e block of E_l; eight 32-byte loads in flight per lane
-    {
-      const int kcs = ne >> 4;
-      const int n_cm = (kRowsBlk / 8) * kcs;
-      for (int cm0 = warp; cm0 < n_cm; cm0 += 8 * (kThreads / 32)) {
-        ulonglong2 v[8][2];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int cm = cm0 + u * (kThreads / 32);
-          if (cm < n_cm) {
-            const int rg = cm / kcs, kc = cm - rg * kcs;
-            const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-            const ulonglong2* src = reinterpret_cast<const ulonglong2*>(E + ((int64_t)l * ne + j0 + row) * ne + k);
-            v[u][0] = __ldg(src);
-            v[u][1] = __ldg(src + 1);
-          }
+
+    if (warp == kIssuerWarp) {
+      // ---------------- issuer: id fetches + MMAs ----------------
+      fetch_ids(G_ & 3, l, j0, c_begin, live(0));
+      if (n_groups > 1) fetch_ids((G_ + 1) & 3, l, j0, c_begin + kCpg, live(1));
+      for (int gi = 0; gi < n_groups; ++gi) {
+        const uint32_t Gg = G_ + gi, s = Gg & 1;
+        mbar_wait(&b_full[s], (Gg >> 1) & 1);                          // A (first group) and B(Gg) built
+        if (Gg >= 2) mbar_wait(&tmem_free[s], ((Gg - 2) >> 1) & 1);   // epilogue of Gg - 2 read buffer s
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(A), b0 = smem_u32(Bst + s * b_bytes);
+          const uint32_t d0 = tmem + s * (kPlanes * kN);
+          for (int b = 0; b < kPlanes; ++b)
+            for (int kk = 0; kk < ne / 32; ++kk)
+              mma_i8(d0 + (uint32_t)(b * kN), kmajor_desc(a0 + b * plane_bytes + kk * 256, sbo),
+                     kmajor_desc(b0 + kk * 256, sbo), prm.idesc, kk > 0 ? 1u : 0u);
+          mma_commit(&mma_done[s]);
         }
+        __syncwarp();
+        // the slot of group Gg + 2 last served group Gg - 2, whose epilogue has finished
+        if (gi + 2 < n_groups) fetch_ids((Gg + 2) & 3, l, j0, c_begin + (int64_t)(gi + 2) * kCpg, live(gi + 2));
+      }
+    } else if (warp >= 4) {
+      // ---------------- producers: A planes once per unit, a one-hot tile per group ----------------
+      const int pwarp = warp - 4;
+      // the previous unit's MMAs read the A planes: wait for the last of them
+      if (G_ >= 1) mbar_wait(&mma_done[(G_ - 1) & 1], ((G_ - 1) >> 1) & 1);
+      {
+        const int kcs = ne >> 4, kcs_shift = ne == 256 ? 4 : 3;
+        const int n_cm = (kRowsBlk / 8) * kcs;
+        for (int cm0 = pwarp; cm0 < n_cm; cm0 += 4 * 4) {
+          ulonglong2 v[4][2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int cm = cm0 + u * (kThreads / 32);
-          if (cm < n_cm) {
-            const int rg = cm / kcs, kc = cm - rg * kcs;
-            const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-            const uint32_t c0 = (uint32_t)v[u][0].x, c1 = (uint32_t)v[u][0].y;
-            const uint32_t c2 = (uint32_t)v[u][1].x, c3 = (uint32_t)v[u][1].y;
-            const uint32_t off = kmajor_off(row, k, sbo);
+          for (int u = 0; u < 4; ++u) {
+            const int cm = cm0 + u * 4;
+            if (cm < n_cm) {
+              const int rg = cm >> kcs_shift, kc = cm & (kcs - 1);
+              const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
+              const ulonglong2* src =
+                  reinterpret_cast<const ulonglong2*>(E + ((int64_t)l * ne + j0 + row) * ne + k);
+              v[u][0] = __ldg(src);
+              v[u][1] = __ldg(src + 1);
+            }
+          }
 #pragma unroll
-            for (int b = 0; b < kPlanes; ++b) {
-              const uint32_t sel = (uint32_t)b | ((uint32_t)(4 + b) << 4);
-              const uint32_t lo = __byte_perm(c0, c1, sel), hi = __byte_perm(c2, c3, sel);
-              *reinterpret_cast<uint32_t*>(A + b * plane_bytes + off) = __byte_perm(lo, hi, 0x5410);
+          for (int u = 0; u < 4; ++u) {
+            const int cm = cm0 + u * 4;
+            if (cm < n_cm) {
+              const int rg = cm >> kcs_shift, kc = cm & (kcs - 1);
+              const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
+              const uint32_t c0 = (uint32_t)v[u][0].x, c1 = (uint32_t)v[u][0].y;
+              const uint32_t c2 = (uint32_t)v[u][1].x, c3 = (uint32_t)v[u][1].y;
+              const uint32_t off = kmajor_off(row, k, sbo);
+#pragma unroll
+              for (int b = 0; b < kPlanes; ++b) {
+                const uint32_t sel = (uint32_t)b | ((uint32_t)(4 + b) << 4);
+                const uint32_t lo = __byte_perm(c0, c1, sel), hi = __byte_perm(c2, c3, sel);
+                *reinterpret_cast<uint32_t*>(A + b * plane_bytes + off) = __byte_perm(lo, hi, 0x5410);
+              }
             }
           }
         }
       }
-    }
-    mbar_wait(&id_bars[grp_global % kIdSlots], (grp_global / kIdSlots) & 1);
-    build_onehot<G>(Bst + (grp_global & 1) * b_bytes, idst + (grp_global % kIdSlots) * ids_bytes, ids_stride, ne,
-                    live(0), sbo);
-    for (int gi = 0; gi < n_groups; ++gi, ++grp_global) {
-      const uint32_t s = grp_global & 1;
-      const int64_t c0 = c_begin + (int64_t)gi * kCpg;
-      const int n_live = live(gi);
-      // A planes and B(gi) written; the previous group's accumulators and ids have been read
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      for (int gi = 0; gi < n_groups; ++gi) {
+        const uint32_t Gg = G_ + gi, s = Gg & 1;
+        // one-hot tile: ids landed, and the stage's previous MMAs (group Gg - 2) are done
+        mbar_wait(&id_full[Gg & 3], (Gg >> 2) & 1);
+        if (Gg >= 2) mbar_wait(&mma_done[s], ((Gg - 2) >> 1) & 1);
+        build_onehot<G>(Bst + s * b_bytes, idst + (Gg & 3) * ids_bytes, ids_stride, ne, live(gi), sbo, pwarp, lane);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_full[s]);
+      }
+    } else {
+      // ---------------- epilogue ----------------
+      const int jr = warp * 32 + lane;  // row of the block = TMEM lane
+      for (int gi = 0; gi < n_groups; ++gi) {
+        const uint32_t Gg = G_ + gi, s = Gg & 1;
+        const int64_t c0 = c_begin + (int64_t)gi * kCpg;
+        const int n_live = live(gi);
+        mbar_wait(&mma_done[s], (Gg >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(A), b0 = smem_u32(Bst + s * b_bytes);
-        for (int b = 0; b < kPlanes; ++b)
-          for (int kk = 0; kk < ne / 32; ++kk)
-            mma_i8(tmem + (uint32_t)(b * kN), kmajor_desc(a0 + b * plane_bytes + kk * 256, sbo),
-                   kmajor_desc(b0 + kk * 256, sbo), prm.idesc, kk > 0 ? 1u : 0u);
-        mma_commit(&bars[s]);
-        // slot of group gi+2 was last read by group gi-1 (finished before the barrier above)
-        if (gi + 2 < n_groups) fetch_ids((grp_global + 2) % kIdSlots, l, j0, c0 + 2 * kCpg, live(gi + 2));
-      }
-      // the next group's one-hot tile goes to the other stage (its MMAs completed last round)
-      if (gi + 1 < n_groups) {
-        const uint32_t nx = grp_global + 1;
-        mbar_wait(&id_bars[nx % kIdSlots], (nx / kIdSlots) & 1);
-        build_onehot<G>(Bst + (s ^ 1) * b_bytes, idst + (nx % kIdSlots) * ids_bytes, ids_stride, ne, live(gi + 1),
-                        sbo);
-      }
-      mbar_wait(&bars[s], (grp_global >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (warp < 4) {
-        const int jr = warp * 32 + lane;  // row of the block = TMEM lane
-        const uint8_t* ids = idst + (grp_global % kIdSlots) * ids_bytes + ne + jr;
+        const uint8_t* ids = idst + (Gg & 3) * ids_bytes + ne + jr;
         unsigned long long acc[kCpg];
         uint32_t pj[kCpg];
 #pragma unroll
@@ -253,27 +299,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc[ci] = 0ull;
           pj[ci] = ci < n_live ? (uint32_t)ids[ci * ids_stride] : 0u;
         }
+        const uint32_t d0 = tmem + ((uint32_t)(warp * 32) << 16) + s * (kPlanes * kN);
 #pragma unroll
         for (int b = 0; b < kPlanes; ++b) {
 #pragma unroll
           for (int ch = 0; ch < kN / 16; ch += 2) {
             uint32_t v[2][16];
-            const uint32_t base = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(b * kN + ch * 16);
-            tmem_ld16(base, v[0]);
-            tmem_ld16(base + 16, v[1]);
+            tmem_ld16(d0 + (uint32_t)(b * kN + ch * 16), v[0]);
+            tmem_ld16(d0 + (uint32_t)(b * kN + ch * 16 + 16), v[1]);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
               for (int q = 0; q < 16 / G; ++q) {
                 const int ci = (ch + h) * (16 / G) + q;
-                uint32_t x = v[h][q * G];
-#pragma unroll
-                for (int p = 1; p < G; ++p) x = pj[ci] == (uint32_t)p ? v[h][q * G + p] : x;
+                const uint32_t x = pick<G>(&v[h][q * G], pj[ci]);
                 acc[ci] += (unsigned long long)x << (8 * b);
               }
           }
         }
+        // the buffer is read: let the issuer reuse it for group Gg + 2
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_free[s]);
         // reduce-scatter over the warp: after log2(kCpg) halvings lane groups hold one candidate
         // each, then a plain butterfly finishes the 32 / kCpg lanes that share it
 #pragma unroll
@@ -286,22 +334,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, half * (32 / kCpg));
           }
         }
-        {
-          unsigned long long s64 = acc[0];
+        unsigned long long s64 = acc[0];
 #pragma unroll
-          for (int o = 32 / kCpg / 2; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
-          // lane bits above log2(32/kCpg) name the candidate this lane group now holds
-          int ci = 0;
+        for (int o = 32 / kCpg / 2; o > 0; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+        int ci = 0;  // lane bits above log2(32 / kCpg) name the candidate this lane group holds
 #pragma unroll
-          for (int half = kCpg / 2; half >= 1; half >>= 1)
-            if (lane & (half * (32 / kCpg))) ci |= half;
-          if ((lane & (32 / kCpg - 1)) == 0 && s64 != 0ull && ci < n_live) atomicAdd(&same[c0 + ci], s64);
-        }
+        for (int half = kCpg / 2; half >= 1; half >>= 1)
+          if (lane & (half * (32 / kCpg))) ci |= half;
+        if ((lane & (32 / kCpg - 1)) == 0 && s64 != 0ull && ci < n_live) atomicAdd(&same[c0 + ci], s64);
       }
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // A planes are rebuilt for the next unit
+    G_ += (uint32_t)n_groups;
   }
+  // every commit was waited by the epilogue; every TMEM read finished before its arrive
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -315,7 +361,7 @@ bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C) {
   if (!(L > 1 && C > 0 && (ne == 128 || ne == 256) && (g == 4 || g == 8 || g == 16) &&
         (reinterpret_cast<uintptr_t>(cands) & 15) == 0))  // 16-B aligned bulk copies
     return false;
-  return eval_mma_smem(ne, g) <= 227 * 1024;  // n_e = 256 with g = 4 does not fit
+  return eval_mma_smem(ne, g) <= 227 * 1024;
 }
 
 size_t eval_mma_smem(int ne, int g) {
@@ -332,15 +378,15 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
   prm.L = L;
   prm.ne = ne;
   prm.g = g;
-  prm.cpg = kN / g;
   prm.n_jb = ne / kRowsBlk;
   prm.C = C;
   prm.m = (int64_t)L * ne;
+  const int cpg = kN / g;
   const int64_t base = (int64_t)(L - 1) * prm.n_jb;
-  const int64_t groups = (C + prm.cpg - 1) / prm.cpg;
+  const int64_t groups = (C + cpg - 1) / cpg;
   // enough units for ~2 per SM, each rebuilding its A planes (n_e x 128 x 8 B of E) once
   prm.n_cr = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (2 * sms + base - 1) / base));
-  prm.range_cands = (groups + prm.n_cr - 1) / prm.n_cr * prm.cpg;
+  prm.range_cands = (groups + prm.n_cr - 1) / prm.n_cr * cpg;
   prm.n_cr = (int)((C + prm.range_cands - 1) / prm.range_cands);
   prm.n_units = base * prm.n_cr;
   // c = s32, a = b = u8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
