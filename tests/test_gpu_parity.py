@@ -508,3 +508,40 @@ def test_eval_tensor_core_path_matches_oracle(G, orc, monkeypatch, L, ne, k, g, 
     alu = G.eval_costs(s, torch.from_numpy(cands).cuda(), 2.0, 0.5)
     for a, b in zip(alu[:3], want[:3]):
         assert np.array_equal(a, b)
+
+
+def test_queued_pass_argument_errors(G):
+    """gimbal_pass_async / gimbal_window_place_async validate like the synchronous API: the
+    reference's messages for a bad anchor and an oversized strong-pair set, and alpha/beta > 0."""
+    import ctypes as C
+
+    from paper_2602_21626_b200 import _native as N
+
+    L, ne, k, g = SHAPES["dsv2lite"]
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 2000, model_seed=1, stream_seed=2, device=0)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(trace)
+    m = L * ne
+    cands = torch.from_numpy(G.shuffled_candidates(m, g, 3, 4)).cuda()
+    buf = torch.zeros(4 + 2 * m + 3 * 4 * 2, dtype=torch.int32, device="cuda")
+    p = buf.data_ptr()
+    lib = N.lib()
+    with pytest.raises(ValueError, match="anchor_gpu out of range"):
+        N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g, g, C.c_void_p(cands.data_ptr()), 4, 1.0, 1.0,
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+    with pytest.raises(ValueError, match="capacity"):
+        N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g + 1, 0, C.c_void_p(cands.data_ptr()), 4, 1.0, 1.0,
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+    with pytest.raises(ValueError, match="alpha and beta"):
+        N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g, 0, C.c_void_p(cands.data_ptr()), 4, 0.0, 1.0,
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+    big = np.arange(m // g + 1, dtype=np.int32)
+    with pytest.raises(ValueError, match="exceeds anchor capacity"):
+        N.check(lib.gimbal_window_place_async(s.handle, big.ctypes.data, big.size, 0, C.c_void_p(cands.data_ptr()), 4,
+                                              1.0, 1.0, C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+    dup = np.array([3, 3], dtype=np.int32)
+    with pytest.raises(ValueError, match="duplicate"):
+        N.check(lib.gimbal_window_place_async(s.handle, dup.ctypes.data, dup.size, 0, C.c_void_p(cands.data_ptr()), 4,
+                                              1.0, 1.0, C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+    s.sync()  # nothing deferred
