@@ -750,14 +750,12 @@ int enqueue_affinity(gimbal_stats_t h, double threshold, int32_t top_e, int32_t 
   GIMBAL_TRY(h->keys.ensure((size_t)n_pad * 8));
   if (top_e >= 1 && top_e <= kTopkMax) {
     // only the top_e heaviest pairs can survive truncation: segment top-K, no full sort
+    // two halves: segment survivors ((n / 2048) * top_e keys) or register top-K partials (<= 4096)
+    const int64_t half = std::max<int64_t>({n_pad / 2, (n + 2047) / 2048 * (int64_t)top_e, 4096});
+    GIMBAL_TRY(h->keys.ensure((size_t)half * 16));
     unsigned long long* ka = h->keys.as<unsigned long long>();
-    unsigned long long* kb = ka + n_pad / 2;
+    unsigned long long* kb = ka + half;
     unsigned long long* sorted = nullptr;
-    if ((n + 2047) / 2048 * (int64_t)top_e > n_pad / 2) {
-      GIMBAL_TRY(h->keys.ensure((size_t)((n + 2047) / 2048 * (int64_t)top_e) * 16));
-      ka = h->keys.as<unsigned long long>();
-      kb = ka + (n + 2047) / 2048 * (int64_t)top_e;
-    }
     GIMBAL_CUDA_TRY(launch_affinity_topk(L, ne, h->dE, threshold, top_e, ka, kb, h->dflags, &sorted, h->stream));
     GIMBAL_CUDA_TRY(launch_affinity_select(L, ne, sorted, top_e, top_e, capacity, bits, dout, dn, h->stream));
   } else {

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -350,6 +351,77 @@ __global__ void __launch_bounds__(1024)
   for (int i = threadIdx.x; i < K; i += blockDim.x) out[(int64_t)blockIdx.x * K + i] = s[i];
 }
 
+// Register top-K for small K (top_e <= kRegTopK, the simulator's default is 4): every thread keeps
+// its K largest composite keys sorted in registers (branch-free insertion, skipped once a key
+// cannot enter), warps merge their lanes' lists by shuffles, warp 0 merges the CTA's warps, and the
+// CTA writes its K keys sorted descending.  One pass over E with ~2 CTAs per SM, then one CTA over
+// the survivors; replaces the 2048-key bitonic segment sorts (0.34 ms -> tens of us at DS-V3).
+constexpr int kRegTopK = 8;
+constexpr int kRegThreads = 256;
+
+__device__ __forceinline__ void topk_insert(unsigned long long (&r)[kRegTopK], unsigned long long key) {
+  if (key <= r[kRegTopK - 1]) return;
+#pragma unroll
+  for (int i = kRegTopK - 1; i >= 0; --i) {
+    const unsigned long long prev = i ? r[i - 1] : ~0ull;
+    r[i] = key > prev ? prev : (key > r[i] ? key : r[i]);
+  }
+}
+
+__device__ __forceinline__ void topk_warp_merge(unsigned long long (&r)[kRegTopK]) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long other[kRegTopK];
+#pragma unroll
+    for (int i = 0; i < kRegTopK; ++i) other[i] = __shfl_xor_sync(0xffffffffu, r[i], o);
+#pragma unroll
+    for (int i = 0; i < kRegTopK; ++i) topk_insert(r, other[i]);
+  }
+}
+
+template <bool FROM_E>
+__global__ void __launch_bounds__(kRegThreads)
+    topk_reg_kernel(const unsigned long long* __restrict__ in, int64_t n, double threshold,
+                    unsigned long long* __restrict__ out, uint32_t* __restrict__ flags) {
+  __shared__ unsigned long long lists[kRegThreads / 32][kRegTopK];
+  unsigned long long r[kRegTopK];
+#pragma unroll
+  for (int i = 0; i < kRegTopK; ++i) r[i] = 0ull;
+  bool over = false;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long key;
+    if constexpr (FROM_E) {
+      const unsigned long long w = in[idx];
+      const double wd = (double)w;
+      key = 0ull;
+      if (wd >= threshold && wd > 0.0) {
+        over |= w >= (1ull << 40);
+        key = (w << 24) | (unsigned long long)(0xffffffll - idx);
+      }
+    } else {
+      key = in[idx];
+    }
+    topk_insert(r, key);
+  }
+  if (FROM_E && __syncthreads_or(over) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagOverflow);
+  topk_warp_merge(r);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < kRegTopK; ++i) lists[warp][i] = r[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < kRegTopK; ++i) r[i] = lane < kRegThreads / 32 ? lists[lane][i] : 0ull;
+    topk_warp_merge(r);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < kRegTopK; ++i) out[(int64_t)blockIdx.x * kRegTopK + i] = r[i];
+    }
+  }
+}
+
 // Sequential endpoint union over the sorted pairs (placement.cpp:221-237): the result is the
 // union of the longest prefix (<= kept pairs) whose union fits `capacity`.
 __global__ void affinity_select_kernel(int L, int ne, const unsigned long long* __restrict__ keys,
@@ -596,6 +668,21 @@ cudaError_t launch_affinity_topk(int L, int ne, const unsigned long long* E, dou
                                  unsigned long long* a, unsigned long long* b, uint32_t* flags,
                                  unsigned long long** result, cudaStream_t s) {
   const int64_t n = (int64_t)(L - 1) * ne * ne;
+  if (K <= kRegTopK && !std::getenv("GIMBAL_TOPK_SORT")) {
+    // a/b hold >= n_pad / 2 keys each (n_pad = next pow2 of n >= 2 * 296 * 8 here, else 1 block)
+    int grid = (int)std::min<int64_t>(296, (n + kRegThreads * 16 - 1) / (kRegThreads * 16));
+    grid = std::max(grid, 1);
+    topk_reg_kernel<true><<<grid, kRegThreads, 0, s>>>(E, n, threshold, a, flags);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (grid == 1) {
+      *result = a;
+      return cudaSuccess;
+    }
+    topk_reg_kernel<false><<<1, kRegThreads, 0, s>>>(a, (int64_t)grid * kRegTopK, 0.0, b, flags);
+    *result = b;
+    return cudaGetLastError();
+  }
   int64_t blocks = (n + kSortLocal - 1) / kSortLocal;
   topk_segment_kernel<true><<<(unsigned)blocks, 1024, 0, s>>>(E, n, threshold, K, a, flags);
   cudaError_t e = cudaGetLastError();
