@@ -308,7 +308,8 @@ def test_stream_infeasible_candidate_reported_at_sync(G):
 
 
 @pytest.mark.parametrize("threshold,top_e,cap", [(0.0, 4, None), (0.0, -1, None), (50.0, 16, 7), (1e12, 4, None),
-                                                 (0.0, 0, None), (0.0, 64, 3), (3.0, 1000, None)])
+                                                 (0.0, 0, None), (0.0, 64, 3), (3.0, 1000, None), (0.0, 1, None),
+                                                 (0.0, 8, None), (50.0, 8, 7), (0.0, 9, None)])
 def test_affinity_set_variants(G, orc, threshold, top_e, cap):
     L, ne, k, g = SHAPES["dsv2lite"]
     topo = G.MoeTopology(L, ne, k, g)
