@@ -248,12 +248,107 @@ class HotPath:
         return self._twin_hp
 
     def stream_distributed(self, window_shards, candidates_shard, cand_offset: int, n_candidates: int,
-                           M: AffinitySet, group=None, previous=None):
+                           M: AffinitySet, group=None, previous=None, reserve_sms: int = 2):
         """stream() with each window's tokens sharded over ranks: count the shard, all-reduce E,
-        re-place with the fixed M, score this rank's candidate slice, merge the argmin."""
+        re-place with the fixed M, score this rank's candidate slice, merge the argmin.
+
+        Over NCCL the whole stream is queued like stream(): window w+1's shard is counted on the
+        twin handle while window w's E is all-reduced on its handle's stream (the collective is
+        ordered behind the counting and ahead of the placement without a host round trip) and
+        placed with gimbal_window_place_async.  Objectives land in one [windows][C] buffer that a
+        single MIN all-reduce merges at the end (lowest global index wins ties).  Global candidate
+        0 is the greedy placement (rank 0's first row); other ranks score their slice behind a
+        scratch greedy row."""
+        import torch
+        import torch.distributed as dist
+
+        windows = list(window_shards)
+        if not windows:
+            return []
+        if dist.get_backend(group) != "nccl":
+            return self._stream_distributed_sync(windows, candidates_shard, cand_offset, n_candidates, M, group,
+                                                 previous)
+        n, m = len(windows), self.topo.total_experts()
+        dev = torch.device("cuda", self.device)
+        c_loc = int(candidates_shard.shape[0])
+        lead = 0 if cand_offset == 0 else 1  # scratch greedy row ahead of a non-leading slice
+        tok = torch.tensor([int(w.shape[0]) for w in windows], dtype=torch.int64, device=dev)
+        dist.all_reduce(tok, op=dist.ReduceOp.SUM, group=group)
+        glob = tok.tolist()
+        pair = (self, self._twin())
+        rows = c_loc + lead
+        scores = torch.empty((n, 3, max(rows, 1)), dtype=torch.float64, device=dev)
+        argmins = torch.empty((n,), dtype=torch.int64, device=dev)
+        places = torch.empty((n, m), dtype=torch.int32, device=dev)
+        objs = torch.full((n, n_candidates), float("inf"), dtype=torch.float64, device=dev)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        exts = []
+        for hp in pair:
+            if getattr(hp, "_wcands", None) is None or tuple(hp._wcands.shape) != (rows, m):
+                hp._wcands = torch.empty((rows, m), dtype=torch.uint8, device=dev)
+            if c_loc:
+                hp._wcands[lead:].copy_(candidates_shard)
+            if lead:
+                hp._wcands[0].copy_(hp._wcands[1] if c_loc else torch.zeros(m, dtype=torch.uint8, device=dev))
+            hp.stats._after_torch(objs)
+            hp.stats.set_count_sms(max(1, sms - max(0, reserve_sms)))
+            exts.append(torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=dev))
+        Mi = np.ascontiguousarray(np.asarray(M.experts, np.int32))
+        lib = N.lib()
+        topo = self.topo
+        n_cells = (topo.n_layers - 1) * topo.n_experts * topo.n_experts if topo.n_layers > 1 else m
+        try:
+            pair[0].stats.reset()
+            pair[0].stats.add_tokens(windows[0])
+            for i in range(n):
+                cur, ext = pair[i % 2], exts[i % 2]
+                if i + 1 < n:
+                    nxt = pair[(i + 1) % 2]
+                    nxt.stats.reset()
+                    nxt.stats.add_tokens(windows[i + 1])
+                e_ptr, a_ptr, _ = cur.stats.device_buffers()
+                view = torch.as_tensor(_CudaArray(e_ptr if topo.n_layers > 1 else a_ptr, n_cells), device=dev)
+                with torch.cuda.stream(ext):  # behind this window's counting, ahead of its placement
+                    dist.all_reduce(view, op=dist.ReduceOp.SUM, group=group)
+                cur.stats.mark_reduced(int(glob[i]))
+                if rows:
+                    N.check(lib.gimbal_window_place_async(
+                        cur.stats.handle, Mi.ctypes.data if Mi.size else None, Mi.size, M.anchor_gpu,
+                        C.c_void_p(cur._wcands.data_ptr()), rows, self.alpha, self.beta,
+                        C.c_void_p(scores[i].data_ptr()), C.c_void_p(argmins[i].data_ptr()),
+                        C.c_void_p(places[i].data_ptr())), "window_place")
+                    if c_loc:
+                        with torch.cuda.stream(ext):
+                            objs[i, cand_offset:cand_offset + c_loc].copy_(scores[i, 2, lead:lead + c_loc])
+        finally:
+            for hp in pair:
+                hp.stats.set_count_sms(sms)
+        errors = []
+        for hp in pair:
+            try:
+                hp.stats.sync()
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+        if errors:
+            raise errors[0]
+        dist.all_reduce(objs, op=dist.ReduceOp.MIN, group=group)
+        allobj = objs.cpu().numpy()
+        pl = places.cpu().numpy()
+        prev = None if previous is None else np.asarray(previous, np.int32)
+        out = []
+        for i in range(n):
+            gp = pl[i]
+            moved = int(np.count_nonzero(prev != gp)) if prev is not None and prev.shape == gp.shape else len(gp)
+            out.append((merge_argmin(allobj[i]), moved, gp))
+            prev = gp
+        return out
+
+    def _stream_distributed_sync(self, windows, candidates_shard, cand_offset: int, n_candidates: int,
+                                 M: AffinitySet, group=None, previous=None):
+        """Per-window synchronous form (any backend): count, all-reduce, place, merge."""
         out = []
         prev = previous
-        for w in window_shards:
+        for w in windows:
             res = self._distributed_pass(w, candidates_shard, cand_offset, n_candidates, group, M)
             moved = (sum(1 for a, b in zip(prev, res.greedy) if a != b) if prev is not None
                      and len(prev) == len(res.greedy) else len(res.greedy))

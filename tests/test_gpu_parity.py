@@ -546,3 +546,35 @@ def test_queued_pass_argument_errors(G):
         N.check(lib.gimbal_window_place_async(s.handle, dup.ctypes.data, dup.size, 0, C.c_void_p(cands.data_ptr()), 4,
                                               1.0, 1.0, C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
     s.sync()  # nothing deferred
+
+
+def test_stream_distributed_single_rank_matches_stream(G):
+    """The queued multi-GPU streaming loop (NCCL all-reduce of E on the handle stream per window,
+    candidate slices, one MIN all-reduce of the objectives) run as a one-rank NCCL group gives the
+    single-GPU loop's per-window argmin, moved count and greedy placement."""
+    import socket
+
+    import torch.distributed as dist
+
+    L, ne, k, g = SHAPES["dsv3"]
+    topo = G.MoeTopology(L, ne, k, g)
+    wins = [G.generate_trace(topo, 5003, model_seed=1, stream_seed=2, first_token=w * 5003, drift=0.05,
+                             drift_epoch=w + 1, device=0) for w in range(4)]
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 77, 24)).cuda()
+    hp = G.HotPath(topo, 0)
+    M = hp.calibrate(wins[0])
+    want = hp.stream(wins, cands.clone(), M)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        hp2 = G.HotPath(topo, 0)
+        got = hp2.stream_distributed(wins, cands.clone(), 0, cands.shape[0], M)
+    finally:
+        dist.destroy_process_group()
+    assert len(got) == len(want)
+    for (am1, mv1, gp1), (am2, mv2, gp2) in zip(want, got):
+        assert am1 == am2 and mv1 == mv2 and np.array_equal(np.asarray(gp1), np.asarray(gp2))
