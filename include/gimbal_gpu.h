@@ -132,7 +132,8 @@ int gimbal_greedy_place(gimbal_stats_t h, const int32_t* M, int32_t n_M, int32_t
 
 /* One tumbling window of streaming re-placement (MoeSubsystem::on_forward_step, sim.cpp:149-165,
  * with the strong-pair set fixed after calibration, sim.cpp:94-104), queued on the handle's stream
- * with NO host synchronisation: greedy_place (placement.cpp:240-299) with M anchored on
+ * with no host synchronisation (one exception: when tokens * top_k^2 >= 2^27 the evaluator first reads
+ * the largest E cell back to pick 32- or 64-bit partial sums): greedy_place (placement.cpp:240-299) with M anchored on
  * anchor_gpu -> `placement` (m int32, device) and row 0 of `candidates` (uint8 [C][m], device),
  * then eval_cost of all C candidates (placement.cpp:58-85) -> `scores` (device f64 [3][C]: D, cut,
  * objective) and `argmin` (device int64, lowest index on ties).  M is validated (reference
@@ -143,8 +144,8 @@ int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t n_M, i
                               uint8_t* candidates_device, int64_t n_candidates, double alpha, double beta,
                               double* scores_device, int64_t* argmin_device, int32_t* placement_device);
 
-/* The whole placement half of the north-star pass queued on the handle's stream with NO host
- * synchronisation: build_affinity_set (placement.cpp:186-238; members -> `members` [m] and
+/* The whole placement half of the north-star pass queued on the handle's stream with no host
+ * synchronisation (same max-cell exception as gimbal_window_place_async): build_affinity_set (placement.cpp:186-238; members -> `members` [m] and
  * `n_members` [1], device int32) -> greedy_place with that set on anchor_gpu (placement.cpp:240-299;
  * -> `placement` [m] int32 and row 0 of `candidates`) -> eval_cost of all C candidates ->
  * `scores` [3][C] f64 and `argmin` [1] int64 (device).  capacity must be <= m/g (the reference's
