@@ -578,3 +578,20 @@ def test_stream_distributed_single_rank_matches_stream(G):
     assert len(got) == len(want)
     for (am1, mv1, gp1), (am2, mv2, gp2) in zip(want, got):
         assert am1 == am2 and mv1 == mv2 and np.array_equal(np.asarray(gp1), np.asarray(gp2))
+
+
+def test_stream_from_pinned_host_windows(G):
+    """The end-to-end streaming path (windows in pinned host memory, copied on the handles' copy
+    streams while counted) gives the device-resident loop's results."""
+    L, ne, k, g = SHAPES["qwen3"]
+    topo = G.MoeTopology(L, ne, k, g)
+    wins = [G.generate_trace(topo, 3001, model_seed=3, stream_seed=4, first_token=w * 3001, drift=0.1,
+                             drift_epoch=w + 1, device=0) for w in range(3)]
+    host = [w.cpu().pin_memory() for w in wins]
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 9, 20)).cuda()
+    hp = G.HotPath(topo, 0)
+    M = hp.calibrate(wins[0])
+    want = hp.stream(wins, cands.clone(), M)
+    got = G.HotPath(topo, 0).stream(host, cands.clone(), M)
+    for (am1, mv1, gp1), (am2, mv2, gp2) in zip(want, got):
+        assert am1 == am2 and mv1 == mv2 and np.array_equal(gp1, gp2)
