@@ -143,10 +143,14 @@ class RoutingStats:
         torch), without a host synchronisation."""
         import torch
 
-        s = C.c_void_p()
-        N.check(N.lib().gimbal_stats_device_buffers(self._h, None, None, C.byref(s)), "buffers")
-        ours = torch.cuda.ExternalStream(s.value, device=tensor.device)
-        ours.wait_stream(torch.cuda.current_stream(tensor.device))
+        ours = getattr(self, "_ext_stream", None)
+        if ours is None or ours.device != tensor.device:
+            s = C.c_void_p()
+            N.check(N.lib().gimbal_stats_device_buffers(self._h, None, None, C.byref(s)), "buffers")
+            ours = self._ext_stream = torch.cuda.ExternalStream(s.value, device=tensor.device)
+        cur = torch.cuda.current_stream(tensor.device)
+        if cur.cuda_stream != ours.cuda_stream:
+            ours.wait_stream(cur)
 
     def _flush(self) -> None:
         if self._pending:
