@@ -155,7 +155,10 @@ struct gimbal_stats_s {
     return GIMBAL_OK;
   }
   // scratch
-  DevBuf cand, same, dout, keys, misc, ints;
+  DevBuf cand, same, dout, keys, misc, ints, probe;
+  // side stream of gimbal_pass_async: the greedy walk runs there beside the candidate scoring
+  cudaStream_t g_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::mutex mu;
   // strong-pair set resident in `ints` for the asynchronous window path (streaming windows keep
   // M fixed, sim.cpp:94-104, so it is uploaded once): valid while ints.p == m_cached_buf
@@ -402,6 +405,9 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->t_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->g_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_order, cudaEventDisableTiming) != cudaSuccess) {
     set_error("gimbal_stats_create: stream creation failed");
     return fail(GIMBAL_CUDA_ERROR);
@@ -451,7 +457,10 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_copied[b]) cudaEventDestroy(h->ev_copied[b]);
       if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
     }
-    for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints}) b->release();
+    if (h->g_stream) cudaStreamSynchronize(h->g_stream);
+    for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints, &h->probe}) b->release();
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->t_stream) cudaStreamSynchronize(h->t_stream);
     for (int b = 0; b < gimbal_stats_s::kStages; ++b) {
       if (h->lm8[b]) cudaFree(h->lm8[b]);
@@ -466,6 +475,7 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->t_stream) cudaStreamDestroy(h->t_stream);
+    if (h->g_stream) cudaStreamDestroy(h->g_stream);
   }
   delete h;
   return GIMBAL_OK;
@@ -645,6 +655,8 @@ int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
 
 namespace {
 
+int pick_cell_width(gimbal_stats_t h);
+
 // Queues the batch evaluator (eval_same + eval_dev + eval_finish) for C device candidates on the
 // handle's stream.  The only host synchronisation is the one-off max-cell probe when the token
 // count alone cannot bound every E cell below 2^27.
@@ -652,6 +664,22 @@ int enqueue_eval(gimbal_stats_t h, const uint8_t* dc, int64_t C, double alpha, d
                  double* dcut, double* dobj, long long* darg, uint32_t* flags) {
   const int L = h->topo.n_layers, ne = h->topo.n_experts, gg = h->topo.n_gpus, k = h->topo.top_k;
   GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
+  GIMBAL_TRY(pick_cell_width(h));
+  GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
+                                    h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
+                                    flags, h->small_cells, h->stream));
+  const unsigned long long total =
+      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
+  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
+                                     dobj, darg, flags, h->stream));
+  return GIMBAL_OK;
+}
+
+// E cells < 2^27 lets the evaluators keep 32-bit partial sums / four byte planes: decided from the
+// token count alone when tokens * k^2 < 2^27, else by reading the largest cell back once per count
+// state (a host synchronisation).
+int pick_cell_width(gimbal_stats_t h) {
+  const int k = h->topo.top_k;
   if (h->max_tokens != h->tokens &&
       (unsigned long long)h->tokens * (unsigned long long)(k * k) < (1ull << 27)) {
     // every cell is at most tokens * k^2 (a token pairs each of its k slots with each of the next
@@ -662,20 +690,13 @@ int enqueue_eval(gimbal_stats_t h, const uint8_t* dc, int64_t C, double alpha, d
   if (h->max_tokens != h->tokens) {
     // cells < 2^27 lets the evaluator keep 32-bit partial sums (one host sync per new count state)
     unsigned long long mx = 0;
-    GIMBAL_TRY(h->misc.ensure(64));
-    GIMBAL_CUDA_TRY(launch_max_cell(h->dE, h->nE(), h->misc.as<unsigned long long>(), h->stream));
-    GIMBAL_CUDA_TRY(cudaMemcpyAsync(&mx, h->misc.p, 8, cudaMemcpyDeviceToHost, h->stream));
+    GIMBAL_TRY(h->probe.ensure(64));  // not `misc`: it may hold a queued pass's member bits
+    GIMBAL_CUDA_TRY(launch_max_cell(h->dE, h->nE(), h->probe.as<unsigned long long>(), h->stream));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(&mx, h->probe.p, 8, cudaMemcpyDeviceToHost, h->stream));
     GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
     h->small_cells = mx < (1ull << 27);
     h->max_tokens = h->tokens;
   }
-  GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
-                                    h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
-                                    flags, h->small_cells, h->stream));
-  const unsigned long long total =
-      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
-  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
-                                     dobj, darg, flags, h->stream));
   return GIMBAL_OK;
 }
 
@@ -958,13 +979,43 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   }
   const int L = h->topo.n_layers, ne = h->topo.n_experts, g = h->topo.n_gpus;
   const int64_t n_pad = next_pow2(m);
-  GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, bits, h->keys.as<unsigned long long>(), n_pad, h->dflags,
-                                     h->stream));
-  GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, h->stream));
-  GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, members, -1, anchor, h->keys.as<unsigned long long>(), m,
-                                     placement, candidates, gs.tent, h->stream, n_members));
-  return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
-                      reinterpret_cast<long long*>(argmin), h->dflags + 1);
+  auto greedy_on = [&](cudaStream_t st) -> int {
+    GIMBAL_CUDA_TRY(launch_greedy_keys(m, h->dA, bits, h->keys.as<unsigned long long>(), n_pad, h->dflags, st));
+    GIMBAL_CUDA_TRY(sort_u64_desc(h->keys.as<unsigned long long>(), n_pad, st));
+    GIMBAL_CUDA_TRY(launch_greedy_walk(L, ne, g, h->dA, members, -1, anchor, h->keys.as<unsigned long long>(), m,
+                                       placement, candidates, gs.tent, st, n_members));
+    return GIMBAL_OK;
+  };
+  // evaluator flags go to the deferred word (dflags[1]) as in gimbal_window_place_async
+  // (tiny shapes: the walk is ~10 us and the extra launches cost more than it hides; measured
+  // Mixtral m = 256: 0.286 vs 0.269 ms per step, DS-V2-Lite m = 1664: 5.15 vs 5.25 ms)
+  if (C < 2 || m < 1024 || std::getenv("GIMBAL_NO_GREEDY_OVERLAP")) {
+    GIMBAL_TRY(greedy_on(h->stream));
+    return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
+                        reinterpret_cast<long long*>(argmin), h->dflags + 1);
+  }
+  // The greedy walk (latency-bound, one CTA) runs on the side stream while candidates 1..C-1 are
+  // scored on the handle's stream; candidate 0 (the greedy row it writes) is scored after the join.
+  GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
+  GIMBAL_TRY(pick_cell_width(h));
+  GIMBAL_CUDA_TRY(cudaEventRecord(h->ev_fork, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamWaitEvent(h->g_stream, h->ev_fork, 0));
+  GIMBAL_TRY(greedy_on(h->g_stream));
+  GIMBAL_CUDA_TRY(cudaEventRecord(h->ev_join, h->g_stream));
+  unsigned long long* same = h->same.as<unsigned long long>();
+  long long* bad = reinterpret_cast<long long*>(same + C);
+  uint32_t* flags = h->dflags + 1;
+  GIMBAL_CUDA_TRY(launch_eval_prepare(C, same, h->stream));
+  GIMBAL_CUDA_TRY(launch_eval_range(L, ne, g, h->dA, h->dE, candidates + m, C - 1, 1, same + 1, scores + 1, flags,
+                                    bad, h->small_cells, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
+  GIMBAL_CUDA_TRY(launch_eval_range(L, ne, g, h->dA, h->dE, candidates, 1, 0, same, scores, flags, bad,
+                                    h->small_cells, h->stream));
+  const unsigned long long total =
+      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)h->topo.top_k * h->topo.top_k;
+  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, same, scores, scores + C, scores + 2 * C,
+                                     reinterpret_cast<long long*>(argmin), flags, h->stream));
+  return GIMBAL_OK;
 }
 
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms) {

@@ -392,7 +392,9 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
   // c = s32, a = b = u8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   prm.idesc = (2u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kRowsBlk >> 4) << 24);
   const size_t smem = eval_mma_smem(ne, g);
-  const int grid = (int)std::min<int64_t>(prm.n_units, sms);
+  // one SM stays free: the greedy walk (one CTA, up to 200 KB of shared memory) of the same pass
+  // runs beside the scoring of the other candidates (capi.cu gimbal_pass_async)
+  const int grid = (int)std::min<int64_t>(prm.n_units, std::max(1, sms - 1));
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -155,6 +155,10 @@ cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned lon
 bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C);
 cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, const uint8_t* cands, int64_t C,
                             unsigned long long* same, cudaStream_t s);
+cudaError_t launch_eval_prepare(int64_t C, unsigned long long* scratch_same, cudaStream_t s);
+cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A, const unsigned long long* E,
+                              const uint8_t* cands, int64_t C, int64_t base, unsigned long long* same, double* D,
+                              uint32_t* flags, long long* bad_index, bool small_cells, cudaStream_t s);
 cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
                                const unsigned long long* same, const double* D, double* cut,
                                double* obj, long long* argmin, uint32_t* flags, cudaStream_t s);

@@ -186,7 +186,7 @@ __global__ void max_cell_kernel(const unsigned long long* __restrict__ E, int64_
 __global__ void __launch_bounds__(256)
     eval_dev_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
                     const uint8_t* __restrict__ cands, int64_t m, double* __restrict__ D,
-                    uint32_t* __restrict__ flags, long long* __restrict__ bad_index) {
+                    uint32_t* __restrict__ flags, long long* __restrict__ bad_index, int64_t base) {
   extern __shared__ unsigned long long sh[];  // [warps][g] loads, then [g] counts (u32)
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256)
       if (counts[p] != cap) infeasible = 1;
     if (infeasible) {
       atomicOr(flags, (uint32_t)kFlagInfeasible);
-      atomicMin(bad_index, (long long)c);
+      atomicMin(bad_index, (long long)(base + c));
     }
   }
 }
@@ -580,24 +580,25 @@ static unsigned candidate_splits(int64_t cell_ctas, int64_t C) {
   return (unsigned)std::max<int64_t>(1, std::min(want, most));
 }
 
-cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
-                              const unsigned long long* E, const uint8_t* cands, int64_t C,
-                              double alpha, double beta, unsigned long long* scratch_same,
-                              double* D, double* cut, double* obj, long long* argmin,
-                              uint32_t* flags, bool small_cells, cudaStream_t s) {
-  if (C <= 0) return cudaSuccess;
-  const int64_t m = (int64_t)L * ne;
+// same[0..C) = 0 and the lowest infeasible index = "none" (a huge value) before any range runs
+cudaError_t launch_eval_prepare(int64_t C, unsigned long long* scratch_same, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(scratch_same, 0, (size_t)C * sizeof(unsigned long long), s);
   if (e != cudaSuccess) return e;
-  long long* bad_index = reinterpret_cast<long long*>(scratch_same + C);
-  // bad_index starts at LLONG_MAX
-  const long long init = 0x7fffffffffffffffll;
-  e = cudaMemcpyAsync(bad_index, &init, sizeof(init), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
+  return cudaMemsetAsync(scratch_same + C, 0x7f, sizeof(long long), s);  // 0x7f7f...7f
+}
+
+// Same-GPU weights and deviations of candidates [base, base + C) (pointers already offset to the
+// range); bad_index / flags are shared by all ranges of one batch.
+cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A, const unsigned long long* E,
+                              const uint8_t* cands, int64_t C, int64_t base, unsigned long long* same, double* D,
+                              uint32_t* flags, long long* bad_index, bool small_cells, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  const int64_t m = (int64_t)L * ne;
+  cudaError_t e = cudaSuccess;
   const bool fast = small_cells && ne % 32 == 0 && 256 % ne == 0;
   if (small_cells && eval_mma_supported(L, ne, g, cands, C)) {
     // tensor cores: E byte planes x one-hot assignment (eval_mma.cu)
-    e = launch_eval_mma(L, ne, g, E, cands, C, scratch_same, s);
+    e = launch_eval_mma(L, ne, g, E, cands, C, same, s);
     if (e != cudaSuccess) return e;
   } else if (L > 1 && fast) {
     const int64_t rows = (int64_t)(L - 1) * ne;
@@ -608,7 +609,7 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     e = cudaFuncSetAttribute(eval_same_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     eval_same_fast_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
-        L, ne, E, cands, C, m, scratch_same);
+        L, ne, E, cands, C, m, same);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   } else if (L > 1) {
@@ -621,7 +622,7 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     e = cudaFuncSetAttribute(eval_same_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     eval_same_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
-        L, ne, E, cands, C, m, scratch_same);
+        L, ne, E, cands, C, m, same);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -630,11 +631,23 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
     const size_t smem = (size_t)(threads / 32) * g * 8 + (size_t)g * 4 + 8;
     e = cudaFuncSetAttribute(eval_dev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    eval_dev_kernel<<<(unsigned)C, threads, smem, s>>>(L, ne, g, A, cands, m, D, flags, bad_index);
+    eval_dev_kernel<<<(unsigned)C, threads, smem, s>>>(L, ne, g, A, cands, m, D, flags, bad_index, base);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
+                              const unsigned long long* E, const uint8_t* cands, int64_t C,
+                              double alpha, double beta, unsigned long long* scratch_same,
+                              double* D, double* cut, double* obj, long long* argmin,
+                              uint32_t* flags, bool small_cells, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  cudaError_t e = launch_eval_prepare(C, scratch_same, s);
+  if (e != cudaSuccess) return e;
+  return launch_eval_range(L, ne, g, A, E, cands, C, 0, scratch_same, D, flags,
+                           reinterpret_cast<long long*>(scratch_same + C), small_cells, s);
 }
 
 cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s) {
