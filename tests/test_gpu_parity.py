@@ -595,3 +595,20 @@ def test_stream_from_pinned_host_windows(G):
     got = G.HotPath(topo, 0).stream(host, cands.clone(), M)
     for (am1, mv1, gp1), (am2, mv2, gp2) in zip(want, got):
         assert am1 == am2 and mv1 == mv2 and np.array_equal(gp1, gp2)
+
+
+@pytest.mark.parametrize("shape", ["dsv2lite", "mixtral"])
+def test_queued_pass_reports_infeasible_candidate(G, shape):
+    """HotPath.run (gimbal_pass_async, greedy walk overlapped with the scoring of candidates 1..C-1
+    where m >= 1024) raises like check_feasible for an infeasible candidate, then runs clean."""
+    L, ne, k, g = SHAPES[shape]
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 4000, model_seed=1, stream_seed=3, device=0)
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 8, 12)).cuda()
+    cands[7, 5] = (int(cands[7, 5]) + 1) % g
+    hp = G.HotPath(topo, 0)
+    with pytest.raises(ValueError, match="infeasible"):
+        hp.run(trace, cands)
+    cands[7, 5] = (int(cands[7, 5]) - 1) % g
+    res = hp.run(trace, cands)
+    assert 0 <= res.argmin < 12
