@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads)
                        int32_t* __restrict__ out, uint8_t* __restrict__ out_u8, uint8_t* __restrict__ tent) {
   extern __shared__ unsigned long long load[];  // [L][g] loads, then counts [g]
   int* counts = reinterpret_cast<int*>(load + (int64_t)L * g);
-  __shared__ long long s_nvalid, s_npos, s_star;
+  __shared__ long long s_nvalid, s_npos;
   const int64_t m = (int64_t)L * ne;
   const int cap = (int)(m / g);
   const unsigned long long inv_ne = ((1ull << 40) + (unsigned long long)ne - 1) / (unsigned long long)ne;
