@@ -111,20 +111,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 }
 
 // One-hot B tile of one group from its staged GPU ids (ids[ci][0..n_e) = P_c(l+1, .)): row
-// n = ci * G + p, column k, byte = [P_c(l+1, k) == p].  Each lane writes one 4-byte word of a core
+// n = ci * G + p, column k, byte = [P_c(l+1, k) == p].  Stacked mode (n_e = 64, ST): rows
+// [0, 32) hold pair l's one-hot of layer l+1, rows [32, 64) pair l+1's of layer l+2.  Each lane writes one 4-byte word of a core
 // matrix (lane = row-in-core * 4 + word), so a warp's stores cover 128 contiguous bytes.
-template <int G>
+template <int G, bool ST>
 __device__ __forceinline__ void build_onehot(uint8_t* B, const uint8_t* ids, int ids_stride, int ne, int n_live,
-                                             uint32_t sbo, int pwarp, int lane) {
+                                             uint32_t sbo, int pwarp, int lane, int halves_live) {
   // warp w covers 8-row groups ng = w, w + 4, ...; a lane's row n and candidate/GPU (ci, p) are
   // fixed per row group, so the k loop is shifts and adds only
 #pragma unroll
   for (int ng = pwarp; ng < kN / 8; ng += 4) {
     const int n = ng * 8 + (lane >> 2);
-    const int ci = n / G, p = n % G;
+    // stacked (n_e = 64): columns [0, 32) one-hot layer l+1 (pair l), [32, 64) layer l+2 (pair l+1)
+    const int h = ST ? n >> 5 : 0, nn = ST ? n & 31 : n;
+    const int ci = nn / G, p = nn % G;
     const uint32_t pat = (uint32_t)p * 0x01010101u;
-    const bool on = ci < n_live;
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(ids + ci * ids_stride) + (lane & 3);
+    const bool on = ci < n_live && h < halves_live;
+    const uint32_t* src =
+        reinterpret_cast<const uint32_t*>(ids + ci * ids_stride + (ST ? (1 + h) * ne : 0)) + (lane & 3);
     uint8_t* dst = B + (uint32_t)ng * sbo + (uint32_t)(lane >> 2) * 16u + (uint32_t)(lane & 3) * 4u;
     for (int kc = 0; kc < (ne >> 4); ++kc) {
       const uint32_t w = on ? (__vcmpeq4(src[kc * 4], pat) & 0x01010101u) : 0u;
@@ -133,20 +137,24 @@ __device__ __forceinline__ void build_onehot(uint8_t* B, const uint8_t* ids, int
   }
 }
 
-template <int G>
+template <int G, bool ST>
 __global__ void __launch_bounds__(kThreads, 1)
     eval_mma_kernel(EvalMmaParams prm, const unsigned long long* __restrict__ E, const uint8_t* __restrict__ cands,
                     unsigned long long* __restrict__ same) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mma_done[kBStages], tmem_free[kBStages], b_full[kBStages], id_full[kIdSlots];
   __shared__ uint32_t tmem_slot;
-  constexpr int kCpg = kN / G;  // candidates per group
+  // stacked (n_e = 64, ST): A rows [0, 64) = E_l, [64, 128) = E_l+1, each half of the N = 64
+  // columns serves one pair, so a group holds 32 / G candidates
+  constexpr int kCols = ST ? kN / 2 : kN;  // accumulator columns one row reads
+  constexpr int kCpg = kCols / G;          // candidates per group
   const int ne = prm.ne;
   const int64_t m = prm.m;
   const uint32_t sbo = (uint32_t)(ne >> 4) * 128u;
   const int plane_bytes = kRowsBlk * ne;
   const int b_bytes = kN * ne;
-  const int ids_stride = ne + kRowsBlk;  // per candidate: P_c(l+1, 0..n_e) then P_c(l, j0..j0+128)
+  // per candidate: P_c(l+1, 0..n_e) then P_c(l, j0..j0+128); stacked: P_c(l), P_c(l+1), P_c(l+2)
+  const int ids_stride = ST ? 3 * ne : ne + kRowsBlk;
   const int ids_bytes = kCpg * ids_stride;
   uint8_t* A = smem;
   uint8_t* Bst = smem + kPlanes * plane_bytes;
@@ -177,6 +185,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto fetch_ids = [&](uint32_t slot, int l, int j0, int64_t c0, int n_live) {
     uint8_t* dst = idst + slot * ids_bytes;
     const uint32_t bar = smem_u32(&id_full[slot]);
+    if (ST) {  // one copy per candidate: layers l .. min(l + 2, L - 1)
+      const int bytes = min(3, prm.L - l) * ne;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)(n_live * bytes))
+                     : "memory");
+      __syncwarp();
+      for (int ci = lane; ci < n_live; ci += 32)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst + ci * ids_stride)),
+                     "l"(cands + (c0 + ci) * m + (int64_t)l * ne), "r"(bytes), "r"(bar)
+                     : "memory");
+      return;
+    }
     if (lane == 0)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                    "r"((uint32_t)(n_live * (ne + kRowsBlk)))
@@ -201,8 +222,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int cr = (int)(unit % prm.n_cr);
     const int64_t rest = unit / prm.n_cr;
     const int jb = (int)(rest % prm.n_jb);
-    const int l = (int)(rest / prm.n_jb);
+    const int l = ST ? 2 * (int)rest : (int)(rest / prm.n_jb);  // stacked: pairs l and l + 1
     const int j0 = jb * kRowsBlk;
+    const int halves_live = ST ? min(2, prm.L - 1 - l) : 1;
     const int64_t c_begin = (int64_t)cr * prm.range_cands;
     const int64_t c_end = min(prm.C, c_begin + prm.range_cands);
     if (c_begin >= c_end) continue;
@@ -237,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the previous unit's MMAs read the A planes: wait for the last of them
       if (G_ >= 1) mbar_wait(&mma_done[(G_ - 1) & 1], ((G_ - 1) >> 1) & 1);
       {
-        const int kcs = ne >> 4, kcs_shift = ne == 256 ? 4 : 3;
+        const int kcs = ne >> 4, kcs_shift = ne == 256 ? 4 : ne == 128 ? 3 : 2;
         const int n_cm = (kRowsBlk / 8) * kcs;
         for (int cm0 = pwarp; cm0 < n_cm; cm0 += 4 * 4) {
           ulonglong2 v[4][2];
@@ -247,10 +269,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (cm < n_cm) {
               const int rg = cm >> kcs_shift, kc = cm & (kcs - 1);
               const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-              const ulonglong2* src =
-                  reinterpret_cast<const ulonglong2*>(E + ((int64_t)l * ne + j0 + row) * ne + k);
-              v[u][0] = __ldg(src);
-              v[u][1] = __ldg(src + 1);
+              // E is [(L-1)][n_e][n_e]: rows l * n_e + 64 .. of the stacked block are E_l+1's
+              const int64_t grow = (int64_t)l * ne + j0 + row;
+              if (grow < (int64_t)(prm.L - 1) * ne) {
+                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(E + grow * ne + k);
+                v[u][0] = __ldg(src);
+                v[u][1] = __ldg(src + 1);
+              } else {
+                v[u][0] = make_ulonglong2(0ull, 0ull);
+                v[u][1] = make_ulonglong2(0ull, 0ull);
+              }
             }
           }
 #pragma unroll
@@ -277,7 +305,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // one-hot tile: ids landed, and the stage's previous MMAs (group Gg - 2) are done
         mbar_wait(&id_full[Gg & 3], (Gg >> 2) & 1);
         if (Gg >= 2) mbar_wait(&mma_done[s], ((Gg - 2) >> 1) & 1);
-        build_onehot<G>(Bst + s * b_bytes, idst + (Gg & 3) * ids_bytes, ids_stride, ne, live(gi), sbo, pwarp, lane);
+        build_onehot<G, ST>(Bst + s * b_bytes, idst + (Gg & 3) * ids_bytes, ids_stride, ne, live(gi), sbo, pwarp,
+                            lane, halves_live);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&b_full[s]);
@@ -291,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n_live = live(gi);
         mbar_wait(&mma_done[s], (Gg >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* ids = idst + (Gg & 3) * ids_bytes + ne + jr;
+        // row jr's assignment P_c(l, j0 + jr); stacked: P_c(l + jr / 64, jr % 64)
+        const uint8_t* ids = idst + (Gg & 3) * ids_bytes + (ST ? (jr >> 6) * ne + (jr & 63) : ne + jr);
         unsigned long long acc[kCpg];
         uint32_t pj[kCpg];
 #pragma unroll
@@ -299,11 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc[ci] = 0ull;
           pj[ci] = ci < n_live ? (uint32_t)ids[ci * ids_stride] : 0u;
         }
-        const uint32_t d0 = tmem + ((uint32_t)(warp * 32) << 16) + s * (kPlanes * kN);
+        // stacked: rows [64, 128) (warps 2-3) read the upper half of the columns
+        const uint32_t d0 = tmem + ((uint32_t)(warp * 32) << 16) + s * (kPlanes * kN) + (ST && warp >= 2 ? kCols : 0);
 #pragma unroll
         for (int b = 0; b < kPlanes; ++b) {
 #pragma unroll
-          for (int ch = 0; ch < kN / 16; ch += 2) {
+          for (int ch = 0; ch < kCols / 16; ch += 2) {
             uint32_t v[2][16];
             tmem_ld16(d0 + (uint32_t)(b * kN + ch * 16), v[0]);
             tmem_ld16(d0 + (uint32_t)(b * kN + ch * 16 + 16), v[1]);
@@ -358,13 +389,15 @@ size_t eval_mma_smem(int ne, int g);
 
 bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C) {
   if (std::getenv("GIMBAL_EVAL_ALU")) return false;
-  if (!(L > 1 && C > 0 && (ne == 128 || ne == 256) && (g == 4 || g == 8 || g == 16) &&
+  if (!(L > 1 && C > 0 && (ne == 64 || ne == 128 || ne == 256) && (g == 4 || g == 8 || g == 16) &&
         (reinterpret_cast<uintptr_t>(cands) & 15) == 0))  // 16-B aligned bulk copies
     return false;
   return eval_mma_smem(ne, g) <= 227 * 1024;
 }
 
 size_t eval_mma_smem(int ne, int g) {
+  if (ne == 64)  // stacked pairs: 32 / g candidates per group, three id rows each
+    return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)kIdSlots * (kN / 2 / g) * (3 * ne);
   return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)kIdSlots * (kN / g) * (ne + kRowsBlk);
 }
 
@@ -378,11 +411,12 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
   prm.L = L;
   prm.ne = ne;
   prm.g = g;
-  prm.n_jb = ne / kRowsBlk;
+  const bool st = ne == 64;
+  prm.n_jb = st ? 1 : ne / kRowsBlk;
   prm.C = C;
   prm.m = (int64_t)L * ne;
-  const int cpg = kN / g;
-  const int64_t base = (int64_t)(L - 1) * prm.n_jb;
+  const int cpg = (st ? kN / 2 : kN) / g;
+  const int64_t base = st ? (int64_t)(L - 1 + 1) / 2 : (int64_t)(L - 1) * prm.n_jb;
   const int64_t groups = (C + cpg - 1) / cpg;
   // enough units for ~2 per SM, each rebuilding its A planes (n_e x 128 x 8 B of E) once
   prm.n_cr = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (2 * sms + base - 1) / base));
@@ -401,10 +435,13 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
     kern<<<grid, kThreads, smem, s>>>(prm, E, cands, same);
     return cudaGetLastError();
   };
-  switch (g) {
-    case 4: return go(eval_mma_kernel<4>);
-    case 8: return go(eval_mma_kernel<8>);
-    case 16: return go(eval_mma_kernel<16>);
+  switch (g * 2 + (st ? 1 : 0)) {
+    case 8: return go(eval_mma_kernel<4, false>);
+    case 9: return go(eval_mma_kernel<4, true>);
+    case 16: return go(eval_mma_kernel<8, false>);
+    case 17: return go(eval_mma_kernel<8, true>);
+    case 32: return go(eval_mma_kernel<16, false>);
+    case 33: return go(eval_mma_kernel<16, true>);
     default: return cudaErrorInvalidValue;
   }
 }

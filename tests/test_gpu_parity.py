@@ -489,11 +489,13 @@ def test_bench_scale_properties(G):
 
 
 @pytest.mark.parametrize("L,ne,k,g,C", [(58, 256, 8, 8, 70), (48, 128, 8, 8, 33), (12, 256, 8, 4, 41),
-                                        (9, 128, 4, 16, 17), (58, 256, 8, 16, 129), (3, 128, 8, 4, 1)])
+                                        (9, 128, 4, 16, 17), (58, 256, 8, 16, 129), (3, 128, 8, 4, 1),
+                                        (26, 64, 6, 8, 70), (25, 64, 6, 4, 33), (9, 64, 4, 16, 17), (2, 64, 6, 8, 5)])
 def test_eval_tensor_core_path_matches_oracle(G, orc, monkeypatch, L, ne, k, g, C):
     """eval_mma.cu (E byte planes x one-hot assignment on tcgen05 kind::i8) gives exactly the
     oracle's D / cut / objective / argmin (placement.cpp:58-85), like the integer-ALU evaluator,
-    on ragged candidate counts (partial groups) and every supported g."""
+    on ragged candidate counts (partial groups), every supported g, and the stacked two-pairs-per-
+    operand mode at 64 experts (odd and even pair counts)."""
     topo = G.MoeTopology(L, ne, k, g)
     trace = G.generate_trace(topo, 20011, model_seed=2, stream_seed=5, device=0)
     s = G.RoutingStats(topo, 0)
