@@ -182,6 +182,95 @@ __global__ void max_cell_kernel(const unsigned long long* __restrict__ E, int64_
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
+// ---- small shapes (Mixtral class): one warp per candidate, one lane per layer ----
+// The whole E ((L-1) x NE x NE u32, cells < 2^27) and A sit in shared memory; lane l reads its
+// candidate's GPU ids of layers l and l+1 (NE bytes each), adds E_l(j, k) for every same-GPU (j, k)
+// pair, and forms layer l's per-GPU loads, |load - ideal_l| and per-GPU expert counts; the warp
+// reduces them.  Replaces eval_same_kernel + eval_dev_kernel (4096 CTAs each) for small n_e.
+template <int NE, int G>
+__global__ void __launch_bounds__(256)
+    eval_small_kernel(int L, const unsigned long long* __restrict__ A, const unsigned long long* __restrict__ E,
+                      const uint8_t* __restrict__ cands, int64_t C, int64_t base, unsigned long long* __restrict__ same,
+                      double* __restrict__ D, uint32_t* __restrict__ flags, long long* __restrict__ bad_index) {
+  extern __shared__ __align__(16) unsigned char sm_small[];
+  uint32_t* sE = reinterpret_cast<uint32_t*>(sm_small);                       // (L-1) * NE * NE
+  double* sIdeal = reinterpret_cast<double*>(sm_small + (((L - 1) * NE * NE * 4 + 15) & ~15));  // L
+  unsigned long long* sA = reinterpret_cast<unsigned long long*>(sIdeal + L);  // L * NE
+  const int m = L * NE;
+  for (int i = threadIdx.x; i < (L - 1) * NE * NE; i += blockDim.x) sE[i] = (uint32_t)E[i];
+  for (int i = threadIdx.x; i < L * NE; i += blockDim.x) sA[i] = A[i];
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    unsigned long long r = 0;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) r += sA[l * NE + j];
+    // ideal_l = A.row(l).sum() / g (placement.cpp:68); integer rowsum < 2^53 is exact in fp64
+    sIdeal[l] = __ddiv_rn((double)r, (double)G);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= C) return;
+  const uint8_t* P = cands + c * m;
+  unsigned long long sm = 0;
+  double dev = 0.0;
+  uint32_t cnt[G];
+#pragma unroll
+  for (int q = 0; q < G; ++q) cnt[q] = 0u;
+  bool bad = false;
+  for (int l = lane; l < L; l += 32) {
+    uint32_t pl[NE], pn[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      pl[j] = P[l * NE + j];
+      bad |= pl[j] >= (uint32_t)G;
+    }
+    unsigned long long load[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) load[q] = 0ull;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const unsigned long long a = sA[l * NE + j];
+#pragma unroll
+      for (int q = 0; q < G; ++q) {
+        load[q] += pl[j] == (uint32_t)q ? a : 0ull;
+        cnt[q] += pl[j] == (uint32_t)q ? 1u : 0u;
+      }
+    }
+    const double ideal = sIdeal[l];
+#pragma unroll
+    for (int q = 0; q < G; ++q) dev = fmax(dev, fabs(__dsub_rn((double)load[q], ideal)));
+    if (l + 1 < L) {
+#pragma unroll
+      for (int k = 0; k < NE; ++k) pn[k] = P[(l + 1) * NE + k];
+      const uint32_t* El = sE + l * NE * NE;
+#pragma unroll
+      for (int j = 0; j < NE; ++j)
+#pragma unroll
+        for (int k = 0; k < NE; ++k) sm += pl[j] == pn[k] ? (unsigned long long)El[j * NE + k] : 0ull;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+#pragma unroll
+    for (int q = 0; q < G; ++q) cnt[q] += __shfl_xor_sync(0xffffffffu, cnt[q], o);
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    same[c] = sm;
+    D[c] = dev;
+    bool infeasible = bad;
+#pragma unroll
+    for (int q = 0; q < G; ++q) infeasible |= cnt[q] != (uint32_t)(m / G);
+    if (infeasible) {
+      atomicOr(flags, (uint32_t)kFlagInfeasible);
+      atomicMin(bad_index, (long long)(base + c));
+    }
+  }
+}
+
 // ---- deviation + feasibility: one CTA per candidate, one warp per layer at a time ----
 __global__ void __launch_bounds__(256)
     eval_dev_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
@@ -595,6 +684,22 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
   if (C <= 0) return cudaSuccess;
   const int64_t m = (int64_t)L * ne;
   cudaError_t e = cudaSuccess;
+  if (small_cells && L > 1 && L <= 256 && (L - 1) * ne * ne * 4 <= 32 * 1024 && !std::getenv("GIMBAL_EVAL_NO_SMALL")) {
+    auto kern = ne == 8 && g == 8   ? eval_small_kernel<8, 8>
+              : ne == 8 && g == 4   ? eval_small_kernel<8, 4>
+              : ne == 8 && g == 2   ? eval_small_kernel<8, 2>
+              : ne == 16 && g == 8  ? eval_small_kernel<16, 8>
+              : ne == 16 && g == 4  ? eval_small_kernel<16, 4>
+              : ne == 16 && g == 16 ? eval_small_kernel<16, 16>
+                                    : nullptr;
+    if (kern) {
+      const size_t smem = (((size_t)(L - 1) * ne * ne * 4 + 15) & ~(size_t)15) + (size_t)L * 8 + (size_t)L * ne * 8;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<(unsigned)((C + 7) / 8), 256, smem, s>>>(L, A, E, cands, C, base, same, D, flags, bad_index);
+      return cudaGetLastError();
+    }
+  }
   const bool fast = small_cells && ne % 32 == 0 && 256 % ne == 0;
   if (small_cells && eval_mma_supported(L, ne, g, cands, C)) {
     // tensor cores: E byte planes x one-hot assignment (eval_mma.cu)

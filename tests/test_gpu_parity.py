@@ -614,3 +614,28 @@ def test_queued_pass_reports_infeasible_candidate(G, shape):
     cands[7, 5] = (int(cands[7, 5]) - 1) % g
     res = hp.run(trace, cands)
     assert 0 <= res.argmin < 12
+
+
+@pytest.mark.parametrize("L,ne,k,g,C", [(32, 8, 2, 8, 4096), (5, 8, 3, 4, 9), (7, 16, 4, 8, 33), (3, 16, 2, 16, 5),
+                                        (40, 8, 2, 2, 17), (2, 8, 8, 8, 3)])
+def test_eval_small_shapes_match_oracle(G, orc, monkeypatch, L, ne, k, g, C):
+    """eval_small_kernel (warp per candidate, lane per layer, E and A in shared memory) gives the
+    oracle's D / cut / objective / argmin exactly, as does the generic evaluator it replaces."""
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 30011, model_seed=4, stream_seed=6, device=0)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(trace)
+    oA, oE, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+    cands = G.shuffled_candidates(L * ne, g, 13, C)
+    want = orc.eval_costs(L, ne, g, oA, oE, cands, 1.5, 0.25)
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("GIMBAL_EVAL_NO_SMALL", env)
+        got = G.eval_costs(s, torch.from_numpy(cands).cuda(), 1.5, 0.25)
+        for a, b in zip(got[:3], want[:3]):
+            assert np.array_equal(a, b)
+        assert got[3] == want[3]
+    bad = cands.copy()
+    bad[C // 2, 0] = (int(bad[C // 2, 0]) + 1) % g
+    with pytest.raises(ValueError, match=f"candidate {C // 2} is infeasible"):
+        G.eval_costs(s, torch.from_numpy(bad).cuda())
