@@ -462,6 +462,95 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
     return int(round(ingest + 2 + probe + topk + 1 + 1 + sort_launches(L * ne) + 1 + 3))
 
 
+def run_stream(args, G, topo, world, rank, local, T, C, desc):
+    """BASELINE configs[4]: one step = the whole stream of T / STREAM_WINDOW tumbling windows.
+    Window w is generated with drift epoch w (STREAM_DRIFT of each layer's Zipf rank permutation
+    re-drawn per window); each rank holds its 1/N token shard of every window (weak in windows'
+    token rate: per-GPU shard fixed), E is all-reduced per window for N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_21626_b200.pipeline import shard_range
+
+    L, k, g, m = topo.n_layers, topo.top_k, topo.n_gpus, topo.total_experts()
+    n_win = T // STREAM_WINDOW
+    per_rank = STREAM_WINDOW  # each rank counts a full window-sized shard: N x tokens per window
+    windows = []
+    for w in range(n_win):
+        windows.append(G.generate_trace(topo, per_rank, model_seed=1, stream_seed=2,
+                                        first_token=(w * world + rank) * per_rank, drift=STREAM_DRIFT,
+                                        drift_epoch=w + 1, device=local))
+    calib = G.generate_trace(topo, 20000, model_seed=1, stream_seed=3, first_token=0, drift=STREAM_DRIFT,
+                             drift_epoch=0, device=local)  # offline_tokens default (sim.hpp:41)
+    c_lo, c_hi = shard_range(C, rank, world)
+    cands = torch.from_numpy(G.shuffled_candidates(m, g, 1000 + c_lo, c_hi - c_lo)).to(f"cuda:{local}")
+    hp = G.HotPath(topo, device=local)
+    M = hp.calibrate(calib)
+    stream = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", local))
+
+    def step():
+        if world > 1 or args.dist_path:
+            return hp.stream_distributed(windows, cands, c_lo, C, M)
+        return hp.stream(windows, cands, M)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    handles = [hp.stats] + ([hp._twin().stats] if getattr(hp, "_twin_hp", None) is not None else [])
+    for h in handles:
+        h.count_timing(True)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1) / args.steps
+    clk = clocks.stop() if clocks else None
+    count_ms, count_launches = 0.0, 0
+    for h in handles:
+        a, b = h.count_timing(False)
+        count_ms, count_launches = count_ms + a, count_launches + b
+    if world > 1:
+        tt = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens = world * per_rank * n_win
+    roof = make_roofline(args, topo, per_rank * n_win, count_ms, count_launches, ms, traffic=False)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_stream_e2e(G, topo, windows, cands.cpu(), M, args, local)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline("dsv3", per_rank * n_win, C, windows=n_win)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"error": str(ex)}
+    if rank == 0:
+        moved = [r[1] for r in res]
+        line = {
+            "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
+            "data": "synthetic (drifting Zipf RoutingModel-semantics windows generated on the GPU)",
+            "config": {"workload": desc, "windows": n_win, "window_tokens_per_gpu": per_rank, "candidates": C, "g": g,
+                       "parallelism": f"token-shard dp{world} per window",
+                       "strong_pair_set": M.experts, "mean_moved_per_window": float(np.mean(moved[1:])) if len(moved) > 1
+                       else None},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": stream_launches(topo, n_win, count_launches / args.steps) * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def stream_launches(topo, n_win, count_launches_per_step):
     """Our kernels per streaming step: per window the counting launch(es) (measured), derive A + W,
     greedy (keys + bitonic sort + walk) and the evaluator (same + dev + finish)."""

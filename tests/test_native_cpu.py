@@ -1,6 +1,7 @@
 """The C ABI library without a GPU: it loads, exports every symbol include/gimbal_gpu.h declares,
 and its host-side validation / utilities match the reference (no kernel launches here)."""
 import ctypes as C
+import os
 import re
 import subprocess
 
@@ -129,3 +130,22 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(N, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(ImportError):
         N.lib()
+
+
+def test_bench_entry_points_exist():
+    """bench.py's config dispatch targets exist (a refactor once dropped run_stream) and the
+    launch-count model runs for every BASELINE config."""
+    import importlib
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    bench = importlib.import_module("bench")
+    for name in ("main", "run_stream", "run_stream_e2e", "run_e2e", "make_roofline", "cpu_baseline",
+                 "run_reference", "kernel_launches_per_step", "stream_launches", "h2d_ceiling", "count_kernel"):
+        assert callable(getattr(bench, name, None)), name
+    import paper_2602_21626_b200 as G
+
+    for cfg, (L, ne, k, g, T, C, _) in bench.CONFIGS.items():
+        n = bench.kernel_launches_per_step(G.MoeTopology(L, ne, k, g), 1, tokens=T)
+        assert 8 <= n <= 40, (cfg, n)
