@@ -269,16 +269,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (cm < n_cm) {
               const int rg = cm >> kcs_shift, kc = cm & (kcs - 1);
               const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-              // E is [(L-1)][n_e][n_e]: rows l * n_e + 64 .. of the stacked block are E_l+1's
-              const int64_t grow = (int64_t)l * ne + j0 + row;
-              if (grow < (int64_t)(prm.L - 1) * ne) {
-                const ulonglong2* src = reinterpret_cast<const ulonglong2*>(E + grow * ne + k);
-                v[u][0] = __ldg(src);
-                v[u][1] = __ldg(src + 1);
-              } else {
-                v[u][0] = make_ulonglong2(0ull, 0ull);
-                v[u][1] = make_ulonglong2(0ull, 0ull);
-              }
+              // E is [(L-1)][n_e][n_e]: rows l * n_e + 64 .. of the stacked block are E_l+1's; rows
+              // past the last pair load a valid row and are zeroed at use (loads stay batched)
+              const int64_t grow = min((int64_t)l * ne + j0 + row, (int64_t)(prm.L - 1) * ne - 1);
+              const ulonglong2* src = reinterpret_cast<const ulonglong2*>(E + grow * ne + k);
+              v[u][0] = __ldg(src);
+              v[u][1] = __ldg(src + 1);
             }
           }
 #pragma unroll
@@ -287,8 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (cm < n_cm) {
               const int rg = cm >> kcs_shift, kc = cm & (kcs - 1);
               const int row = rg * 8 + (lane >> 2), k = kc * 16 + (lane & 3) * 4;
-              const uint32_t c0 = (uint32_t)v[u][0].x, c1 = (uint32_t)v[u][0].y;
-              const uint32_t c2 = (uint32_t)v[u][1].x, c3 = (uint32_t)v[u][1].y;
+              const uint32_t live_row = (int64_t)l * ne + j0 + row < (int64_t)(prm.L - 1) * ne ? ~0u : 0u;
+              const uint32_t c0 = (uint32_t)v[u][0].x & live_row, c1 = (uint32_t)v[u][0].y & live_row;
+              const uint32_t c2 = (uint32_t)v[u][1].x & live_row, c3 = (uint32_t)v[u][1].y & live_row;
               const uint32_t off = kmajor_off(row, k, sbo);
 #pragma unroll
               for (int b = 0; b < kPlanes; ++b) {
