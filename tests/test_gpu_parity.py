@@ -489,8 +489,8 @@ def test_bench_scale_properties(G):
 
 
 @pytest.mark.parametrize("L,ne,k,g,C", [(58, 256, 8, 8, 70), (48, 128, 8, 8, 33), (12, 256, 8, 4, 41),
-                                        (9, 128, 4, 16, 17), (58, 256, 8, 16, 129), (3, 128, 8, 4, 1),
-                                        (26, 64, 6, 8, 70), (25, 64, 6, 4, 33), (9, 64, 4, 16, 17), (2, 64, 6, 8, 5)])
+                                        (9, 128, 4, 16, 17), (58, 256, 8, 16, 129), (3, 128, 8, 4, 9), (3, 128, 8, 4, 1),
+                                        (26, 64, 6, 8, 70), (25, 64, 6, 4, 33), (9, 64, 4, 16, 17), (2, 64, 6, 8, 11)])
 def test_eval_tensor_core_path_matches_oracle(G, orc, monkeypatch, L, ne, k, g, C):
     """eval_mma.cu (E byte planes x one-hot assignment on tcgen05 kind::i8) gives exactly the
     oracle's D / cut / objective / argmin (placement.cpp:58-85), like the integer-ALU evaluator,
