@@ -422,7 +422,7 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
     plus one transposition each on the layer-major path), derive A + derive W, the max-cell probe
     (when tokens * k^2 >= 2^27), the strong-pair set (register top-K: 1-2 launches, else segment
     top-K passes) + select, greedy (keys + bitonic sort + walk) and the evaluator (same + dev +
-    finish)."""
+    finish; split around the overlapped greedy walk for m >= 1024; one fused kernel for small shapes)."""
     L, ne, k = topo.n_layers, topo.n_experts, topo.top_k
     _, engine = count_kernel(ne, k, L)
     kernel = count_kernel(ne, k, L)[0]
@@ -459,7 +459,14 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
             if b <= 1:
                 break
     probe = 1 if tokens * k * k >= (1 << 27) else 0
-    return int(round(ingest + 2 + probe + topk + 1 + 1 + sort_launches(L * ne) + 1 + 3))
+    m = L * ne
+    if (L - 1) * ne * ne * 4 <= 32 * 1024 and ne in (8, 16):
+        evaluator = 2      # eval_small (same + deviation in one kernel) + finish
+    elif m >= 1024:
+        evaluator = 5      # candidates 1..C-1 (same + dev) beside the greedy walk, row 0 (same + dev), finish
+    else:
+        evaluator = 3      # same + dev + finish
+    return int(round(ingest + 2 + probe + topk + 1 + 1 + sort_launches(m) + 1 + evaluator))
 
 
 def run_stream(args, G, topo, world, rank, local, T, C, desc):

@@ -701,8 +701,10 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
     }
   }
   const bool fast = small_cells && ne % 32 == 0 && 256 % ne == 0;
-  if (small_cells && eval_mma_supported(L, ne, g, cands, C)) {
-    // tensor cores: E byte planes x one-hot assignment (eval_mma.cu)
+  // tensor cores: E byte planes x one-hot assignment (eval_mma.cu); a handful of candidates (the
+  // greedy row scored after the overlapped walk) is cheaper on the integer path, which reads E once
+  // instead of building every unit's byte planes (DS-V3: 8.5 us vs 0.12 ms for the one row)
+  if (small_cells && eval_mma_supported(L, ne, g, cands, C) && !(C <= 8 && ne % 32 == 0 && 256 % ne == 0)) {
     e = launch_eval_mma(L, ne, g, E, cands, C, same, s);
     if (e != cudaSuccess) return e;
   } else if (L > 1 && fast) {
