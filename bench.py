@@ -331,8 +331,11 @@ def main():
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(G, topo, trace, cands_host, T, args, local)
+    if not args.no_e2e and e2e_fits(world, T * L * k, dev if world > 1 else None):
+        e2e = run_e2e(G, topo, trace, cands_host, T, args, local, world=world, dist_on=dist_on, c_lo=c_lo,
+                      n_candidates=C)
+    elif not args.no_e2e:
+        e2e = {"unavailable": f"host RAM below {world} pinned trace shards of {T * L * k / 1e9:.1f} GB"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -624,10 +627,32 @@ def run_stream_e2e(G, topo, windows, cands_host, M, args, local):
     return out
 
 
-def run_e2e(G, topo, trace, cands_host, T, args, local):
-    """Same step through the public API from pinned host memory: H2D of the trace and the
-    candidates and D2H of the scores inside the timed region."""
+def e2e_fits(world, shard_bytes, dev):
+    """Every rank pins its whole trace shard: run the end-to-end leg only when the node's available
+    host RAM holds all of them with margin (decided on rank 0's reading, agreed over the group)."""
+    try:
+        import psutil
+
+        ok = psutil.virtual_memory().available * 0.8 > world * shard_bytes * 1.05
+    except Exception:
+        ok = world == 1
+    if world == 1:
+        return ok
     import torch
+    import torch.distributed as dist
+
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.broadcast(flag, src=0)
+    return bool(flag.item())
+
+
+def run_e2e(G, topo, trace, cands_host, T, args, local, world=1, dist_on=False, c_lo=0, n_candidates=0):
+    """Same step through the public API from pinned host memory: H2D of the trace and the
+    candidates and D2H of the scores inside the timed region.  With N ranks each rank copies its
+    own shard and candidate slice, the step is run_distributed (NCCL all-reduce of E, global
+    argmin), and the time is the max over ranks."""
+    import torch
+    import torch.distributed as dist
 
     L, k = topo.n_layers, topo.top_k
     try:
@@ -644,6 +669,9 @@ def run_e2e(G, topo, trace, cands_host, T, args, local):
     out = {}
 
     def step():
+        if dist_on:
+            dcands = ch.to(f"cuda:{local}", non_blocking=True)   # H2D of this rank's candidate slice
+            return hp.run_distributed(host, dcands, c_lo, n_candidates)  # host shard counted while copied
         hp.stats.reset()
         hp.stats.add_tokens(host)            # H2D inside (pinned, double-buffered)
         dcands = ch.to(f"cuda:{local}", non_blocking=True)   # H2D of the candidates
@@ -666,10 +694,15 @@ def run_e2e(G, topo, trace, cands_host, T, args, local):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     wall = (time.perf_counter() - t0) / n * 1e3
-    h2d = int(T * L * k + C * topo.total_experts())
-    out = {"value": T / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": int(3 * C * 8 + 8), "ms_per_step": ms, "wall_ms_per_step": wall, "steps": n}
-    out.update(h2d_ceiling(host, h2d, ms, local))
+    if world > 1:
+        tt = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    h2d = int(T * L * k + C * topo.total_experts())  # this rank's copies
+    out = {"value": world * T / (ms * 1e-3), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(world * T * L * k + (n_candidates if world > 1 else C) * topo.total_experts()),
+           "d2h_bytes_per_step": int(world * (3 * C * 8 + 8)), "ms_per_step": ms, "wall_ms_per_step": wall, "steps": n}
+    out.update(h2d_ceiling(host, h2d, ms, local))  # per rank: its bytes against its own PCIe link
     return out
 
 
