@@ -630,14 +630,14 @@ def run_stream_e2e(G, topo, windows, cands_host, M, args, local):
 def e2e_fits(world, shard_bytes, dev):
     """Every rank pins its whole trace shard: run the end-to-end leg only when the node's available
     host RAM holds all of them with margin (decided on rank 0's reading, agreed over the group)."""
+    if world == 1:  # one shard: run_e2e reports a failed pinned allocation itself
+        return True
     try:
         import psutil
 
         ok = psutil.virtual_memory().available * 0.5 > world * shard_bytes
     except Exception:
-        ok = world == 1
-    if world == 1:
-        return ok
+        ok = False
     import torch
     import torch.distributed as dist
 
