@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GIMBAL_ABI_VERSION 1
+#define GIMBAL_ABI_VERSION 2
 
 typedef enum gimbal_status {
   GIMBAL_OK = 0,
@@ -150,11 +150,13 @@ int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t n_M, i
  * -> `placement` [m] int32 and row 0 of `candidates`) -> eval_cost of all C candidates ->
  * `scores` [3][C] f64 and `argmin` [1] int64 (device).  capacity must be <= m/g (the reference's
  * greedy_place would reject a larger set).  Device-side errors are reported by the next
- * gimbal_stats_sync. */
+ * gimbal_stats_sync; when `flags_device` (2 x u32, may be NULL) is given, the handle's error words
+ * are copied there at the end of the pass, so a caller reading its results back can skip that sync
+ * when both are zero. */
 int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity, int32_t anchor_gpu,
                       uint8_t* candidates_device, int64_t n_candidates, double alpha, double beta,
                       double* scores_device, int64_t* argmin_device, int32_t* placement_device,
-                      int32_t* members_device, int32_t* n_members_device);
+                      int32_t* members_device, int32_t* n_members_device, uint32_t* flags_device);
 
 /* Counting kernels of this handle run on n_sms SMs (default: all).  Leaving SMs free lets a
  * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */

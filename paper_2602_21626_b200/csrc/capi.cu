@@ -938,7 +938,7 @@ int gimbal_window_place_async(gimbal_stats_t h, const int32_t* M, int32_t nM, in
 
 int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t capacity, int32_t anchor,
                       uint8_t* candidates, int64_t C, double alpha, double beta, double* scores, int64_t* argmin,
-                      int32_t* placement, int32_t* members, int32_t* n_members) {
+                      int32_t* placement, int32_t* members, int32_t* n_members, uint32_t* flags_out) {
   GIMBAL_TRY(check_handle(h));
   if (!(alpha > 0.0) || !(beta > 0.0)) return invalid("PlacementProblem: alpha and beta must be > 0");
   if (anchor < 0 || anchor >= h->topo.n_gpus) return invalid("build_affinity_set: anchor_gpu out of range");
@@ -982,8 +982,10 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   // Mixtral m = 256: 0.286 vs 0.269 ms per step, DS-V2-Lite m = 1664: 5.15 vs 5.25 ms)
   if (C < 2 || m < 1024 || std::getenv("GIMBAL_NO_GREEDY_OVERLAP")) {
     GIMBAL_TRY(greedy_on(h->stream));
-    return enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
-                        reinterpret_cast<long long*>(argmin), h->dflags + 1);
+    GIMBAL_TRY(enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
+                            reinterpret_cast<long long*>(argmin), h->dflags + 1));
+    if (flags_out) GIMBAL_CUDA_TRY(cudaMemcpyAsync(flags_out, h->dflags, 8, cudaMemcpyDeviceToDevice, h->stream));
+    return GIMBAL_OK;
   }
   // The greedy walk (latency-bound, one CTA) runs on the side stream while candidates 1..C-1 are
   // scored on the handle's stream; candidate 0 (the greedy row it writes) is scored after the join.
@@ -1006,6 +1008,7 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
       (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)h->topo.top_k * h->topo.top_k;
   GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, same, scores, scores + C, scores + 2 * C,
                                      reinterpret_cast<long long*>(argmin), flags, h->stream));
+  if (flags_out) GIMBAL_CUDA_TRY(cudaMemcpyAsync(flags_out, h->dflags, 8, cudaMemcpyDeviceToDevice, h->stream));
   return GIMBAL_OK;
 }
 

@@ -123,9 +123,10 @@ class HotPath:
         m, C_ = topo.total_experts(), int(candidates.shape[0])
         dev = torch.device("cuda", self.device)
         if getattr(self, "_pk", None) is None:
-            # int32 words: [0:2] argmin (int64), [2] |M|, [3] pad, [4:4+m] M, [4+m:4+2m] greedy
-            self._pk = torch.zeros(4 + 2 * m, dtype=torch.int32, device=dev)
-            self._pk_host = torch.empty(4 + 2 * m, dtype=torch.int32).pin_memory()
+            # int32 words: [0:2] argmin (int64), [2] |M|, [3] pad, [4:6] error flags, [6:6+m] M,
+            # [6+m:6+2m] greedy
+            self._pk = torch.zeros(6 + 2 * m, dtype=torch.int32, device=dev)
+            self._pk_host = torch.empty(6 + 2 * m, dtype=torch.int32).pin_memory()
             self._hstream = torch.cuda.ExternalStream(self.stats.device_buffers()[2], device=dev)
         scores = self._scores(C_)
         self.stats._after_torch(candidates)
@@ -133,19 +134,20 @@ class HotPath:
         N.check(N.lib().gimbal_pass_async(
             self.stats.handle, self.threshold, self.top_e, m // topo.n_gpus, self.anchor_gpu,
             C.c_void_p(candidates.data_ptr()), C_, self.alpha, self.beta, C.c_void_p(scores.data_ptr()),
-            C.c_void_p(base), C.c_void_p(base + 16 + 4 * m), C.c_void_p(base + 16), C.c_void_p(base + 8)),
-            "pass")
+            C.c_void_p(base), C.c_void_p(base + 24 + 4 * m), C.c_void_p(base + 24), C.c_void_p(base + 8),
+            C.c_void_p(base + 16)), "pass")
         # the read-back runs on torch's stream behind the handle's (a pinned block used on the
         # handle's own stream would outlive it in torch's host allocator)
         cur = torch.cuda.current_stream(dev)
         cur.wait_stream(self._hstream)
         self._pk_host.copy_(self._pk, non_blocking=True)
-        self.stats.sync()  # raises deferred device-side errors
         cur.synchronize()
         h = self._pk_host.numpy()
+        if h[4] or h[5]:
+            self.stats.sync()  # raises (and clears) the deferred device-side error
         n = int(h[2])
-        return HotPathResult(affinity=AffinitySet(experts=h[4:4 + n].tolist(), anchor_gpu=self.anchor_gpu),
-                             greedy=h[4 + m:4 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
+        return HotPathResult(affinity=AffinitySet(experts=h[6:6 + n].tolist(), anchor_gpu=self.anchor_gpu),
+                             greedy=h[6 + m:6 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
 
     def place_with(self, M: AffinitySet, candidates, greedy_row: bool = True) -> HotPathResult:
         """Stats already counted, strong-pair set fixed (sim.cpp:94-104 computes M once from a

@@ -532,13 +532,13 @@ def test_queued_pass_argument_errors(G):
     lib = N.lib()
     with pytest.raises(ValueError, match="anchor_gpu out of range"):
         N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g, g, C.c_void_p(cands.data_ptr()), 4, 1.0, 1.0,
-                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), None))
     with pytest.raises(ValueError, match="capacity"):
         N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g + 1, 0, C.c_void_p(cands.data_ptr()), 4, 1.0, 1.0,
-                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), None))
     with pytest.raises(ValueError, match="alpha and beta"):
         N.check(lib.gimbal_pass_async(s.handle, 0.0, 4, m // g, 0, C.c_void_p(cands.data_ptr()), 4, 0.0, 1.0,
-                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p)))
+                                      C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), C.c_void_p(p), None))
     big = np.arange(m // g + 1, dtype=np.int32)
     with pytest.raises(ValueError, match="exceeds anchor capacity"):
         N.check(lib.gimbal_window_place_async(s.handle, big.ctypes.data, big.size, 0, C.c_void_p(cands.data_ptr()), 4,
