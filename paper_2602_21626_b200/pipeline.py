@@ -372,11 +372,34 @@ class HotPath:
         self.stats.add_tokens(trace_shard)
         allreduce_counts(self.stats, group)
         topo = self.topo
+        n_local = candidates_shard.shape[0]
+        if (M_fixed is None and dist.get_backend(group) == "nccl" and getattr(candidates_shard, "is_cuda", False)
+                and topo.n_gpus <= 255):
+            # the queued pass (gimbal_pass_async) on this rank's slice; ranks other than the first
+            # score their slice behind a scratch row that receives the (identical) greedy placement
+            dev = torch.device("cuda", self.device)
+            lead = 0 if cand_offset == 0 else 1
+            if lead or n_local == 0:
+                m = topo.total_experts()
+                if getattr(self, "_dcands", None) is None or tuple(self._dcands.shape) != (n_local + 1, m):
+                    self._dcands = torch.zeros((n_local + 1, m), dtype=torch.uint8, device=dev)
+                if n_local:
+                    self._dcands[1:].copy_(candidates_shard)
+                buf, lead = self._dcands, 1
+            else:
+                buf = candidates_shard
+            res = self._place_queued(buf)
+            local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
+            if n_local:
+                local[cand_offset:cand_offset + n_local] = self._out[2, lead:lead + n_local]
+            dist.all_reduce(local, op=dist.ReduceOp.MIN, group=group)
+            objs = local.cpu().numpy()
+            return HotPathResult(affinity=res.affinity, greedy=res.greedy, argmin=merge_argmin(objs),
+                                 objective=float(objs.min()) if objs.size else None)
         M = M_fixed if M_fixed is not None else build_affinity_set(
             self.stats, topo, self.threshold, self.top_e, topo.total_experts() // topo.n_gpus, self.anchor_gpu)
         gp = greedy_place(self.stats, M, topo.n_gpus,
                           out_u8_device=candidates_shard[0] if cand_offset == 0 else None)
-        n_local = candidates_shard.shape[0]
         dev = torch.device("cuda", self.device)
         local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
         if n_local:

@@ -639,3 +639,38 @@ def test_eval_small_shapes_match_oracle(G, orc, monkeypatch, L, ne, k, g, C):
     bad[C // 2, 0] = (int(bad[C // 2, 0]) + 1) % g
     with pytest.raises(ValueError, match=f"candidate {C // 2} is infeasible"):
         G.eval_costs(s, torch.from_numpy(bad).cuda())
+
+
+def test_run_distributed_single_rank_matches_run(G, orc):
+    """run_distributed over NCCL (one rank) uses the queued pass: the first rank's slice carries the
+    greedy row, a later slice is scored behind a scratch row; both give the oracle's answers."""
+    import socket
+
+    import torch.distributed as dist
+
+    L, ne, k, g = SHAPES["qwen3"]
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 9001, model_seed=2, stream_seed=4, device=0)
+    C = 20
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 21, C)).cuda()
+    want = G.HotPath(topo, 0).run(trace, cands.clone())
+    oA, oE, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        hp = G.HotPath(topo, 0)
+        got = hp.run_distributed(trace, cands.clone(), 0, C)
+        assert got.argmin == want.argmin and got.greedy == want.greedy
+        assert got.affinity.experts == want.affinity.experts
+        part = cands[5:].clone()
+        got2 = hp.run_distributed(trace, part, 5, C)
+        _, _, obj, am = orc.eval_costs(L, ne, g, oA, oE, part.cpu().numpy())
+        assert got2.argmin == 5 + am and got2.objective == obj.min()
+        assert got2.greedy == want.greedy
+        assert torch.equal(part, cands[5:])  # the caller's slice is not overwritten
+    finally:
+        dist.destroy_process_group()
