@@ -448,34 +448,36 @@ __global__ void __launch_bounds__(1024)
 constexpr int kRegTopK = 8;
 constexpr int kRegThreads = 256;
 
-__device__ __forceinline__ void topk_insert(unsigned long long (&r)[kRegTopK], unsigned long long key) {
-  if (key <= r[kRegTopK - 1]) return;
+template <int K>
+__device__ __forceinline__ void topk_insert(unsigned long long (&r)[K], unsigned long long key) {
+  if (key <= r[K - 1]) return;
 #pragma unroll
-  for (int i = kRegTopK - 1; i >= 0; --i) {
+  for (int i = K - 1; i >= 0; --i) {
     const unsigned long long prev = i ? r[i - 1] : ~0ull;
     r[i] = key > prev ? prev : (key > r[i] ? key : r[i]);
   }
 }
 
-__device__ __forceinline__ void topk_warp_merge(unsigned long long (&r)[kRegTopK]) {
+template <int K>
+__device__ __forceinline__ void topk_warp_merge(unsigned long long (&r)[K]) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long other[kRegTopK];
+    unsigned long long other[K];
 #pragma unroll
-    for (int i = 0; i < kRegTopK; ++i) other[i] = __shfl_xor_sync(0xffffffffu, r[i], o);
+    for (int i = 0; i < K; ++i) other[i] = __shfl_xor_sync(0xffffffffu, r[i], o);
 #pragma unroll
-    for (int i = 0; i < kRegTopK; ++i) topk_insert(r, other[i]);
+    for (int i = 0; i < K; ++i) topk_insert<K>(r, other[i]);
   }
 }
 
-template <bool FROM_E>
+template <bool FROM_E, int K>  // K = kept keys per list (4 when top_e <= 4, else 8)
 __global__ void __launch_bounds__(kRegThreads)
     topk_reg_kernel(const unsigned long long* __restrict__ in, int64_t n, double threshold,
                     unsigned long long* __restrict__ out, uint32_t* __restrict__ flags) {
-  __shared__ unsigned long long lists[kRegThreads / 32][kRegTopK];
-  unsigned long long r[kRegTopK];
+  __shared__ unsigned long long lists[kRegThreads / 32][K];
+  unsigned long long r[K];
 #pragma unroll
-  for (int i = 0; i < kRegTopK; ++i) r[i] = 0ull;
+  for (int i = 0; i < K; ++i) r[i] = 0ull;
   bool over = false;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long key;
@@ -490,23 +492,23 @@ __global__ void __launch_bounds__(kRegThreads)
     } else {
       key = in[idx];
     }
-    topk_insert(r, key);
+    topk_insert<K>(r, key);
   }
   if (FROM_E && __syncthreads_or(over) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagOverflow);
-  topk_warp_merge(r);
+  topk_warp_merge<K>(r);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < kRegTopK; ++i) lists[warp][i] = r[i];
+    for (int i = 0; i < K; ++i) lists[warp][i] = r[i];
   }
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
-    for (int i = 0; i < kRegTopK; ++i) r[i] = lane < kRegThreads / 32 ? lists[lane][i] : 0ull;
-    topk_warp_merge(r);
+    for (int i = 0; i < K; ++i) r[i] = lane < kRegThreads / 32 ? lists[lane][i] : 0ull;
+    topk_warp_merge<K>(r);
     if (lane == 0) {
 #pragma unroll
-      for (int i = 0; i < kRegTopK; ++i) out[(int64_t)blockIdx.x * kRegTopK + i] = r[i];
+      for (int i = 0; i < K; ++i) out[(int64_t)blockIdx.x * K + i] = r[i];
     }
   }
 }
@@ -792,14 +794,17 @@ cudaError_t launch_affinity_topk(int L, int ne, const unsigned long long* E, dou
     // a/b hold >= n_pad / 2 keys each (n_pad = next pow2 of n >= 2 * 296 * 8 here, else 1 block)
     int grid = (int)std::min<int64_t>(296, (n + kRegThreads * 16 - 1) / (kRegThreads * 16));
     grid = std::max(grid, 1);
-    topk_reg_kernel<true><<<grid, kRegThreads, 0, s>>>(E, n, threshold, a, flags);
+    const int kk = K <= 4 ? 4 : kRegTopK;  // keys kept per list (>= K, the caller reads K of them)
+    (kk == 4 ? topk_reg_kernel<true, 4> : topk_reg_kernel<true, kRegTopK>)<<<grid, kRegThreads, 0, s>>>(
+        E, n, threshold, a, flags);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (grid == 1) {
       *result = a;
       return cudaSuccess;
     }
-    topk_reg_kernel<false><<<1, kRegThreads, 0, s>>>(a, (int64_t)grid * kRegTopK, 0.0, b, flags);
+    (kk == 4 ? topk_reg_kernel<false, 4> : topk_reg_kernel<false, kRegTopK>)<<<1, kRegThreads, 0, s>>>(
+        a, (int64_t)grid * kk, 0.0, b, flags);
     *result = b;
     return cudaGetLastError();
   }
