@@ -48,12 +48,14 @@ METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
 ATOMS_RANDOM_PEAK = 2.553e12
 # dram__bytes_read.sum + dram__bytes_write.sum per counting launch from one `ncu --set full`
 # capture (profiles/r1c_ncu_count_<config>.md), bytes / launch, with the tokens of that launch.
-TRAFFIC = {"dsv3": {"bytes": 51.768141e9 + 1.372393e9, "tokens_in_launch": 67108864,
-                    "source": "profiles/r1c_ncu_count_dsv3.md"},
-           "qwen3": {"bytes": 18.002675e9 + 9.890816e6, "tokens_in_launch": 33554432,
-                     "source": "profiles/r1c_ncu_count_qwen3.md"},
-           "dsv2lite": {"bytes": 4.356829e9 + 7.6224e6, "tokens_in_launch": 16777216,
-                        "source": "profiles/r1c_ncu_count_dsv2lite.md"}}
+TRAFFIC = {"dsv3": {"bytes": 52.823845e9 + 1.497470e9, "tokens_in_launch": 67108864,
+                    "source": "profiles/r1f_ncu_count_dsv3.md"},
+           "qwen3": {"bytes": 35.337853e9 + 18.544128e6, "tokens_in_launch": 33554432,
+                     "source": "profiles/r1f_ncu_count_qwen3.md"},
+           "dsv2lite": {"bytes": 4.358883e9 + 5.723648e6, "tokens_in_launch": 16777216,
+                        "source": "profiles/r1f_ncu_count_dsv2lite.md"},
+           "mixtral": {"bytes": 67.134720e6 + 344.576e3, "tokens_in_launch": 1048576,
+                       "source": "profiles/r1f_ncu_count_mixtral.md"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 REASON_BITS = {
