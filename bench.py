@@ -424,7 +424,7 @@ def make_roofline(args, topo, T, count_total_ms, count_launches, ms, traffic=Tru
 
 def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
     """Our kernels per step (memsets/copies are not kernels): the counting launch(es) (measured;
-    plus one transposition each on the layer-major path), derive A + derive W, the max-cell probe
+    plus one transposition each on the layer-major path), derive A (W only on read-back), the max-cell probe
     (when tokens * k^2 >= 2^27), the strong-pair set (register top-K: 1-2 launches, else segment
     top-K passes) + select, greedy (keys + bitonic sort + walk) and the evaluator (same + dev +
     finish; split around the overlapped greedy walk for m >= 1024; one fused kernel for small shapes)."""
@@ -471,7 +471,7 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
         evaluator = 5      # candidates 1..C-1 (same + dev) beside the greedy walk, row 0 (same + dev), finish
     else:
         evaluator = 3      # same + dev + finish
-    return int(round(ingest + 2 + probe + topk + 1 + 1 + sort_launches(m) + 1 + evaluator))
+    return int(round(ingest + 1 + probe + topk + 1 + 1 + sort_launches(m) + 1 + evaluator))
 
 
 def run_stream(args, G, topo, world, rank, local, T, C, desc):
@@ -564,7 +564,7 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
 
 
 def stream_launches(topo, n_win, count_launches_per_step):
-    """Our kernels per streaming step: per window the counting launch(es) (measured), derive A + W,
+    """Our kernels per streaming step: per window the counting launch(es) (measured), derive A,
     greedy (keys + bitonic sort + walk) and the evaluator (same + dev + finish)."""
     def sort_launches(n):
         p = 1
@@ -582,7 +582,7 @@ def stream_launches(topo, n_win, count_launches_per_step):
             kk *= 2
         return c
 
-    per_window = 2 + 1 + sort_launches(topo.total_experts()) + 1 + 3
+    per_window = 1 + 1 + sort_launches(topo.total_experts()) + 1 + 3
     return int(round(count_launches_per_step + n_win * per_window))
 
 

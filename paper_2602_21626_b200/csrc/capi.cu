@@ -160,14 +160,25 @@ struct gimbal_stats_s {
   int64_t m() const { return (int64_t)topo.n_layers * topo.n_experts; }
   int64_t nE() const { return (int64_t)(topo.n_layers - 1) * topo.n_experts * topo.n_experts; }
 
+  // A is derived from E for every placement; W = sum_l E_l only when it is read back (the
+  // placement pass scores cuts on E directly), which saves a launch per pass and per window
+  bool w_derived = true;
+  void set_derived(bool d) {
+    derived = d;
+    w_derived = d;
+  }
   int derive() {
     if (derived) return GIMBAL_OK;
     const int L = topo.n_layers, ne = topo.n_experts;
-    if (L > 1) {
-      GIMBAL_CUDA_TRY(launch_derive_activation(L, ne, topo.top_k, dE, dA, stream));
-      GIMBAL_CUDA_TRY(launch_derive_w(L, ne, dE, dW, stream));
-    }
+    if (L > 1) GIMBAL_CUDA_TRY(launch_derive_activation(L, ne, topo.top_k, dE, dA, stream));
     derived = true;
+    return GIMBAL_OK;
+  }
+  int derive_w() {
+    GIMBAL_TRY(derive());
+    if (w_derived) return GIMBAL_OK;
+    if (topo.n_layers > 1) GIMBAL_CUDA_TRY(launch_derive_w(topo.n_layers, topo.n_experts, dE, dW, stream));
+    w_derived = true;
     return GIMBAL_OK;
   }
 
@@ -484,7 +495,7 @@ int gimbal_stats_reset(gimbal_stats_t h) {
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 4, h->stream));  // word 1 (deferred) survives
   h->tokens = 0;
   h->max_tokens = -1;
-  h->derived = true;
+  h->set_derived(true);
   return GIMBAL_OK;
 }
 
@@ -503,7 +514,7 @@ int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int
     GIMBAL_TRY(h->count_host(ids, id_bytes, n_tokens));
   }
   h->tokens += n_tokens;
-  h->derived = false;
+  h->set_derived(false);
   return GIMBAL_OK;
 }
 
@@ -535,7 +546,7 @@ int gimbal_stats_read(gimbal_stats_t h, uint64_t* A, uint64_t* E, uint64_t* W, i
   GIMBAL_TRY(check_handle(h));
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
-  GIMBAL_TRY(h->derive());
+  GIMBAL_TRY(h->derive_w());
   const int64_t ne = h->topo.n_experts;
   GIMBAL_TRY(copy_out(A, h->dA, h->m() * 8, mem, h->stream));
   if (h->nE() > 0) GIMBAL_TRY(copy_out(E, h->dE, h->nE() * 8, mem, h->stream));
@@ -629,7 +640,7 @@ int gimbal_stats_merge(gimbal_stats_t h, const uint64_t* counts, int64_t tokens,
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
   tmp.release();
   h->tokens += tokens;
-  h->derived = !pairs;
+  h->set_derived(!pairs);
   h->max_tokens = -1;
   return GIMBAL_OK;
 }
@@ -640,7 +651,7 @@ int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
   std::lock_guard<std::mutex> lk(h->mu);
   h->tokens = global_tokens;
   h->max_tokens = -1;
-  h->derived = h->topo.n_layers < 2;
+  h->set_derived(h->topo.n_layers < 2);
   return GIMBAL_OK;
 }
 
