@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GIMBAL_ABI_VERSION 2
+#define GIMBAL_ABI_VERSION 3
 
 typedef enum gimbal_status {
   GIMBAL_OK = 0,

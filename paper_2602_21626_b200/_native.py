@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GIMBAL_LIB") or os.path.join(HERE, "lib", "libgimbal_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "gimbal_gpu.h")
 
+ABI_VERSION = 3  # include/gimbal_gpu.h GIMBAL_ABI_VERSION
 OK, INVALID_ARGUMENT, CUDA_ERROR, NCCL_ERROR, OVERFLOW, OUT_OF_RANGE, NOT_SUPPORTED = range(7)
 MEM_HOST, MEM_DEVICE = 0, 1
 
@@ -85,6 +86,12 @@ def lib() -> C.CDLL:
                 fn = getattr(L, name)
                 fn.restype = res
                 fn.argtypes = args
+            got = L.gimbal_abi_version()
+            if got != ABI_VERSION:
+                # an older build would ignore arguments this binding passes (e.g. ABI 2's flags_out
+                # of gimbal_pass_async) and silently drop device-side errors
+                raise ImportError(f"{LIB_PATH}: ABI version {got}, this binding needs {ABI_VERSION} "
+                                  f"(include/gimbal_gpu.h GIMBAL_ABI_VERSION); rebuild the library")
             _LIB = L
         return _LIB
 

@@ -237,7 +237,7 @@ struct gimbal_stats_s {
   int count_device(const void* ids, int id_bytes, int64_t n) {
     const int L = topo.n_layers;
     if (use_stack && mma_stack_supported(L, topo.n_experts, topo.top_k, id_bytes, ids) &&
-        !std::getenv("GIMBAL_NO_DIRECT")) {
+        !GIMBAL_KNOB("GIMBAL_NO_DIRECT")) {
       // 64-expert layers: two layers per 128-row tensor-core operand, straight from the trace
       GIMBAL_TRY(timing_begin());
       const cudaError_t e = launch_count_mma_stack(L, topo.n_experts, topo.top_k, sms, smem_optin,
@@ -250,7 +250,7 @@ struct gimbal_stats_s {
       cudaGetLastError();  // shape does not fit the stacked kernel: fall through (timing slot reused)
     }
     if (use_fp4 && fp4_count_supported(L, topo.n_experts, topo.top_k, id_bytes, ids, n) &&
-        !std::getenv("GIMBAL_NO_DIRECT")) {
+        !GIMBAL_KNOB("GIMBAL_NO_DIRECT")) {
       // 256 experts, top-8: block-scaled FP4 tensor-core contraction straight from the trace
       GIMBAL_TRY(timing_begin());
       const cudaError_t e = launch_count_fp4(L, sms, static_cast<const uint8_t*>(ids), n, dE, stream);
@@ -261,7 +261,7 @@ struct gimbal_stats_s {
       }
       cudaGetLastError();  // not mappable: fall through (timing slot reused)
     }
-    if (!use_mma && direct_u15_supported(lm8_plan, id_bytes, ids) && !std::getenv("GIMBAL_NO_DIRECT")) {
+    if (!use_mma && direct_u15_supported(lm8_plan, id_bytes, ids) && !GIMBAL_KNOB("GIMBAL_NO_DIRECT")) {
       // every uint8 id is a valid expert at n_e = 256: no validation / transposition pass
       GIMBAL_TRY(timing_begin());
       GIMBAL_CUDA_TRY(launch_count_direct_u15(lm8_plan, static_cast<const uint8_t*>(ids), n, dE, stream));
@@ -269,7 +269,7 @@ struct gimbal_stats_s {
       return GIMBAL_OK;
     }
     if (use_mma && id_bytes == 1 && topo.top_k == 8 && L % 2 == 0 && (reinterpret_cast<uintptr_t>(ids) & 15) == 0 &&
-        n < INT32_MAX && !std::getenv("GIMBAL_NO_DIRECT") && !std::getenv("GIMBAL_NO_TMA")) {
+        n < INT32_MAX && !GIMBAL_KNOB("GIMBAL_NO_DIRECT") && !GIMBAL_KNOB("GIMBAL_NO_TMA")) {
       // tensor-core contraction straight from the token-major trace (TMA-mapped rows)
       GIMBAL_TRY(timing_begin());
       GIMBAL_CUDA_TRY(launch_count_mma_direct(L, topo.n_experts, sms, static_cast<const uint8_t*>(ids), n, dE,
@@ -277,7 +277,7 @@ struct gimbal_stats_s {
       GIMBAL_TRY(timing_end());
       return GIMBAL_OK;
     }
-    if (small_count_supported(L, topo.n_experts, topo.top_k, id_bytes, n) && !std::getenv("GIMBAL_NO_SMALL")) {
+    if (small_count_supported(L, topo.n_experts, topo.top_k, id_bytes, n) && !GIMBAL_KNOB("GIMBAL_NO_SMALL")) {
       // the whole E fits every CTA's shared memory (Mixtral class): one pass, no transposition
       GIMBAL_TRY(timing_begin());
       GIMBAL_CUDA_TRY(launch_count_small(L, topo.n_experts, topo.top_k, sms, static_cast<const uint8_t*>(ids), n,
@@ -396,7 +396,7 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
   h->lm8_plan = make_lm8_plan(topo->n_layers, topo->n_experts, topo->top_k, h->sms, optin);
   {
     // GIMBAL_COUNT_PATH=atomic|lm8|split|fp4 overrides the default (tensor cores where supported)
-    const char* path = std::getenv("GIMBAL_COUNT_PATH");
+    const char* path = GIMBAL_KNOB("GIMBAL_COUNT_PATH");
     const bool want_mma = !(path && std::string(path) == "atomic");
     h->use_mma = want_mma && mma_count_supported(topo->n_layers, topo->n_experts, topo->top_k);
     h->use_stack = want_mma && !(path && std::string(path) == "lm8");
@@ -991,7 +991,7 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   // evaluator flags go to the deferred word (dflags[1]) as in gimbal_window_place_async
   // (tiny shapes: the walk is ~10 us and the extra launches cost more than it hides; measured
   // Mixtral m = 256: 0.286 vs 0.269 ms per step, DS-V2-Lite m = 1664: 5.15 vs 5.25 ms)
-  if (C < 2 || m < 1024 || std::getenv("GIMBAL_NO_GREEDY_OVERLAP")) {
+  if (C < 2 || m < 1024 || GIMBAL_KNOB("GIMBAL_NO_GREEDY_OVERLAP")) {
     GIMBAL_TRY(greedy_on(h->stream));
     GIMBAL_TRY(enqueue_eval(h, candidates, C, alpha, beta, scores, scores + C, scores + 2 * C,
                             reinterpret_cast<long long*>(argmin), h->dflags + 1));

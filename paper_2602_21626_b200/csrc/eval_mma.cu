@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 size_t eval_mma_smem(int ne, int g);
 
 bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C) {
-  if (std::getenv("GIMBAL_EVAL_ALU")) return false;
+  if (GIMBAL_KNOB("GIMBAL_EVAL_ALU")) return false;
   if (!(L > 1 && C > 0 && (ne == 64 || ne == 128 || ne == 256) && (g == 4 || g == 8 || g == 16) &&
         (reinterpret_cast<uintptr_t>(cands) & 15) == 0))  // 16-B aligned bulk copies
     return false;

@@ -314,7 +314,14 @@ constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tok
 // with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor instead.
 // Without the return-value dependency a warp issues its 64 increments back to back.
 // !U16 = guarded 15-bit halves with per-increment overflow detection (u15_count_token).
-template <bool U16>
+// AGG (issue-order experiments, U16 only; the AB build selects them with GIMBAL_TMA_AGG):
+//   0 = slot order as drawn (default);
+//   1 = both id words rotated by a lane-dependent number of slots, so the lanes of one atomic
+//       instruction read different draw positions (a hot expert, usually drawn into the same
+//       slot by every token, no longer lands on one address in one instruction);
+//   2 = warp aggregation: lanes with equal (j, k) cells in one instruction are merged with
+//       __match_any_sync and the leader adds the group size (the north_star's prescription).
+template <bool U16, int AGG = 0>
 __global__ void __launch_bounds__(kTmaBlock, 1)
     count_tm_u15_tma_kernel(const __grid_constant__ CUtensorMap tmap, Lm8Params prm,
                             unsigned long long* __restrict__ E) {
@@ -375,6 +382,11 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
       if (t_begin + (int64_t)i * kTmaBlock + tid < t_end) {
         if constexpr (U16) {
           if (!(has_dup8(cur) | has_dup8(nxt))) {
+            if constexpr (AGG == 1) {
+              const uint32_t rc = 8u * (uint32_t)(lane & 7), rn = 8u * (uint32_t)((lane >> 3) & 7);
+              cur = (cur >> rc) | (cur << ((64u - rc) & 63u));
+              nxt = (nxt >> rn) | (nxt << ((64u - rn) & 63u));
+            }
             uint32_t col[8], inc[8];
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
@@ -387,8 +399,18 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
               const uint32_t j = id_of(cur, a);
               uint32_t* rowp = cnt + j * wpr;
               const uint32_t sw = j & 31u;
+              if constexpr (AGG == 2) {
+                const uint32_t act = __activemask();
 #pragma unroll
-              for (int b = 0; b < 8; ++b) atomicAdd(rowp + (col[b] ^ sw), inc[b]);
+                for (int b = 0; b < 8; ++b) {
+                  const uint32_t grp = __match_any_sync(act, (j << 8) | id_of(nxt, b));
+                  if ((grp & ((1u << lane) - 1u)) == 0u)  // lowest lane of its group adds for all
+                    atomicAdd(rowp + (col[b] ^ sw), inc[b] * (uint32_t)__popc(grp));
+                }
+              } else {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) atomicAdd(rowp + (col[b] ^ sw), inc[b]);
+              }
             }
           } else {
 #pragma unroll 1
@@ -569,8 +591,8 @@ Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin) {
     const int ng = (pairs + p.P - 1) / p.P;
     p.P = (pairs + ng - 1) / ng;
     p.n_groups = (pairs + p.P - 1) / p.P;
-  } else if (ne % 64 == 0 && ne * ne * 2 <= budget && !(std::getenv("GIMBAL_COUNT_PATH") &&
-                                                         std::string(std::getenv("GIMBAL_COUNT_PATH")) == "split")) {
+  } else if (ne % 64 == 0 && ne * ne * 2 <= budget && !(GIMBAL_KNOB("GIMBAL_COUNT_PATH") &&
+                                                         std::string(GIMBAL_KNOB("GIMBAL_COUNT_PATH")) == "split")) {
     p.u15 = true;
     p.P = 1;
     p.R = ne;
@@ -617,10 +639,10 @@ bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L, 
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
   if (!encode || (L & 1) || (reinterpret_cast<uintptr_t>(trace) & 15) || T >= (int64_t)INT32_MAX ||
-      std::getenv("GIMBAL_NO_TMA"))
+      GIMBAL_KNOB("GIMBAL_NO_TMA"))
     return false;
   CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_NONE;
-  if (const char* e = std::getenv("GIMBAL_TMA_PROMO")) {
+  if (const char* e = GIMBAL_KNOB("GIMBAL_TMA_PROMO")) {
     const int v = std::atoi(e);
     promo = v >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
             : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -662,7 +684,7 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   // (up to 64 Ki u64 global atomics), so chunks stay >= 512 Ki tokens: a 1 Mi-token streaming
   // window counts in 2 chunks (measured 2.08 ms/window vs 2.53 ms with 16 Ki-token chunks)
   int64_t n_chunks = std::min<int64_t>(96, std::max<int64_t>(1, T >> 19));
-  if (const char* e = std::getenv("GIMBAL_DIRECT_CHUNKS")) n_chunks = std::max(1, std::atoi(e));
+  if (const char* e = GIMBAL_KNOB("GIMBAL_DIRECT_CHUNKS")) n_chunks = std::max(1, std::atoi(e));
   n_chunks = std::min<int64_t>(n_chunks, std::max<int64_t>(1, T / 16384));
   prm.chunk_tokens = (T + n_chunks - 1) / n_chunks;
   n_chunks = (T + prm.chunk_tokens - 1) / prm.chunk_tokens;
@@ -671,8 +693,12 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   CUtensorMap tmap;
   if (encode_trace_map(&tmap, trace, T, plan.L, 2, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
-    static const bool u16 = !(std::getenv("GIMBAL_TMA_MODE") && std::string(std::getenv("GIMBAL_TMA_MODE")) == "u15");
-    auto kern = u16 ? count_tm_u15_tma_kernel<true> : count_tm_u15_tma_kernel<false>;
+    static const bool u16 = !(GIMBAL_KNOB("GIMBAL_TMA_MODE") && std::string(GIMBAL_KNOB("GIMBAL_TMA_MODE")) == "u15");
+    static const int agg = GIMBAL_KNOB("GIMBAL_TMA_AGG") ? std::atoi(GIMBAL_KNOB("GIMBAL_TMA_AGG")) : 0;
+    auto kern = !u16      ? count_tm_u15_tma_kernel<false>
+                : agg == 1 ? count_tm_u15_tma_kernel<true, 1>
+                : agg == 2 ? count_tm_u15_tma_kernel<true, 2>
+                           : count_tm_u15_tma_kernel<true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, kTmaBlock, smem, s>>>(tmap, prm, E);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "gimbal_gpu.h"
@@ -42,6 +43,15 @@ enum KernelFlag : uint32_t {
     int s_ = (expr);                \
     if (s_ != GIMBAL_OK) return s_; \
   } while (0)
+
+// Experiment knobs (alternate kernels for A/B timing and engine-specific tests).  Compiled in only
+// for the test/tool build lib/libgimbal_gpu_ab.so (-DGIMBAL_AB_KNOBS); in the shipped
+// libgimbal_gpu.so every knob reads as unset, so the kernel choice depends on the inputs alone.
+#ifdef GIMBAL_AB_KNOBS
+#define GIMBAL_KNOB(name) std::getenv(name)
+#else
+#define GIMBAL_KNOB(name) (static_cast<const char*>(nullptr))
+#endif
 
 inline int invalid(const std::string& msg) {
   set_error(msg);

@@ -686,7 +686,7 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
   if (C <= 0) return cudaSuccess;
   const int64_t m = (int64_t)L * ne;
   cudaError_t e = cudaSuccess;
-  if (small_cells && L > 1 && L <= 256 && (L - 1) * ne * ne * 4 <= 32 * 1024 && !std::getenv("GIMBAL_EVAL_NO_SMALL")) {
+  if (small_cells && L > 1 && L <= 256 && (L - 1) * ne * ne * 4 <= 32 * 1024 && !GIMBAL_KNOB("GIMBAL_EVAL_NO_SMALL")) {
     auto kern = ne == 8 && g == 8   ? eval_small_kernel<8, 8>
               : ne == 8 && g == 4   ? eval_small_kernel<8, 4>
               : ne == 8 && g == 2   ? eval_small_kernel<8, 2>
@@ -790,7 +790,7 @@ cudaError_t launch_affinity_topk(int L, int ne, const unsigned long long* E, dou
                                  unsigned long long* a, unsigned long long* b, uint32_t* flags,
                                  unsigned long long** result, cudaStream_t s) {
   const int64_t n = (int64_t)(L - 1) * ne * ne;
-  if (K <= kRegTopK && !std::getenv("GIMBAL_TOPK_SORT")) {
+  if (K <= kRegTopK && !GIMBAL_KNOB("GIMBAL_TOPK_SORT")) {
     // a/b hold >= n_pad / 2 keys each (n_pad = next pow2 of n >= 2 * 296 * 8 here, else 1 block)
     int grid = (int)std::min<int64_t>(296, (n + kRegThreads * 16 - 1) / (kRegThreads * 16));
     grid = std::max(grid, 1);

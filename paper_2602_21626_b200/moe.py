@@ -113,6 +113,7 @@ class RoutingStats:
         N.check(N.lib().gimbal_stats_create(C.byref(topo.c()), device, C.byref(h)), "RoutingStats")
         self._h = h
         self._pending: list = []
+        self._inflight: list = []  # pinned host inputs whose asynchronous copies may be in flight
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -136,7 +137,22 @@ class RoutingStats:
         if mem == N.MEM_DEVICE:
             self._after_torch(keep)
         N.check(N.lib().gimbal_stats_add_tokens(self._h, C.c_void_p(ptr), ib, n, mem), "add_tokens")
+        self._keep_until_done(keep, mem)
         del keep
+
+    def _keep_until_done(self, tensor, mem) -> None:
+        """The count queued on the handle's stream may still read ``tensor`` after this call returns:
+        a device tensor (possibly a temporary made by ``.contiguous()``) is recorded on that stream so
+        torch's caching allocator does not hand its memory out before the count has run; a pinned
+        host torch tensor (copied asynchronously, gimbal_gpu.h) is held until the next synchronising
+        call.  numpy inputs are pageable (copied through the library's own bounce buffers) or
+        synchronously consumed."""
+        if not hasattr(tensor, "data_ptr"):
+            return
+        if mem == N.MEM_DEVICE:
+            tensor.record_stream(self._ext_stream)
+        else:
+            self._inflight.append(tensor)
 
     def _after_torch(self, tensor) -> None:
         """Orders the handle's stream after torch's current stream (device inputs produced by
@@ -179,6 +195,7 @@ class RoutingStats:
         W = np.zeros((ne, ne), np.uint64)
         N.check(N.lib().gimbal_stats_read(self._h, A.ctypes.data, E.ctypes.data if E.size else None,
                                           W.ctypes.data, N.MEM_HOST), "read")
+        self._inflight.clear()
         return A, E, W
 
     def activation(self) -> np.ndarray:  # moe.hpp:91
@@ -232,6 +249,7 @@ class RoutingStats:
     def sync(self) -> None:
         self._flush()
         N.check(N.lib().gimbal_stats_sync(self._h), "sync")
+        self._inflight.clear()
 
     @property
     def handle(self):

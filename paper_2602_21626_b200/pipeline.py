@@ -273,7 +273,9 @@ class HotPath:
         n, m = len(windows), self.topo.total_experts()
         dev = torch.device("cuda", self.device)
         c_loc = int(candidates_shard.shape[0])
-        lead = 0 if cand_offset == 0 else 1  # scratch greedy row ahead of a non-leading slice
+        # scratch greedy row ahead of a non-leading (or empty) slice: with C < world some ranks hold
+        # no candidates, and their window placement still needs row 0 to receive the greedy row
+        lead = 0 if (cand_offset == 0 and c_loc > 0) else 1
         tok = torch.tensor([int(w.shape[0]) for w in windows], dtype=torch.int64, device=dev)
         dist.all_reduce(tok, op=dist.ReduceOp.SUM, group=group)
         glob = tok.tolist()

@@ -43,7 +43,7 @@ def test_library_is_sm100a_only(G):
 
 
 def test_abi_version(G):
-    assert G._native.lib().gimbal_abi_version() == 2
+    assert G._native.lib().gimbal_abi_version() == G._native.ABI_VERSION == 3
 
 
 def test_topology_validation_messages(G):
