@@ -151,96 +151,154 @@ def dist_env():
     return world, rank, local
 
 
+def bench_config(config, world, T, C, scaling):
+    """The `config` object both arms print (same keys, so the driver can pair them)."""
+    L, ne, k, g, _, _, desc = CONFIGS[config]
+    out = {"workload": desc, "tokens": T, "candidates": C, "g": g, "scaling": scaling,
+           "parallelism": f"token-shard dp{world}" + (" per window" if config == "stream" else "")}
+    if config != "stream":
+        out["l2"] = f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def sample_size(config):
+    """(tokens generated, tokens counted per step, candidates scored per step) of the bounded CPU
+    sample.  BASELINE.md §4: Mixtral runs in full; the large shapes are timed on a 2^22-token
+    prefix and 16 candidates (rates are linear in T and in C).  A step counts one 2^19-token
+    slice of the prefix (slices rotate, so a run covers all of it) and scores the 16
+    candidates, which keeps the --impl reference run within a few minutes."""
+    return {"mixtral": (1 << 20, 1 << 20, 4096), "dsv2lite": (1 << 22, 1 << 20, 16),
+            "qwen3": (1 << 22, 1 << 19, 16), "dsv3": (1 << 22, 1 << 19, 16),
+            "stream": (1 << 22, 1 << 19, 16)}[config]
+
+
+def sample_inputs(config, T, C, n_threads):
+    """The bounded CPU sample, built from the reference alone: the generator's tables from the
+    reference RoutingModel's weights (moe.cpp:43-78), the trace from the oracle's C twin of the
+    GPU generator (same bytes as the GPU arm's tokens 0..T-1), candidates by the reference's own
+    recipe (acceptance_main.cpp:344-351, Rng(1000 + c).shuffle).  No product library is loaded."""
+    import oracle
+
+    L, ne, k, g, _, _, _ = CONFIGS[config]
+    ref = oracle.Ref()
+    cdf, thr = oracle.generator_tables_from_ref(ref, L, ne, k, g, model_seed=1)
+    ids = oracle.Oracle().generate_trace(L, ne, k, cdf, int(thr[0]), int(thr[1]), 2, 0, T, n_threads=n_threads)
+    m = L * ne
+    cands = np.stack([ref.shuffled_balanced(m, g, 1000 + c) for c in range(C)]).astype(np.uint8)
+    return ids, cands
+
+
+def extrapolated_rate(r, sT, sC, T, C, windows=1):
+    """Tokens/s of the whole workload from one timed sample: stats linear in tokens, the strong-
+    pair set + greedy once per pass (per window when streaming), eval_cost linear in candidates."""
+    per_token = r["t_stats"] / sT
+    per_cand = r["t_eval"] / max(sC, 1)
+    total = per_token * T + windows * (r["t_place"] + per_cand * C)
+    return T / total
+
+
+def reference_samples(config, T, C, steps, n_threads, windows=1):
+    """Runs `steps` bounded samples of the reference pipeline (oracle/_ref: the reference's own
+    moe.cpp / placement.cpp) on n_threads host cores; returns (per-step results, description)."""
+    import oracle
+
+    L, ne, k, g, _, _, _ = CONFIGS[config]
+    gen_T, step_T, sC = sample_size(config)
+    ids, cands = sample_inputs(config, gen_T, sC, n_threads)
+    ref = oracle.Ref()
+    out = []
+    n_slices = max(1, gen_T // step_T)
+    for i in range(steps):
+        sl = ids[(i % n_slices) * step_T:(i % n_slices + 1) * step_T]
+        r = ref.pipeline(L, ne, k, g, sl, cands, n_threads=n_threads)
+        r["rate"] = extrapolated_rate(r, step_T, sC, T, C, windows)
+        out.append(r)
+    desc = (f"reference moe.cpp/placement.cpp (oracle/_ref) on {n_threads} thread(s) of '{cpu_model()}': per step "
+            f"add_token over a {step_T}-token slice of a {gen_T}-token prefix (slices rotate; one RoutingStats per "
+            f"thread, built before the clock), affinity + flat forms + build_affinity_set + greedy_place, and "
+            f"{sC} eval_cost calls; rate extrapolated linearly to {T} tokens and {C} candidates"
+            + (f" per window x {windows} windows" if windows > 1 else ""))
+    return out, desc
+
+
+def single_thread_figure(config, T, C, windows=1):
+    """the reference as shipped, one thread, on a small bounded sample."""
+    import oracle
+
+    L, ne, k, g, _, _, _ = CONFIGS[config]
+    sT, sC = {"mixtral": (1 << 16, 256)}.get(config, (1 << 13, 1))
+    ids, cands = sample_inputs(config, sT, sC, os.cpu_count() or 1)
+    r = oracle.Ref().pipeline(L, ne, k, g, ids, cands, n_threads=1)
+    return {"value": extrapolated_rate(r, sT, sC, T, C, windows), "unit": "tokens/s", "cores": 1,
+            "sample": f"{sT} tokens, {sC} eval_cost calls, 1 thread; stage times {r['t_stats']:.3f}/"
+                      f"{r['t_place']:.3f}/{r['t_eval']:.3f} s, extrapolated linearly"}
+
+
+def workload_size(config, world, args):
+    L, ne, k, g, T, C, desc = CONFIGS[config]
+    if args.tokens:
+        T = args.tokens
+    if args.candidates:
+        C = args.candidates
+    return T, C
+
+
 def run_reference(args):
-    """--impl reference: the reference's own moe.cpp/placement.cpp (oracle/_ref) on host cores."""
+    """--impl reference: the reference's own moe.cpp/placement.cpp (oracle/_ref) on the host cores,
+    rank 0 only.  This process loads only oracle libraries (checked in tests/test_bench.py)."""
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    import oracle
-
-    L, ne, k, g, T, C, desc = CONFIGS[args.config]
-    ref = oracle.Ref()
     cores = os.cpu_count() or 1
-    sample_T, sample_C = sample_size(args.config)
-    ids, cands = sample_inputs(args.config, sample_T, sample_C)
-    times = []
-    for i in range(args.warmup + args.steps):
-        r = ref.pipeline(L, ne, k, g, ids, cands, n_threads=cores)
-        if i >= args.warmup:
-            times.append(r)
-    rate = np.median([extrapolated_rate(r, sample_T, sample_C, T, C) for r in times])
-    ms = T / rate * 1e3
+    T, C = workload_size(args.config, world, args)
+    if args.weak:
+        T *= world
+    windows = T // STREAM_WINDOW if args.config == "stream" else 1
+    res, desc = reference_samples(args.config, T, C, args.warmup + args.steps, cores, windows)
+    timed = res[args.warmup:]
+    rate = float(np.median([r["rate"] for r in timed]))
+    step_ms = float(np.median([r["t_total"] for r in timed])) * 1e3
+    single = single_thread_figure(args.config, T, C, windows)
+    scaling = "weak" if args.weak else "strong"
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int-in-f64 (reference Eigen doubles)",
-        "data": "synthetic (GPU generator, RoutingModel semantics)",
-        "config": {"workload": desc, "tokens": T, "candidates": C, "g": g},
-        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                         "sample": f"{sample_T} tokens through add_token+flat forms+affinity+greedy, {sample_C} "
-                                   f"eval_cost calls; rate extrapolated linearly to {T} tokens and {C} candidates"},
+        "steps": args.steps, "warmup": args.warmup,
+        # wall time of one bounded sample step (what this process spent per step); the whole
+        # workload's time at `value` is in extrapolated_ms_per_workload
+        "ms_per_step": step_ms, "extrapolated_ms_per_workload": T / rate * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "int-in-f64 (reference Eigen doubles)",
+        "data": "synthetic (the GPU arm's generator restated on the CPU from the reference RoutingModel weights)",
+        "config": bench_config(args.config, world, T, C, scaling),
+        "cpu_baseline": {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": desc,
+                         "cpu_model": cpu_model(), "single_thread": single},
         "e2e": {"value": rate, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def sample_size(config):
-    # (tokens, candidates) of the bounded CPU sample: ~5-15 s of reference work on 16 cores;
-    # Mixtral runs in full (BASELINE.md §4)
-    return {"mixtral": (1 << 20, 4096), "dsv2lite": (1 << 18, 32), "qwen3": (1 << 16, 8), "dsv3": (1 << 15, 2),
-            "stream": (1 << 15, 2)}[config]
-
-
-def sample_inputs(config, T, C):
-    """Bounded CPU sample: generated with the bit-exact CPU twin of the GPU generator."""
-    import oracle
-
-    L, ne, k, g, _, _, _ = CONFIGS[config]
-    o = oracle.Oracle()
-    cdf, thr = generator_tables_host(L, ne, k, g)
-    ids = o.generate_trace(L, ne, k, cdf.ravel(), int(thr[0]), int(thr[1]), 2, 0, T)
-    cands = np.zeros((C, L * ne), np.uint8)
-    import paper_2602_21626_b200 as G
-
-    cands[:] = G.shuffled_candidates(L * ne, g, 1000, C)
-    return ids, cands
-
-
-def generator_tables_host(L, ne, k, g):
-    import paper_2602_21626_b200 as G
-
-    return G.generator_tables(G.MoeTopology(L, ne, k, g), model_seed=1)
-
-
-def extrapolated_rate(r, sT, sC, T, C):
-    per_token = r["t_stats"] / sT
-    per_cand = r["t_eval"] / max(sC, 1)
-    total = per_token * T + r["t_place"] + per_cand * C
-    return T / total
-
-
 def cpu_baseline(config, T, C, windows=1):
-    """Rank 0, N = 1: the reference's own code (oracle/_ref) on host cores, bounded sample.  With
-    `windows` > 1 (streaming) the placement stages run once per window: stats scale with T, strong-
-    pair set + greedy + C eval_cost calls with the window count."""
+    """Rank 0, N = 1: the reference's own code (oracle/_ref) on host cores, one bounded sample step
+    (plus the single-thread figure)."""
     import oracle
 
-    L, ne, k, g, _, _, _ = CONFIGS[config]
     if not oracle.ref_available():
         return None
-    sT, sC = sample_size(config)
-    ids, cands = sample_inputs(config, sT, sC)
     cores = os.cpu_count() or 1
-    r = oracle.Ref().pipeline(L, ne, k, g, ids, cands, n_threads=cores)
-    rate = extrapolated_rate(r, sT, sC, T, C)
-    if windows > 1:
-        rate = T / (r["t_stats"] / sT * T + windows * (r["t_place"] + r["t_eval"] / max(sC, 1) * C))
-    return {"value": rate, "unit": "tokens/s", "cores": cores, "kind": "reference",
-            "sample": f"{sT} tokens (add_token over {cores} RoutingStats shards + affinity/flat forms + "
-                      f"build_affinity_set + greedy_place) and {sC} eval_cost calls on the reference's own "
-                      f"moe.cpp/placement.cpp; stage times {r['t_stats']:.3f}/{r['t_place']:.3f}/{r['t_eval']:.3f} s, "
-                      f"extrapolated linearly to {T} tokens, {C} candidates"
-                      + (f" per window x {windows} windows" if windows > 1 else "")}
+    res, desc = reference_samples(config, T, C, 1, cores, windows)
+    return {"value": res[0]["rate"], "unit": "tokens/s", "cores": cores, "kind": "reference", "sample": desc,
+            "cpu_model": cpu_model(), "single_thread": single_thread_figure(config, T, C, windows)}
 
 
 def main():
@@ -250,7 +308,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="dsv3", choices=list(CONFIGS))
-    ap.add_argument("--tokens", type=int, default=0, help="override tokens per GPU")
+    ap.add_argument("--tokens", type=int, default=0,
+                    help="override the workload's tokens (the whole job's; per GPU with --weak)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank counts the configured token count (default: strong "
+                         "scaling, the BASELINE workload's fixed total split over the ranks)")
     ap.add_argument("--candidates", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -277,11 +339,8 @@ def main():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    L, ne, k, g, T, C, desc = CONFIGS[args.config]
-    if args.tokens:
-        T = args.tokens
-    if args.candidates:
-        C = args.candidates
+    L, ne, k, g, _, _, desc = CONFIGS[args.config]
+    T, C = workload_size(args.config, world, args)
     topo = G.MoeTopology(L, ne, k, g)
     m = topo.total_experts()
     dev = torch.device("cuda", local)
@@ -289,8 +348,14 @@ def main():
     if args.config == "stream":
         return run_stream(args, G, topo, world, rank, local, T, C, desc)
 
-    # inputs resident in HBM: this rank's token shard (tokens rank*T .. (rank+1)*T of one stream)
-    trace = G.generate_trace(topo, T, model_seed=1, stream_seed=2, first_token=rank * T, device=local)
+    # inputs resident in HBM: this rank's token shard of one stream.  Strong scaling (default, the
+    # BASELINE configs fix the total: "32M tokens, 1/2/4/8 GPUs"): tokens [T*r/N, T*(r+1)/N);
+    # --weak: tokens [r*T, (r+1)*T), i.e. N*T in the job
+    scaling = "weak" if args.weak else "strong"
+    T_job = T * world if args.weak else T
+    t_lo, t_hi = (rank * T, (rank + 1) * T) if args.weak else shard_range(T, rank, world)
+    T_rank = t_hi - t_lo
+    trace = G.generate_trace(topo, T_rank, model_seed=1, stream_seed=2, first_token=t_lo, device=local)
     c_lo, c_hi = shard_range(C, rank, world)
     cands_host = torch.from_numpy(G.shuffled_candidates(m, g, 1000 + c_lo, c_hi - c_lo))
     cands = cands_host.to(dev)
@@ -327,36 +392,34 @@ def main():
         tt = torch.tensor([ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    value = world * T / (ms * 1e-3)
+    value = T_job / (ms * 1e-3)
 
-    roof = make_roofline(args, topo, T, count_total_ms, count_launches, ms)
+    roof = make_roofline(args, topo, T_rank, count_total_ms, count_launches, ms)
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e and e2e_fits(world, T * L * k, dev if world > 1 else None):
-        e2e = run_e2e(G, topo, trace, cands_host, T, args, local, world=world, dist_on=dist_on, c_lo=c_lo,
-                      n_candidates=C)
+    if not args.no_e2e and e2e_fits(world, T_rank * L * k, dev if world > 1 else None):
+        e2e = run_e2e(G, topo, trace, cands_host, T_rank, T_job, args, local, world=world, dist_on=dist_on,
+                      c_lo=c_lo, n_candidates=C)
     elif not args.no_e2e:
-        e2e = {"unavailable": f"host RAM below {world} pinned trace shards of {T * L * k / 1e9:.1f} GB"}
+        e2e = {"unavailable": f"host RAM below {world} pinned trace shards of {T_rank * L * k / 1e9:.1f} GB"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(args.config, T, C)
+            cpu = cpu_baseline(args.config, T_job, C)
         except Exception as ex:  # reported, not fatal
             cpu = {"error": str(ex)}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
             "data": "synthetic (Zipf-skewed RoutingModel-semantics trace generated on the GPU)",
-            "config": {"workload": desc, "tokens_per_gpu": T, "candidates": C, "g": g,
-                       "parallelism": f"token-shard dp{world}",
-                       "l2": f"inputs ({T * L * k / 1e9:.1f} GB trace) exceed the 126 MB L2; no flush needed"},
+            "config": bench_config(args.config, world, T_job, C, scaling),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-            "gpu_launches": kernel_launches_per_step(topo, count_launches / args.steps, tokens=T) * args.steps,
+            "gpu_launches": kernel_launches_per_step(topo, count_launches / args.steps, tokens=T_rank) * args.steps,
         }
         print(json.dumps(line), flush=True)
     if dist.is_initialized():
@@ -477,8 +540,9 @@ def kernel_launches_per_step(topo, count_launches_per_step, top_e=4, tokens=0):
 def run_stream(args, G, topo, world, rank, local, T, C, desc):
     """BASELINE configs[4]: one step = the whole stream of T / STREAM_WINDOW tumbling windows.
     Window w is generated with drift epoch w (STREAM_DRIFT of each layer's Zipf rank permutation
-    re-drawn per window); each rank holds its 1/N token shard of every window (weak in windows'
-    token rate: per-GPU shard fixed), E is all-reduced per window for N > 1."""
+    re-drawn per window); each rank holds its 1/N token shard of every window (strong: the
+    STREAM_WINDOW-token window split over the ranks; --weak: a full window-sized shard per rank,
+    N x STREAM_WINDOW tokens per window), E is all-reduced per window for N > 1."""
     import torch
     import torch.distributed as dist
 
@@ -486,11 +550,13 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
 
     L, k, g, m = topo.n_layers, topo.top_k, topo.n_gpus, topo.total_experts()
     n_win = T // STREAM_WINDOW
-    per_rank = STREAM_WINDOW  # each rank counts a full window-sized shard: N x tokens per window
+    win_tokens = STREAM_WINDOW * (world if args.weak else 1)  # tokens per window, whole job
+    w_lo, w_hi = shard_range(win_tokens, rank, world)
+    per_rank = w_hi - w_lo
     windows = []
     for w in range(n_win):
         windows.append(G.generate_trace(topo, per_rank, model_seed=1, stream_seed=2,
-                                        first_token=(w * world + rank) * per_rank, drift=STREAM_DRIFT,
+                                        first_token=w * win_tokens + w_lo, drift=STREAM_DRIFT,
                                         drift_epoch=w + 1, device=local))
     calib = G.generate_trace(topo, 20000, model_seed=1, stream_seed=3, first_token=0, drift=STREAM_DRIFT,
                              drift_epoch=0, device=local)  # offline_tokens default (sim.hpp:41)
@@ -533,7 +599,7 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
         tt = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    tokens = world * per_rank * n_win
+    tokens = win_tokens * n_win
     roof = make_roofline(args, topo, per_rank * n_win, count_ms, count_launches, ms, traffic=False)
     e2e = None
     if not args.no_e2e and world == 1:
@@ -548,13 +614,13 @@ def run_stream(args, G, topo, world, rank, local, T, C, desc):
         moved = [r[1] for r in res]
         line = {
             "metric": METRIC, "value": tokens / (ms * 1e-3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None, "dtype": "u8 ids / u32-u64 counts / f64 costs",
             "data": "synthetic (drifting Zipf RoutingModel-semantics windows generated on the GPU)",
-            "config": {"workload": desc, "windows": n_win, "window_tokens_per_gpu": per_rank, "candidates": C, "g": g,
-                       "parallelism": f"token-shard dp{world} per window",
-                       "strong_pair_set": M.experts, "mean_moved_per_window": float(np.mean(moved[1:])) if len(moved) > 1
-                       else None},
+            "config": dict(bench_config("stream", world, tokens, C, "weak" if args.weak else "strong"),
+                           windows=n_win, window_tokens=win_tokens, strong_pair_set=M.experts,
+                           mean_moved_per_window=float(np.mean(moved[1:])) if len(moved) > 1 else None),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": stream_launches(topo, n_win, count_launches / args.steps) * args.steps,
         }
@@ -648,7 +714,7 @@ def e2e_fits(world, shard_bytes, dev):
     return bool(flag.item())
 
 
-def run_e2e(G, topo, trace, cands_host, T, args, local, world=1, dist_on=False, c_lo=0, n_candidates=0):
+def run_e2e(G, topo, trace, cands_host, T, T_job, args, local, world=1, dist_on=False, c_lo=0, n_candidates=0):
     """Same step through the public API from pinned host memory: H2D of the trace and the
     candidates and D2H of the scores inside the timed region.  With N ranks each rank copies its
     own shard and candidate slice, the step is run_distributed (NCCL all-reduce of E, global
@@ -701,8 +767,8 @@ def run_e2e(G, topo, trace, cands_host, T, args, local, world=1, dist_on=False, 
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     h2d = int(T * L * k + C * topo.total_experts())  # this rank's copies
-    out = {"value": world * T / (ms * 1e-3), "unit": "tokens/s",
-           "h2d_bytes_per_step": int(world * T * L * k + (n_candidates if world > 1 else C) * topo.total_experts()),
+    out = {"value": T_job / (ms * 1e-3), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(T_job * L * k + (n_candidates if world > 1 else C) * topo.total_experts()),
            "d2h_bytes_per_step": int(world * (3 * C * 8 + 8)), "ms_per_step": ms, "wall_ms_per_step": wall, "steps": n}
     out.update(h2d_ceiling(host, h2d, ms, local))  # per rank: its bytes against its own PCIe link
     return out

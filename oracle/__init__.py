@@ -78,6 +78,8 @@ class Oracle:
         L.go_generate_trace.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, C.c_uint64, C.c_uint64,
                                         C.c_uint64, _i64, _i64, _u8p]
         L.go_check_feasible.argtypes = [C.c_int, C.c_int, _i32p]
+        L.go_generate_trace_mt.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, C.c_uint64, C.c_uint64,
+                                           C.c_uint64, _i64, _i64, _u8p, C.c_int]
 
     @staticmethod
     def _ok(st: int, what: str):
@@ -172,12 +174,22 @@ class Oracle:
         self._ok(self.lib.go_static_placement(L, ne, k, g, out), "static_placement")
         return out
 
-    def generate_trace(self, L, ne, k, cdf, thr_base, thr_unif, seed, t0, T):
+    def generate_trace(self, L, ne, k, cdf, thr_base, thr_unif, seed, t0, T, n_threads: int = 1):
         out = np.zeros(T * L * k, np.uint8)
-        cdf = np.ascontiguousarray(cdf, np.uint32)
-        self._ok(self.lib.go_generate_trace(L, ne, k, cdf, thr_base, thr_unif, seed, t0, T, out),
+        cdf = np.ascontiguousarray(cdf, np.uint32).ravel()
+        self._ok(self.lib.go_generate_trace_mt(L, ne, k, cdf, thr_base, thr_unif, seed, t0, T, out, n_threads),
                  "generate_trace")
         return out.reshape(T, L, k)
+
+    def stats_accumulate(self, L, ne, k, ids, A, E, n_threads: int = 8) -> None:
+        """Adds a trace chunk's counts into A [L][n_e] / E [(L-1)][n_e][n_e] (uint64, C-contiguous,
+        updated in place): the incremental form of RoutingStats::add_token used to check
+        BASELINE-size GPU counts chunk by chunk."""
+        ids, ib = _ids(ids)
+        T = ids.size // (L * k)
+        assert A.dtype == np.uint64 and E.dtype == np.uint64 and A.flags.c_contiguous and E.flags.c_contiguous
+        self._ok(self.lib.go_stats(L, ne, k, ids.ctypes.data, ib, T, n_threads, A.reshape(-1),
+                                   E.reshape(-1) if E.size else np.zeros(1, np.uint64)), "stats")
 
 
 class Ref:
@@ -327,6 +339,32 @@ class Ref:
         out = np.zeros(m, np.int32)
         self.lib.ref_shuffled_balanced(m, g, seed, out)
         return out
+
+
+def generator_tables_from_ref(ref: "Ref", L, ne, k, g, model_seed=1, zipf_s=1.2, lam=0.5, peak=0.8):
+    """The trace generator's tables (cdf [L][n_e] u32, thresholds [2] u64; gimbal_gpu.h
+    gimbal_generator_tables, drift 0) restated from the REFERENCE's RoutingModel weights
+    (moe.cpp:43-78 via ref_model_weights): cdf = floor(2^32 x running sum of the normalised base
+    row), the last entry saturated; thr = the base / uniform / successor component boundaries
+    (1 - lambda, + lambda x rest x n_e) scaled to 2^32.  Lets the --impl reference leg build its
+    inputs from the reference alone (no product library in that process)."""
+    base, _ = ref.model_weights(L, ne, k, g, model_seed, zipf_s, lam, peak)
+    two32 = 4294967296.0
+    cdf = np.zeros((L, ne), np.uint32)
+    for l in range(L):
+        cum = 0.0
+        for e in range(ne):
+            cum += float(base[l, e])
+            q = np.floor(cum * two32)
+            cdf[l, e] = 0xFFFFFFFF if (e == ne - 1 or q >= 4294967295.0) else int(q)
+    rest = (1.0 - peak) / (ne - 1) if ne > 1 else 0.0
+    pb = 1.0 - lam
+    pu = lam * rest * ne
+    thr = np.array([min(two32, np.floor(pb * two32 + 0.5)), min(two32, np.floor((pb + pu) * two32 + 0.5))],
+                   np.float64).astype(np.uint64)
+    if lam == 0.0:
+        thr[:] = np.uint64(1 << 32)
+    return cdf, thr
 
 
 def ref_available() -> bool:

