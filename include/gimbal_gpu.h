@@ -162,6 +162,47 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
  * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms);
 
+/* ---- multi-GPU: token shards over ranks, NCCL over NVLink ----
+ * A, E and W are sums over tokens (moe.cpp:169-191), so ranks count contiguous token shards and
+ * one in-place SUM all-reduce of the u64 counts gives every rank the counts of the whole trace;
+ * the strong-pair set and greedy (placement.cpp:186-299) are then recomputed identically per
+ * rank, candidates are split into contiguous slices, and a MIN all-reduce of the per-candidate
+ * objectives yields the global argmin (lowest index on ties, as the single-GPU argmin).  NCCL is
+ * resolved at run time from the process's libnccl.so.2 (no link dependency). */
+#define GIMBAL_DIST_UNIQUE_ID_BYTES 128
+typedef void* gimbal_comm_t; /* an ncclComm_t: from gimbal_dist_comm_init, or the caller's own */
+/* ncclGetUniqueId: rank 0 calls it and shares the bytes with the other ranks out of band. */
+int gimbal_dist_unique_id(void* unique_id);
+/* ncclCommInitRank on `device` (one rank per GPU). */
+int gimbal_dist_comm_init(int32_t n_ranks, int32_t rank, const void* unique_id, int device, gimbal_comm_t* out);
+int gimbal_dist_comm_destroy(gimbal_comm_t comm);
+int gimbal_dist_comm_size(gimbal_comm_t comm, int32_t* n_ranks, int32_t* rank);
+/* In-place SUM all-reduce of the handle's counts (E, or A when L == 1) over `comm`, queued on the
+ * handle's stream behind its counting (no host synchronisation).  global_tokens >= 0 sets the
+ * token count; < 0 leaves it on the device (gimbal_stats_tokens reads it back as sum_j A(0,j)/k). */
+int gimbal_stats_allreduce(gimbal_stats_t h, gimbal_comm_t comm, int64_t global_tokens);
+/* Global argmin over the ranks' candidate slices, queued on the handle's stream: this rank's
+ * objectives [n_local] (device) land at [offset, offset + n_local) of `global_objectives` [n_total]
+ * (device scratch, +inf elsewhere), a MIN all-reduce merges the ranks, and the lowest index of the
+ * minimum goes to argmin_device. */
+int gimbal_dist_merge_argmin(gimbal_stats_t h, gimbal_comm_t comm, const double* objectives_device,
+                             int64_t n_local, int64_t offset, int64_t n_total, double* global_objectives_device,
+                             int64_t* argmin_device);
+/* One rank's whole distributed pass, queued on the handle's stream with no host synchronisation:
+ * gimbal_stats_allreduce (token count left on the device) -> gimbal_pass_async on this rank's
+ * candidate slice -> gimbal_dist_merge_argmin.  Global candidate 0 is the greedy placement.  The
+ * rank holding global candidates [cand_offset, cand_offset + n_local) passes them in
+ * `candidates_device` with one extra leading scratch row (which receives the greedy placement)
+ * unless cand_offset == 0 and n_local > 0 (its row 0 is global candidate 0 itself): rows =
+ * n_local + lead, lead = (cand_offset == 0 && n_local > 0) ? 0 : 1.  scores_device: [3][rows];
+ * global_objectives_device: [n_total] scratch; argmin_device: the global argmin. */
+int gimbal_pass_distributed_async(gimbal_stats_t h, gimbal_comm_t comm, double threshold, int32_t top_e,
+                                  int32_t capacity, int32_t anchor_gpu, uint8_t* candidates_device, int64_t n_local,
+                                  int64_t cand_offset, int64_t n_total, double alpha, double beta,
+                                  double* scores_device, double* global_objectives_device, int64_t* argmin_device,
+                                  int32_t* placement_device, int32_t* members_device, int32_t* n_members_device,
+                                  uint32_t* flags_device);
+
 /* ---- the reference's general dense forms (PlacementProblem with arbitrary A / W) ---- */
 
 /* eval_cost (placement.cpp:58-85) on dense A [rows][m] and W [m][m] doubles (host). */

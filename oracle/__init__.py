@@ -78,6 +78,8 @@ class Oracle:
         L.go_generate_trace.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, C.c_uint64, C.c_uint64,
                                         C.c_uint64, _i64, _i64, _u8p]
         L.go_check_feasible.argtypes = [C.c_int, C.c_int, _i32p]
+        L.go_eval_costs_mt.argtypes = [C.c_int, C.c_int, C.c_int, _u64p, _u64p, _u8p, _i64, C.c_double,
+                                       C.c_double, _f64p, _f64p, _f64p, _i64p, C.c_int]
         L.go_generate_trace_mt.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, C.c_uint64, C.c_uint64,
                                            C.c_uint64, _i64, _i64, _u8p, C.c_int]
 
@@ -121,7 +123,7 @@ class Oracle:
                  "eval_cost")
         return D.value, c.value, o.value
 
-    def eval_costs(self, L, ne, g, A, E, cands, alpha=1.0, beta=1.0):
+    def eval_costs(self, L, ne, g, A, E, cands, alpha=1.0, beta=1.0, n_threads: int = 1):
         A = np.ascontiguousarray(A, np.uint64).ravel()
         E = np.ascontiguousarray(E, np.uint64).ravel()
         if E.size == 0:
@@ -130,8 +132,12 @@ class Oracle:
         Cn = cands.shape[0]
         D, cut, obj = (np.zeros(Cn) for _ in range(3))
         am = C.c_int64(-1)
-        self._ok(self.lib.go_eval_costs(L, ne, g, A, E, cands, Cn, alpha, beta, D, cut, obj, C.byref(am)),
-                 "eval_costs")
+        if n_threads > 1:
+            self._ok(self.lib.go_eval_costs_mt(L, ne, g, A, E, cands, Cn, alpha, beta, D, cut, obj, C.byref(am),
+                                               n_threads), "eval_costs")
+        else:
+            self._ok(self.lib.go_eval_costs(L, ne, g, A, E, cands, Cn, alpha, beta, D, cut, obj, C.byref(am)),
+                     "eval_costs")
         return D, cut, obj, am.value
 
     def eval_cost_dense(self, A, W, g, assign, alpha=1.0, beta=1.0):

@@ -58,6 +58,14 @@ SIGNATURES = [
     ("gimbal_window_place_async", C.c_int, [_P, _P, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P]),
     ("gimbal_stats_set_count_sms", C.c_int, [_P, C.c_int]),
     ("gimbal_pass_async", C.c_int, [_P, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P, _P, _P]),
+    ("gimbal_dist_unique_id", C.c_int, [_P]),
+    ("gimbal_dist_comm_init", C.c_int, [_i32, _i32, _P, C.c_int, C.POINTER(_P)]),
+    ("gimbal_dist_comm_destroy", C.c_int, [_P]),
+    ("gimbal_dist_comm_size", C.c_int, [_P, C.POINTER(_i32), C.POINTER(_i32)]),
+    ("gimbal_stats_allreduce", C.c_int, [_P, _P, _i64]),
+    ("gimbal_dist_merge_argmin", C.c_int, [_P, _P, _P, _i64, _i64, _i64, _P, _P]),
+    ("gimbal_pass_distributed_async", C.c_int, [_P, _P, _d, _i32, _i32, _i32, _P, _i64, _i64, _i64, _d, _d, _P, _P, _P,
+                                                _P, _P, _P, _P]),
     ("gimbal_eval_cost_dense", C.c_int, [_i32, _i32, _P, _P, _i32, _d, _d, _P, C.POINTER(_d), C.POINTER(_d),
                                          C.POINTER(_d)]),
     ("gimbal_affinity_set_dense", C.c_int, [_TP, _P, _i32, _d, _i32, _i32, _i32, _P, C.POINTER(_i32)]),

@@ -100,10 +100,15 @@ struct gimbal_stats_s {
   uint32_t* dflags = nullptr;
   int64_t tokens = 0;
   bool derived = true;
-  // evaluator choice cached per count state (counts only change through add/reset/reduce,
-  // each of which changes `tokens` or resets max_tokens)
-  int64_t max_tokens = -1;
+  // evaluator cell width (pick_cell_width): bounded on the host from the token count, else decided
+  // on the device from a max-cell probe that is re-run only when the counts changed
+  int64_t count_version = 0;     // bumped by every reset / add / merge / reduction
+  int64_t probed_version = -1;   // count state the device probe (`probe`) was taken on
   bool small_cells = false;
+  const unsigned long long* width_guard = nullptr;
+  // after an all-reduce without a known global total the token count lives on the device only
+  // (as sum_j A(0, j) / k); gimbal_stats_tokens reads it back on demand
+  bool tokens_on_device = false;
   // host-ingest staging (double-buffered)
   static constexpr int kStages = 2;
   size_t stage_bytes = 0;
@@ -146,7 +151,7 @@ struct gimbal_stats_s {
     return GIMBAL_OK;
   }
   // scratch
-  DevBuf cand, same, dout, keys, misc, ints, probe;
+  DevBuf cand, same, dout, keys, misc, ints, probe, dscr;
   // side stream of gimbal_pass_async: the greedy walk runs there beside the candidate scoring
   cudaStream_t g_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -179,6 +184,21 @@ struct gimbal_stats_s {
     if (w_derived) return GIMBAL_OK;
     if (topo.n_layers > 1) GIMBAL_CUDA_TRY(launch_derive_w(topo.n_layers, topo.n_experts, dE, dW, stream));
     w_derived = true;
+    return GIMBAL_OK;
+  }
+
+  // Host token count after an all-reduce that left it on the device: every token adds k
+  // activations to layer 0, so tokens = sum_j A(0, j) / k (one small read-back, synchronising).
+  int resolve_tokens() {
+    if (!tokens_on_device) return GIMBAL_OK;
+    GIMBAL_TRY(derive());
+    std::vector<unsigned long long> a0((size_t)topo.n_experts);
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(a0.data(), dA, a0.size() * 8, cudaMemcpyDeviceToHost, stream));
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(stream));
+    unsigned long long s = 0;
+    for (unsigned long long v : a0) s += v;
+    tokens = (int64_t)(s / (unsigned long long)topo.top_k);
+    tokens_on_device = false;
     return GIMBAL_OK;
   }
 
@@ -460,7 +480,7 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
     }
     if (h->g_stream) cudaStreamSynchronize(h->g_stream);
-    for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints, &h->probe}) b->release();
+    for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints, &h->probe, &h->dscr}) b->release();
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->t_stream) cudaStreamSynchronize(h->t_stream);
@@ -494,7 +514,8 @@ int gimbal_stats_reset(gimbal_stats_t h) {
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dW, 0, nW * 8, h->stream));
   GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags, 0, 4, h->stream));  // word 1 (deferred) survives
   h->tokens = 0;
-  h->max_tokens = -1;
+  h->tokens_on_device = false;
+  ++h->count_version;
   h->set_derived(true);
   return GIMBAL_OK;
 }
@@ -507,6 +528,10 @@ int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int
   if (n_tokens == 0) return GIMBAL_OK;
   if (!ids) return invalid("add_token: null ids");
   std::lock_guard<std::mutex> lk(h->mu);
+  {
+    DeviceGuard g(h->device);
+    GIMBAL_TRY(h->resolve_tokens());
+  }
   DeviceGuard g(h->device);
   if (mem == GIMBAL_MEM_DEVICE) {
     GIMBAL_TRY(h->count_device(ids, id_bytes, n_tokens));
@@ -514,6 +539,7 @@ int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int
     GIMBAL_TRY(h->count_host(ids, id_bytes, n_tokens));
   }
   h->tokens += n_tokens;
+  ++h->count_version;
   h->set_derived(false);
   return GIMBAL_OK;
 }
@@ -521,6 +547,9 @@ int gimbal_stats_add_tokens(gimbal_stats_t h, const void* ids, int id_bytes, int
 int gimbal_stats_tokens(gimbal_stats_t h, int64_t* tokens) {
   GIMBAL_TRY(check_handle(h));
   if (!tokens) return invalid("null tokens");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->resolve_tokens());
   *tokens = h->tokens;
   return GIMBAL_OK;
 }
@@ -626,6 +655,7 @@ int gimbal_stats_merge(gimbal_stats_t h, const uint64_t* counts, int64_t tokens,
   if (!counts) return invalid("merge: null counts");
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
+  GIMBAL_TRY(h->resolve_tokens());
   const bool pairs = h->topo.n_layers > 1;
   const int64_t n = pairs ? h->nE() : h->m();
   unsigned long long* dst = pairs ? h->dE : h->dA;
@@ -640,8 +670,8 @@ int gimbal_stats_merge(gimbal_stats_t h, const uint64_t* counts, int64_t tokens,
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
   tmp.release();
   h->tokens += tokens;
+  ++h->count_version;
   h->set_derived(!pairs);
-  h->max_tokens = -1;
   return GIMBAL_OK;
 }
 
@@ -650,7 +680,8 @@ int gimbal_stats_mark_reduced(gimbal_stats_t h, int64_t global_tokens) {
   if (global_tokens < 0) return invalid("mark_reduced: negative token count");
   std::lock_guard<std::mutex> lk(h->mu);
   h->tokens = global_tokens;
-  h->max_tokens = -1;
+  h->tokens_on_device = false;
+  ++h->count_version;
   h->set_derived(h->topo.n_layers < 2);
   return GIMBAL_OK;
 }
@@ -669,36 +700,31 @@ int enqueue_eval(gimbal_stats_t h, const uint8_t* dc, int64_t C, double alpha, d
   GIMBAL_TRY(pick_cell_width(h));
   GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
                                     h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
-                                    flags, h->small_cells, h->stream));
-  const unsigned long long total =
-      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)k * k;
-  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
+                                    flags, h->small_cells, h->width_guard, h->stream));
+  GIMBAL_CUDA_TRY(launch_eval_finish(C, L, ne, k, h->dA, alpha, beta, h->same.as<unsigned long long>(), dD, dcut,
                                      dobj, darg, flags, h->stream));
   return GIMBAL_OK;
 }
 
-// E cells < 2^27 lets the evaluators keep 32-bit partial sums / four byte planes: decided from the
-// token count alone when tokens * k^2 < 2^27, else by reading the largest cell back once per count
-// state (a host synchronisation).
+// E cells < 2^27 lets the evaluators keep 32-bit partial sums / four byte planes.  Decided on the
+// host when the token count bounds every cell (a token adds at most k^2 to a cell); otherwise a
+// max-cell probe is queued (once per count state) and the evaluators pick their form on the
+// device (WidthGuard), so a pass never waits on the host.
 int pick_cell_width(gimbal_stats_t h) {
   const int k = h->topo.top_k;
-  if (h->max_tokens != h->tokens &&
-      (unsigned long long)h->tokens * (unsigned long long)(k * k) < (1ull << 27)) {
-    // every cell is at most tokens * k^2 (a token pairs each of its k slots with each of the next
-    // layer's k): small enough for 32-bit partial sums without looking
+  if (!h->tokens_on_device && (unsigned long long)h->tokens * (unsigned long long)(k * k) < (1ull << 27)) {
     h->small_cells = true;
-    h->max_tokens = h->tokens;
+    h->width_guard = nullptr;
+    return GIMBAL_OK;
   }
-  if (h->max_tokens != h->tokens) {
-    // cells < 2^27 lets the evaluator keep 32-bit partial sums (one host sync per new count state)
-    unsigned long long mx = 0;
+  if (h->probed_version != h->count_version) {
     GIMBAL_TRY(h->probe.ensure(64));  // not `misc`: it may hold a queued pass's member bits
-    GIMBAL_CUDA_TRY(launch_max_cell(h->dE, h->nE(), h->probe.as<unsigned long long>(), h->stream));
-    GIMBAL_CUDA_TRY(cudaMemcpyAsync(&mx, h->probe.p, 8, cudaMemcpyDeviceToHost, h->stream));
-    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    h->small_cells = mx < (1ull << 27);
-    h->max_tokens = h->tokens;
+    GIMBAL_CUDA_TRY(launch_max_cell(h->dE, h->topo.n_layers > 1 ? h->nE() : 0, h->probe.as<unsigned long long>(),
+                                    h->stream));
+    h->probed_version = h->count_version;
   }
+  h->small_cells = true;
+  h->width_guard = h->probe.as<unsigned long long>();
   return GIMBAL_OK;
 }
 
@@ -1011,16 +1037,67 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   uint32_t* flags = h->dflags + 1;
   GIMBAL_CUDA_TRY(launch_eval_prepare(C, same, h->stream));
   GIMBAL_CUDA_TRY(launch_eval_range(L, ne, g, h->dA, h->dE, candidates + m, C - 1, 1, same + 1, scores + 1, flags,
-                                    bad, h->small_cells, h->stream));
+                                    bad, h->small_cells, h->width_guard, h->stream));
   GIMBAL_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_join, 0));
   GIMBAL_CUDA_TRY(launch_eval_range(L, ne, g, h->dA, h->dE, candidates, 1, 0, same, scores, flags, bad,
-                                    h->small_cells, h->stream));
-  const unsigned long long total =
-      (unsigned long long)h->tokens * (unsigned long long)(L - 1) * (unsigned long long)h->topo.top_k * h->topo.top_k;
-  GIMBAL_CUDA_TRY(launch_eval_finish(C, total, alpha, beta, same, scores, scores + C, scores + 2 * C,
+                                    h->small_cells, h->width_guard, h->stream));
+  GIMBAL_CUDA_TRY(launch_eval_finish(C, L, ne, h->topo.top_k, h->dA, alpha, beta, same, scores, scores + C,
+                                     scores + 2 * C,
                                      reinterpret_cast<long long*>(argmin), flags, h->stream));
   if (flags_out) GIMBAL_CUDA_TRY(cudaMemcpyAsync(flags_out, h->dflags, 8, cudaMemcpyDeviceToDevice, h->stream));
   return GIMBAL_OK;
+}
+
+int gimbal_stats_allreduce(gimbal_stats_t h, gimbal_comm_t comm, int64_t global_tokens) {
+  GIMBAL_TRY(check_handle(h));
+  if (!comm) return invalid("gimbal_stats_allreduce: null communicator");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  const bool pairs = h->topo.n_layers > 1;
+  // the counted buffer (A is re-derived from the reduced E on use)
+  GIMBAL_TRY(nccl_allreduce_u64_sum(pairs ? h->dE : h->dA, (size_t)(pairs ? h->nE() : h->m()), comm, h->stream));
+  if (global_tokens >= 0) {
+    h->tokens = global_tokens;
+    h->tokens_on_device = false;
+  } else {
+    h->tokens_on_device = true;
+  }
+  ++h->count_version;
+  h->set_derived(!pairs);
+  return GIMBAL_OK;
+}
+
+int gimbal_dist_merge_argmin(gimbal_stats_t h, gimbal_comm_t comm, const double* objectives, int64_t n_local,
+                             int64_t offset, int64_t n_total, double* global, int64_t* argmin) {
+  GIMBAL_TRY(check_handle(h));
+  if (!comm || !global || !argmin || (n_local > 0 && !objectives)) return invalid("merge_argmin: null argument");
+  if (n_local < 0 || offset < 0 || n_total < 1 || offset + n_local > n_total)
+    return invalid("merge_argmin: slice outside [0, n_total)");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  return nccl_merge_argmin(objectives, n_local, offset, global, n_total, reinterpret_cast<long long*>(argmin), comm,
+                           h->stream);
+}
+
+int gimbal_pass_distributed_async(gimbal_stats_t h, gimbal_comm_t comm, double threshold, int32_t top_e,
+                                  int32_t capacity, int32_t anchor, uint8_t* candidates, int64_t n_local,
+                                  int64_t cand_offset, int64_t n_total, double alpha, double beta, double* scores,
+                                  double* global, int64_t* argmin, int32_t* placement, int32_t* members,
+                                  int32_t* n_members, uint32_t* flags_out) {
+  GIMBAL_TRY(check_handle(h));
+  if (n_local < 0 || cand_offset < 0 || n_total < 1 || cand_offset + n_local > n_total)
+    return invalid("pass_distributed: candidate slice outside [0, n_total)");
+  if (!global || !argmin || !scores || !candidates) return invalid("pass_distributed: null argument");
+  const int64_t lead = (cand_offset == 0 && n_local > 0) ? 0 : 1;
+  const int64_t rows = n_local + lead;
+  GIMBAL_TRY(gimbal_stats_allreduce(h, comm, -1));
+  {
+    std::lock_guard<std::mutex> lk(h->mu);
+    GIMBAL_TRY(h->dscr.ensure(64));
+  }
+  GIMBAL_TRY(gimbal_pass_async(h, threshold, top_e, capacity, anchor, candidates, rows, alpha, beta, scores,
+                               reinterpret_cast<int64_t*>(h->dscr.p), placement, members, n_members, flags_out));
+  return gimbal_dist_merge_argmin(h, comm, scores + 2 * rows + lead, n_local, cand_offset, n_total, global, argmin);
 }
 
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms) {

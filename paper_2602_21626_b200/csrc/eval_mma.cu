@@ -140,8 +140,9 @@ __device__ __forceinline__ void build_onehot(uint8_t* B, const uint8_t* ids, int
 template <int G, bool ST>
 __global__ void __launch_bounds__(kThreads, 1)
     eval_mma_kernel(EvalMmaParams prm, const unsigned long long* __restrict__ E, const uint8_t* __restrict__ cands,
-                    unsigned long long* __restrict__ same) {
+                    unsigned long long* __restrict__ same, WidthGuard guard) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  if (width_skip(guard)) return;  // a cell >= 2^27: the generic evaluator runs instead
   __shared__ uint64_t mma_done[kBStages], tmem_free[kBStages], b_full[kBStages], id_full[kIdSlots];
   __shared__ uint32_t tmem_slot;
   // stacked (n_e = 64, ST): A rows [0, 64) = E_l, [64, 128) = E_l+1, each half of the N = 64
@@ -400,7 +401,7 @@ size_t eval_mma_smem(int ne, int g) {
 
 // same[c] += sum over pairs of the same-GPU weight (same[] zeroed by the caller); E cells < 2^27.
 cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, const uint8_t* cands, int64_t C,
-                            unsigned long long* same, cudaStream_t s) {
+                            unsigned long long* same, WidthGuard guard, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -429,7 +430,7 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kThreads, smem, s>>>(prm, E, cands, same);
+    kern<<<grid, kThreads, smem, s>>>(prm, E, cands, same, guard);
     return cudaGetLastError();
   };
   switch (g * 2 + (st ? 1 : 0)) {

@@ -44,6 +44,12 @@ enum KernelFlag : uint32_t {
     if (s_ != GIMBAL_OK) return s_; \
   } while (0)
 
+// NCCL (dist.cu, resolved at run time): in-place u64 SUM all-reduce; objectives scatter + MIN
+// all-reduce + argmin (lowest index).  `comm` is an ncclComm_t.
+int nccl_allreduce_u64_sum(unsigned long long* buf, size_t n, void* comm, cudaStream_t s);
+int nccl_merge_argmin(const double* local, int64_t n_local, int64_t offset, double* global, int64_t n_total,
+                      long long* argmin, void* comm, cudaStream_t s);
+
 // Experiment knobs (alternate kernels for A/B timing and engine-specific tests).  Compiled in only
 // for the test/tool build lib/libgimbal_gpu_ab.so (-DGIMBAL_AB_KNOBS); in the shipped
 // libgimbal_gpu.so every knob reads as unset, so the kernel choice depends on the inputs alone.
@@ -156,21 +162,39 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
                               const unsigned long long* E, const uint8_t* cands, int64_t C,
                               double alpha, double beta, unsigned long long* scratch_same,
                               double* D, double* cut, double* obj, long long* argmin,
-                              uint32_t* flags, bool small_cells, cudaStream_t s);
+                              uint32_t* flags, bool small_cells, const unsigned long long* device_max_cell,
+                              cudaStream_t s);
 size_t eval_scratch_bytes(int64_t C);
 // max over E cells (for choosing 32-bit partial sums in the evaluator)
 cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s);
 
+// Which evaluator kernels may run: the u32-partial-sum / byte-plane forms need every E cell
+// < 2^27.  When the host can bound the cells (tokens * k^2 < 2^27, or a known max) it launches one
+// form; otherwise (`max_cell` != nullptr: written on the device by launch_max_cell just before) both
+// forms are launched and each returns at once unless the device max matches its `want_small`, so
+// the choice needs no host synchronisation.
+struct WidthGuard {
+  const unsigned long long* max_cell = nullptr;
+  int want_small = 0;
+};
+__device__ __forceinline__ bool width_skip(const WidthGuard& g) {
+  return g.max_cell != nullptr && ((*g.max_cell < (1ull << 27)) != (g.want_small != 0));
+}
+
 // tensor-core same-GPU weights (eval_mma.cu): n_e in {128, 256}, g in {4, 8, 16}, cells < 2^27
 bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C);
 cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, const uint8_t* cands, int64_t C,
-                            unsigned long long* same, cudaStream_t s);
+                            unsigned long long* same, WidthGuard guard, cudaStream_t s);
 cudaError_t launch_eval_prepare(int64_t C, unsigned long long* scratch_same, cudaStream_t s);
 cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A, const unsigned long long* E,
                               const uint8_t* cands, int64_t C, int64_t base, unsigned long long* same, double* D,
-                              uint32_t* flags, long long* bad_index, bool small_cells, cudaStream_t s);
-cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
-                               const unsigned long long* same, const double* D, double* cut,
+                              uint32_t* flags, long long* bad_index, bool small_cells,
+                              const unsigned long long* device_max_cell, cudaStream_t s);
+// cut = total - same with total = sum_l sum E_l = (L-1) * k * sum_j A(0, j) (every token adds k^2
+// pairings per layer pair and k activations per layer), read from the device A, so scoring needs
+// no host-side token count (after an all-reduce it is only known on the device).
+cudaError_t launch_eval_finish(int64_t C, int L, int ne, int k, const unsigned long long* A, double alpha,
+                               double beta, const unsigned long long* same, const double* D, double* cut,
                                double* obj, long long* argmin, uint32_t* flags, cudaStream_t s);
 
 cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E, double threshold,

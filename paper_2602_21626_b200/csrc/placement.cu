@@ -40,8 +40,9 @@ constexpr int kSortLocal = 2048;  // keys per CTA in the shared-memory sort / to
 __global__ void __launch_bounds__(kEvalThreads)
     eval_same_kernel(int L, int ne, const unsigned long long* __restrict__ E,
                      const uint8_t* __restrict__ cands, int64_t C, int64_t m,
-                     unsigned long long* __restrict__ same) {
+                     unsigned long long* __restrict__ same, WidthGuard guard) {
   extern __shared__ uint8_t sm[];
+  if (width_skip(guard)) return;
   const int64_t nE = (int64_t)(L - 1) * ne * ne;
   const int64_t cell0 = (int64_t)blockIdx.x * kEvalCellsPerCta;
   const int64_t row_lo = cell0 / ne;
@@ -107,8 +108,9 @@ __global__ void __launch_bounds__(kEvalThreads)
 __global__ void __launch_bounds__(kEvalThreads)
     eval_same_fast_kernel(int L, int ne, const unsigned long long* __restrict__ E,
                           const uint8_t* __restrict__ cands, int64_t C, int64_t m,
-                          unsigned long long* __restrict__ same) {
+                          unsigned long long* __restrict__ same, WidthGuard guard) {
   extern __shared__ __align__(16) uint8_t sm[];
+  if (width_skip(guard)) return;
   const int rows_per_cta = kEvalCellsPerCta / ne;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;          // first flat row of this CTA
   const int64_t n_rows = (int64_t)(L - 1) * ne;
@@ -335,13 +337,25 @@ __global__ void __launch_bounds__(256)
 }
 
 // cut/objective per candidate, then the argmin (lowest index among minima) in one CTA.
-__global__ void eval_finish_kernel(int64_t C, unsigned long long total, double alpha, double beta,
-                                   const unsigned long long* __restrict__ same,
+__global__ void eval_finish_kernel(int64_t C, int L, int ne, int k, const unsigned long long* __restrict__ A,
+                                   double alpha, double beta, const unsigned long long* __restrict__ same,
                                    const double* __restrict__ D, double* __restrict__ cut,
                                    double* __restrict__ obj, long long* __restrict__ argmin,
                                    uint32_t* __restrict__ flags) {
   __shared__ double bv[1024];
   __shared__ long long bi[1024];
+  __shared__ unsigned long long tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  if (L > 1) {  // total pair weight: (L-1) * k * (tokens * k) with tokens * k = sum_j A(0, j)
+    unsigned long long a = 0;
+    for (int j = threadIdx.x; j < ne; j += blockDim.x) a += A[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0 && a) atomicAdd(&tot, a);
+  }
+  __syncthreads();
+  const unsigned long long total = tot * (unsigned long long)(L - 1) * (unsigned long long)k;
   double best = 0.0;
   long long besti = -1;
   for (int64_t c = threadIdx.x; c < C; c += blockDim.x) {
@@ -682,11 +696,17 @@ cudaError_t launch_eval_prepare(int64_t C, unsigned long long* scratch_same, cud
 // range); bad_index / flags are shared by all ranges of one batch.
 cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A, const unsigned long long* E,
                               const uint8_t* cands, int64_t C, int64_t base, unsigned long long* same, double* D,
-                              uint32_t* flags, long long* bad_index, bool small_cells, cudaStream_t s) {
+                              uint32_t* flags, long long* bad_index, bool small_cells,
+                              const unsigned long long* device_max_cell, cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
   const int64_t m = (int64_t)L * ne;
   cudaError_t e = cudaSuccess;
-  if (small_cells && L > 1 && L <= 256 && (L - 1) * ne * ne * 4 <= 32 * 1024 && !GIMBAL_KNOB("GIMBAL_EVAL_NO_SMALL")) {
+  // width decided on the device: the small-cell form and the generic form both launch, guarded
+  const bool guarded = device_max_cell != nullptr;
+  if (guarded) small_cells = true;
+  const WidthGuard g_small{device_max_cell, 1}, g_any{device_max_cell, 0};
+  bool small_ran = false;
+  if (!guarded && small_cells && L > 1 && L <= 256 && (L - 1) * ne * ne * 4 <= 32 * 1024 && !GIMBAL_KNOB("GIMBAL_EVAL_NO_SMALL")) {
     auto kern = ne == 8 && g == 8   ? eval_small_kernel<8, 8>
               : ne == 8 && g == 4   ? eval_small_kernel<8, 4>
               : ne == 8 && g == 2   ? eval_small_kernel<8, 2>
@@ -707,8 +727,9 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
   // greedy row scored after the overlapped walk) is cheaper on the integer path, which reads E once
   // instead of building every unit's byte planes (DS-V3: 8.5 us vs 0.12 ms for the one row)
   if (small_cells && eval_mma_supported(L, ne, g, cands, C) && !(C <= 8 && ne % 32 == 0 && 256 % ne == 0)) {
-    e = launch_eval_mma(L, ne, g, E, cands, C, same, s);
+    e = launch_eval_mma(L, ne, g, E, cands, C, same, g_small, s);
     if (e != cudaSuccess) return e;
+    small_ran = true;
   } else if (L > 1 && fast) {
     const int64_t rows = (int64_t)(L - 1) * ne;
     const int rows_per_cta = kEvalCellsPerCta / ne;
@@ -718,10 +739,12 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
     e = cudaFuncSetAttribute(eval_same_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     eval_same_fast_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
-        L, ne, E, cands, C, m, same);
+        L, ne, E, cands, C, m, same, g_small);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-  } else if (L > 1) {
+    small_ran = true;
+  }
+  if (L > 1 && (!small_ran || guarded)) {  // any cell width (guarded: only when a cell >= 2^27)
     const int64_t nE = (int64_t)(L - 1) * ne * ne;
     const int64_t ctas = (nE + kEvalCellsPerCta - 1) / kEvalCellsPerCta;
     // staged span per candidate: rows of this CTA plus the next layer
@@ -731,7 +754,7 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
     e = cudaFuncSetAttribute(eval_same_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     eval_same_kernel<<<dim3((unsigned)ctas, candidate_splits(ctas, C)), kEvalThreads, smem, s>>>(
-        L, ne, E, cands, C, m, same);
+        L, ne, E, cands, C, m, same, small_ran ? g_any : WidthGuard{});
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -751,12 +774,13 @@ cudaError_t launch_eval_costs(int L, int ne, int g, const unsigned long long* A,
                               const unsigned long long* E, const uint8_t* cands, int64_t C,
                               double alpha, double beta, unsigned long long* scratch_same,
                               double* D, double* cut, double* obj, long long* argmin,
-                              uint32_t* flags, bool small_cells, cudaStream_t s) {
+                              uint32_t* flags, bool small_cells, const unsigned long long* device_max_cell,
+                              cudaStream_t s) {
   if (C <= 0) return cudaSuccess;
   cudaError_t e = launch_eval_prepare(C, scratch_same, s);
   if (e != cudaSuccess) return e;
   return launch_eval_range(L, ne, g, A, E, cands, C, 0, scratch_same, D, flags,
-                           reinterpret_cast<long long*>(scratch_same + C), small_cells, s);
+                           reinterpret_cast<long long*>(scratch_same + C), small_cells, device_max_cell, s);
 }
 
 cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned long long* out, cudaStream_t s) {
@@ -768,10 +792,10 @@ cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned lon
   return cudaGetLastError();
 }
 
-cudaError_t launch_eval_finish(int64_t C, unsigned long long total, double alpha, double beta,
-                               const unsigned long long* same, const double* D, double* cut,
+cudaError_t launch_eval_finish(int64_t C, int L, int ne, int k, const unsigned long long* A, double alpha,
+                               double beta, const unsigned long long* same, const double* D, double* cut,
                                double* obj, long long* argmin, uint32_t* flags, cudaStream_t s) {
-  eval_finish_kernel<<<1, 1024, 0, s>>>(C, total, alpha, beta, same, D, cut, obj, argmin, flags);
+  eval_finish_kernel<<<1, 1024, 0, s>>>(C, L, ne, k, A, alpha, beta, same, D, cut, obj, argmin, flags);
   return cudaGetLastError();
 }
 

@@ -44,11 +44,34 @@ class _CudaArray:
                                          "strides": None}
 
 
-def allreduce_counts(stats: RoutingStats, group=None) -> None:
-    """In-place SUM all-reduce of the handle's counted buffer over the process group."""
+def nccl_comm(group=None, device: int = 0):
+    """The ncclComm_t (as an int) behind a torch NCCL process group, for the library's own
+    collectives (gimbal_stats_allreduce, gimbal_pass_distributed_async); None when the group is
+    not NCCL or torch does not expose it."""
     import torch
     import torch.distributed as dist
 
+    if dist.get_backend(group) != "nccl":
+        return None
+    try:
+        pg = group if group is not None else dist.distributed_c10d._get_default_group()
+        ptr = pg._get_backend(torch.device("cuda", device))._comm_ptr()
+        return int(ptr) or None
+    except Exception:  # noqa: BLE001 - older torch / lazily initialised communicator
+        return None
+
+
+def allreduce_counts(stats: RoutingStats, group=None) -> None:
+    """In-place SUM all-reduce of the handle's counted buffer over the process group.  NCCL: the
+    library's gimbal_stats_allreduce on the group's communicator, queued on the handle's stream
+    (no host round trip); other backends: through host memory."""
+    import torch
+    import torch.distributed as dist
+
+    comm = nccl_comm(group, stats.device)
+    if comm is not None:
+        N.check(N.lib().gimbal_stats_allreduce(stats.handle, C.c_void_p(comm), -1), "allreduce")
+        return
     topo = stats.topo
     e_ptr, a_ptr, _ = stats.device_buffers()
     if topo.n_layers > 1:
@@ -114,6 +137,36 @@ class HotPath:
         out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
         return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
 
+    def _ensure_pk(self) -> None:
+        import torch
+
+        m = self.topo.total_experts()
+        if getattr(self, "_pk", None) is None:
+            dev = torch.device("cuda", self.device)
+            # int32 words: [0:2] argmin (int64), [2] |M|, [3] pad, [4:6] error flags, [6:6+m] M,
+            # [6+m:6+2m] greedy
+            self._pk = torch.zeros(6 + 2 * m, dtype=torch.int32, device=dev)
+            self._pk_host = torch.empty(6 + 2 * m, dtype=torch.int32).pin_memory()
+            self._hstream = torch.cuda.ExternalStream(self.stats.device_buffers()[2], device=dev)
+
+    def _read_pk(self, extra=None):
+        """One read-back of the packed results (plus an optional (device, pinned host) pair) behind
+        the handle's stream, one sync; raises a deferred device-side error."""
+        import torch
+
+        # the read-back runs on torch's stream behind the handle's (a pinned block used on the
+        # handle's own stream would outlive it in torch's host allocator)
+        cur = torch.cuda.current_stream(torch.device("cuda", self.device))
+        cur.wait_stream(self._hstream)
+        self._pk_host.copy_(self._pk, non_blocking=True)
+        if extra is not None:
+            extra[1].copy_(extra[0], non_blocking=True)
+        cur.synchronize()
+        h = self._pk_host.numpy()
+        if h[4] or h[5]:
+            self.stats.sync()  # raises (and clears) the deferred device-side error
+        return h
+
     def _place_queued(self, candidates) -> HotPathResult:
         """place() as one queued device chain (gimbal_pass_async: strong-pair set, greedy, scores,
         argmin), then a single read-back of [argmin | |M| | M | greedy] and one stream sync."""
@@ -121,13 +174,7 @@ class HotPath:
 
         topo = self.topo
         m, C_ = topo.total_experts(), int(candidates.shape[0])
-        dev = torch.device("cuda", self.device)
-        if getattr(self, "_pk", None) is None:
-            # int32 words: [0:2] argmin (int64), [2] |M|, [3] pad, [4:6] error flags, [6:6+m] M,
-            # [6+m:6+2m] greedy
-            self._pk = torch.zeros(6 + 2 * m, dtype=torch.int32, device=dev)
-            self._pk_host = torch.empty(6 + 2 * m, dtype=torch.int32).pin_memory()
-            self._hstream = torch.cuda.ExternalStream(self.stats.device_buffers()[2], device=dev)
+        self._ensure_pk()
         scores = self._scores(C_)
         self.stats._after_torch(candidates)
         base = self._pk.data_ptr()
@@ -136,15 +183,7 @@ class HotPath:
             C.c_void_p(candidates.data_ptr()), C_, self.alpha, self.beta, C.c_void_p(scores.data_ptr()),
             C.c_void_p(base), C.c_void_p(base + 24 + 4 * m), C.c_void_p(base + 24), C.c_void_p(base + 8),
             C.c_void_p(base + 16)), "pass")
-        # the read-back runs on torch's stream behind the handle's (a pinned block used on the
-        # handle's own stream would outlive it in torch's host allocator)
-        cur = torch.cuda.current_stream(dev)
-        cur.wait_stream(self._hstream)
-        self._pk_host.copy_(self._pk, non_blocking=True)
-        cur.synchronize()
-        h = self._pk_host.numpy()
-        if h[4] or h[5]:
-            self.stats.sync()  # raises (and clears) the deferred device-side error
+        h = self._read_pk()
         n = int(h[2])
         return HotPathResult(affinity=AffinitySet(experts=h[6:6 + n].tolist(), anchor_gpu=self.anchor_gpu),
                              greedy=h[6 + m:6 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
@@ -300,6 +339,7 @@ class HotPath:
         Mi = np.ascontiguousarray(np.asarray(M.experts, np.int32))
         lib = N.lib()
         topo = self.topo
+        comm = nccl_comm(group, self.device)
         n_cells = (topo.n_layers - 1) * topo.n_experts * topo.n_experts if topo.n_layers > 1 else m
         try:
             pair[0].stats.reset()
@@ -310,11 +350,15 @@ class HotPath:
                     nxt = pair[(i + 1) % 2]
                     nxt.stats.reset()
                     nxt.stats.add_tokens(windows[i + 1])
-                e_ptr, a_ptr, _ = cur.stats.device_buffers()
-                view = torch.as_tensor(_CudaArray(e_ptr if topo.n_layers > 1 else a_ptr, n_cells), device=dev)
-                with torch.cuda.stream(ext):  # behind this window's counting, ahead of its placement
-                    dist.all_reduce(view, op=dist.ReduceOp.SUM, group=group)
-                cur.stats.mark_reduced(int(glob[i]))
+                if comm is not None:  # the library's NCCL SUM on the handle's stream
+                    N.check(lib.gimbal_stats_allreduce(cur.stats.handle, C.c_void_p(comm), int(glob[i])),
+                            "allreduce")
+                else:
+                    e_ptr, a_ptr, _ = cur.stats.device_buffers()
+                    view = torch.as_tensor(_CudaArray(e_ptr if topo.n_layers > 1 else a_ptr, n_cells), device=dev)
+                    with torch.cuda.stream(ext):  # behind this window's counting, ahead of its placement
+                        dist.all_reduce(view, op=dist.ReduceOp.SUM, group=group)
+                    cur.stats.mark_reduced(int(glob[i]))
                 if rows:
                     N.check(lib.gimbal_window_place_async(
                         cur.stats.handle, Mi.ctypes.data if Mi.size else None, Mi.size, M.anchor_gpu,
@@ -365,43 +409,68 @@ class HotPath:
         """This rank's token shard and candidate slice; returns the global argmin."""
         return self._distributed_pass(trace_shard, candidates_shard, cand_offset, n_candidates, group, None)
 
+    def _distributed_queued(self, trace_shard, candidates_shard, cand_offset: int, n_candidates: int, comm):
+        """One rank's pass as one queued device chain (gimbal_pass_distributed_async): count the shard,
+        NCCL SUM of the counts, strong-pair set, greedy, scores of this slice, NCCL MIN merge of the
+        objectives and the global argmin; then one read-back and one sync."""
+        import torch
+
+        topo = self.topo
+        m = topo.total_experts()
+        dev = torch.device("cuda", self.device)
+        n_local = int(candidates_shard.shape[0])
+        lead = 0 if (cand_offset == 0 and n_local > 0) else 1
+        if lead:
+            if getattr(self, "_dcands", None) is None or tuple(self._dcands.shape) != (n_local + 1, m):
+                self._dcands = torch.zeros((n_local + 1, m), dtype=torch.uint8, device=dev)
+            if n_local:
+                self._dcands[1:].copy_(candidates_shard)
+            buf = self._dcands
+        else:
+            buf = candidates_shard
+        rows = n_local + lead
+        scores = self._scores(rows)
+        if getattr(self, "_gobj", None) is None or self._gobj.numel() != n_candidates:
+            self._gobj = torch.empty(n_candidates, dtype=torch.float64, device=dev)
+            self._gobj_host = torch.empty(n_candidates, dtype=torch.float64).pin_memory()
+        self._ensure_pk()
+        self.stats.reset()
+        self.stats.add_tokens(trace_shard)
+        self.stats._after_torch(buf)
+        base = self._pk.data_ptr()
+        N.check(N.lib().gimbal_pass_distributed_async(
+            self.stats.handle, C.c_void_p(comm), self.threshold, self.top_e, m // topo.n_gpus, self.anchor_gpu,
+            C.c_void_p(buf.data_ptr()), n_local, cand_offset, n_candidates, self.alpha, self.beta,
+            C.c_void_p(scores.data_ptr()), C.c_void_p(self._gobj.data_ptr()), C.c_void_p(base),
+            C.c_void_p(base + 24 + 4 * m), C.c_void_p(base + 24), C.c_void_p(base + 8), C.c_void_p(base + 16)),
+            "pass_distributed")
+        h = self._read_pk(extra=(self._gobj, self._gobj_host))
+        n = int(h[2])
+        objs = self._gobj_host.numpy()
+        am = int(h[0:2].view(np.int64)[0])
+        return HotPathResult(affinity=AffinitySet(experts=h[6:6 + n].tolist(), anchor_gpu=self.anchor_gpu),
+                             greedy=h[6 + m:6 + 2 * m].tolist(), argmin=am,
+                             objective=float(objs[am]) if am >= 0 else None)
+
     def _distributed_pass(self, trace_shard, candidates_shard, cand_offset: int, n_candidates: int,
                           group=None, M_fixed=None) -> HotPathResult:
         import torch
         import torch.distributed as dist
 
+        topo = self.topo
+        n_local = candidates_shard.shape[0]
+        comm = nccl_comm(group, self.device)
+        if (M_fixed is None and comm is not None and getattr(candidates_shard, "is_cuda", False)
+                and topo.n_gpus <= 255):
+            return self._distributed_queued(trace_shard, candidates_shard, cand_offset, n_candidates, comm)
         self.stats.reset()
         self.stats.add_tokens(trace_shard)
         allreduce_counts(self.stats, group)
-        topo = self.topo
-        n_local = candidates_shard.shape[0]
-        if (M_fixed is None and dist.get_backend(group) == "nccl" and getattr(candidates_shard, "is_cuda", False)
-                and topo.n_gpus <= 255):
-            # the queued pass (gimbal_pass_async) on this rank's slice; ranks other than the first
-            # score their slice behind a scratch row that receives the (identical) greedy placement
-            dev = torch.device("cuda", self.device)
-            lead = 0 if cand_offset == 0 else 1
-            if lead or n_local == 0:
-                m = topo.total_experts()
-                if getattr(self, "_dcands", None) is None or tuple(self._dcands.shape) != (n_local + 1, m):
-                    self._dcands = torch.zeros((n_local + 1, m), dtype=torch.uint8, device=dev)
-                if n_local:
-                    self._dcands[1:].copy_(candidates_shard)
-                buf, lead = self._dcands, 1
-            else:
-                buf = candidates_shard
-            res = self._place_queued(buf)
-            local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
-            if n_local:
-                local[cand_offset:cand_offset + n_local] = self._out[2, lead:lead + n_local]
-            dist.all_reduce(local, op=dist.ReduceOp.MIN, group=group)
-            objs = local.cpu().numpy()
-            return HotPathResult(affinity=res.affinity, greedy=res.greedy, argmin=merge_argmin(objs),
-                                 objective=float(objs.min()) if objs.size else None)
         M = M_fixed if M_fixed is not None else build_affinity_set(
             self.stats, topo, self.threshold, self.top_e, topo.total_experts() // topo.n_gpus, self.anchor_gpu)
+        # global candidate 0 is the greedy placement: written into the slice that holds it
         gp = greedy_place(self.stats, M, topo.n_gpus,
-                          out_u8_device=candidates_shard[0] if cand_offset == 0 else None)
+                          out_u8_device=candidates_shard[0] if (cand_offset == 0 and n_local > 0) else None)
         dev = torch.device("cuda", self.device)
         local = torch.full((n_candidates,), float("inf"), dtype=torch.float64, device=dev)
         if n_local:

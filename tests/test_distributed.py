@@ -1,7 +1,8 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): token sharding, the u64 SUM reduction of
 partial counts (as int64 all-reduce), candidate slicing and the global argmin merge, checked
-bit-exact against the single-process oracle.  The per-rank counts come from the oracle here;
-on B200 the same logic runs over libgimbal_gpu.so + NCCL (pipeline.run_distributed)."""
+bit-exact against the single-process oracle.  The per-rank counts come from the oracle here; the
+product's own run_distributed / stream_distributed run multi-rank on the GPU in
+tests/test_gpu_distributed.py (gloo, world 2-3, and NCCL through the C ABI)."""
 import os
 import socket
 

@@ -465,6 +465,11 @@ def test_bench_scale_properties(G):
     assert (A.sum(axis=1) == T * k).all()
     assert (E.reshape(L - 1, -1).sum(axis=1) == T * k * k).all()
     assert np.array_equal(W, E.sum(axis=0, dtype=np.uint64))
+    # A counted independently of our kernels (A is derived from E inside the library): torch's
+    # bincount over each layer's ids on the device
+    offs = (torch.arange(L, device=trace.device, dtype=torch.int64) * ne).view(1, L, 1)
+    tA = torch.bincount((trace.to(torch.int64) + offs).view(-1), minlength=L * ne).view(L, ne).cpu().numpy()
+    assert np.array_equal(A, tA.astype(np.uint64))
     assert (E.sum(axis=2) == A[:-1] * k).all() and (E[-1].sum(axis=0) == A[-1] * k).all()
     stream = G.RoutedStream(topo, T, trace)
     for assign in (G.static_placement(topo).assign, list(G.shuffled_candidates(L * ne, g, 5, 1)[0])):
