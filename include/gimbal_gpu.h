@@ -203,6 +203,28 @@ int gimbal_pass_distributed_async(gimbal_stats_t h, gimbal_comm_t comm, double t
                                   int32_t* placement_device, int32_t* members_device, int32_t* n_members_device,
                                   uint32_t* flags_device);
 
+/* ---- the online expert-layer hook: MoeHook::iteration_cost (sim.cpp:113-147) on the GPU ----
+ * Replaces the per-token host loop of MoeSubsystem (engine.hpp:56-68, called once per engine
+ * iteration from Engine::try_start_iteration, engine.cpp:149-152).  The routed ids of one batch
+ * are counted into a window statistics handle (RoutingStats::add_token semantics), and the
+ * layer x GPU load histogram under the current placement, the cross-GPU transitions
+ * (token_crossings, sim.cpp:183-198) and the bottleneck excess sum_l max(0, peak_l * g / (n * k) - 1)
+ * (sim.cpp:132-144, the reference's double arithmetic in layer order) come back per call; the
+ * per-GPU activation totals (gpu_activation_total_, report.expert_load) accumulate on the device.
+ * One CUDA graph per call (H2D ids, two kernels, 16-byte D2H). */
+typedef struct gimbal_online_s* gimbal_online_t;
+/* Per-iteration state counting into `window` (its device, stream and topology; n_e <= 256). */
+int gimbal_online_create(gimbal_stats_t window, gimbal_online_t* out);
+int gimbal_online_destroy(gimbal_online_t o);
+/* The placement the loads are measured under (m int32 GPU ids, host). */
+int gimbal_online_set_placement(gimbal_online_t o, const int32_t* assign, int64_t m);
+/* One iteration: n tokens of [n][L][k] ids (host; id_bytes 1 or 4).  Synchronises (the engine's
+ * iteration time depends on the result). */
+int gimbal_online_iteration(gimbal_online_t o, const void* ids, int id_bytes, int64_t n, double* excess_sum,
+                            int64_t* crossings);
+/* Activations per GPU over every iteration so far (g int64, host). */
+int gimbal_online_gpu_totals(gimbal_online_t o, int64_t* out);
+
 /* ---- the reference's general dense forms (PlacementProblem with arbitrary A / W) ---- */
 
 /* eval_cost (placement.cpp:58-85) on dense A [rows][m] and W [m][m] doubles (host). */

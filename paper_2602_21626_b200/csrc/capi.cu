@@ -1048,6 +1048,36 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   return GIMBAL_OK;
 }
 
+}  // extern "C"
+
+namespace gimbal_gpu {
+
+// Internals for the online hook (online.cu), which counts straight into a handle's tensors.
+StatsInternals stats_internals(gimbal_stats_t h) {
+  StatsInternals v;
+  v.dE = h->dE;
+  v.dA = h->dA;
+  v.dflags = h->dflags;
+  v.stream = h->stream;
+  v.device = h->device;
+  v.topo = h->topo;
+  v.mu = &h->mu;
+  return v;
+}
+
+// n tokens were counted into the handle's counted buffer behind its stream (caller holds mu)
+void stats_note_added(gimbal_stats_t h, int64_t n) {
+  h->tokens += n;
+  ++h->count_version;
+  h->set_derived(h->topo.n_layers < 2);
+}
+
+int stats_resolve_tokens(gimbal_stats_t h) { return h->resolve_tokens(); }
+
+}  // namespace gimbal_gpu
+
+extern "C" {
+
 int gimbal_stats_allreduce(gimbal_stats_t h, gimbal_comm_t comm, int64_t global_tokens) {
   GIMBAL_TRY(check_handle(h));
   if (!comm) return invalid("gimbal_stats_allreduce: null communicator");

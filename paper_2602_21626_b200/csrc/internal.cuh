@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include "gimbal_gpu.h"
@@ -43,6 +44,21 @@ enum KernelFlag : uint32_t {
     int s_ = (expr);                \
     if (s_ != GIMBAL_OK) return s_; \
   } while (0)
+
+// A stats handle's device tensors and stream (capi.cu), for kernels that count into it directly
+// (online.cu).  Callers hold *mu while queueing and call stats_note_added afterwards.
+struct StatsInternals {
+  unsigned long long* dE = nullptr;
+  unsigned long long* dA = nullptr;
+  uint32_t* dflags = nullptr;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  gimbal_topology topo{};
+  std::mutex* mu = nullptr;
+};
+StatsInternals stats_internals(gimbal_stats_t h);
+void stats_note_added(gimbal_stats_t h, int64_t n);
+int stats_resolve_tokens(gimbal_stats_t h);
 
 // NCCL (dist.cu, resolved at run time): in-place u64 SUM all-reduce; objectives scatter + MIN
 // all-reduce + argmin (lowest index).  `comm` is an ncclComm_t.

@@ -1,0 +1,368 @@
+// The online expert-layer hook on the GPU: MoeHook::iteration_cost (sim.cpp:113-147) and its
+// token_crossings (sim.cpp:183-198), one engine iteration at a time.
+//
+// Per iteration the routed ids of the batch ([n][L][k], packed to uint8 on the host) go to the
+// device in one copy, and two kernels do the whole per-token loop of the reference:
+//   online_count_kernel  every (token, layer) unit: the window statistics (all k x k pairings into
+//                        E, as RoutingStats::add_token, moe.cpp:169-191), the layer x GPU load
+//                        histogram under the current placement (layer_gpu_tokens_) and the
+//                        cross-GPU transitions (token_crossings);
+//   online_finish_kernel per-layer peaks, the bottleneck excess sum_l max(0, peak_l g / (n k) - 1)
+//                        in the reference's double arithmetic and layer order, the lifetime
+//                        per-GPU activation totals (gpu_activation_total_), and the reset of the
+//                        per-iteration accumulators.
+// The copy, both kernels and the 16-byte read-back of {excess_sum, crossings} are one CUDA graph
+// (node parameters updated per launch for the batch size); the host turns them into seconds with
+// the reference's own expression.  Statistics stay device-resident: the window handle is the
+// caller's gimbal_stats_t (its E/A feed maybe_relocate's greedy on the GPU).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace gimbal_gpu {
+
+namespace {
+
+constexpr int kOnlineThreads = 256;
+
+struct OnlineOut {
+  double excess_sum;
+  long long crossings;
+};
+
+__global__ void __launch_bounds__(kOnlineThreads)
+    online_count_kernel(const uint8_t* __restrict__ ids, long long n, int L, int ne, int k, int g,
+                        const uint8_t* __restrict__ place, unsigned long long* __restrict__ E,
+                        unsigned long long* __restrict__ A, unsigned int* __restrict__ hist,
+                        unsigned long long* __restrict__ crossings, uint32_t* __restrict__ flags) {
+  extern __shared__ unsigned int sh_hist[];  // [L][g]
+  for (int i = threadIdx.x; i < L * g; i += blockDim.x) sh_hist[i] = 0u;
+  __syncthreads();
+  unsigned long long cross = 0;
+  bool bad = false;
+  const long long units = n * (long long)L;
+  const long long nE = (long long)ne * ne;
+  for (long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x; u < units;
+       u += (long long)gridDim.x * blockDim.x) {
+    const long long t = u / L;
+    const int l = (int)(u - t * L);
+    const uint8_t* row = ids + (t * L + l) * k;
+    const uint8_t* pl = place + (long long)l * ne;
+    for (int a = 0; a < k; ++a) {  // layer_gpu_tokens_(l, P(f(l, e))) += 1 (sim.cpp:117-126)
+      const uint32_t e = row[a];
+      if (e >= (uint32_t)ne) {
+        bad = true;
+        continue;
+      }
+      atomicAdd(&sh_hist[l * g + pl[e]], 1u);
+      if (L == 1) atomicAdd(A + e, 1ull);  // no layer pairs: activation is the counted buffer
+    }
+    if (l + 1 < L) {
+      const uint8_t* nxt = row + k;
+      const uint8_t* pn = pl + ne;
+      unsigned long long* El = E + (long long)l * nE;
+      for (int a = 0; a < k; ++a) {
+        const uint32_t j = row[a];
+        if (j >= (uint32_t)ne) continue;
+        const uint32_t pj = pl[j];
+        unsigned long long* Erow = El + (long long)j * ne;
+        for (int b = 0; b < k; ++b) {
+          const uint32_t kk = nxt[b];
+          if (kk >= (uint32_t)ne) continue;  // flagged by the unit owning layer l + 1
+          atomicAdd(Erow + kk, 1ull);         // moe.cpp:179-188, with multiplicity
+          cross += (pj != pn[kk]) ? 1u : 0u;  // token_crossings (sim.cpp:183-198)
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cross += __shfl_xor_sync(0xffffffffu, cross, o);
+  if ((threadIdx.x & 31) == 0 && cross) atomicAdd(crossings, cross);
+  __syncthreads();
+  for (int i = threadIdx.x; i < L * g; i += blockDim.x)
+    if (sh_hist[i]) atomicAdd(hist + i, sh_hist[i]);
+}
+
+__global__ void online_finish_kernel(long long n, int L, int k, int g, unsigned int* __restrict__ hist,
+                                     unsigned long long* __restrict__ crossings,
+                                     unsigned long long* __restrict__ gpu_totals, OnlineOut* __restrict__ out) {
+  // gpu_activation_total_[p] += every activation placed on p this iteration
+  for (int p = threadIdx.x; p < g; p += blockDim.x) {
+    unsigned long long s = 0;
+    for (int l = 0; l < L; ++l) s += hist[l * g + p];
+    gpu_totals[p] += s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // sim.cpp:132-144, operation by operation: per_layer = double(n * k); for each layer in order
+    // excess_sum += max(0.0, peak * n_gpus / per_layer - 1.0)  (IEEE, no contraction)
+    const double per_layer = (double)(n * (long long)k);
+    double sum = 0.0;
+    for (int l = 0; l < L; ++l) {
+      unsigned int peak = 0;
+      for (int p = 0; p < g; ++p) peak = max(peak, hist[l * g + p]);
+      const double x = __dsub_rn(__ddiv_rn(__dmul_rn((double)peak, (double)g), per_layer), 1.0);
+      sum = __dadd_rn(sum, 0.0 < x ? x : 0.0);  // std::max(0.0, x)
+    }
+    out->excess_sum = sum;
+    out->crossings = (long long)*crossings;
+    *crossings = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < L * g; i += blockDim.x) hist[i] = 0u;
+}
+
+}  // namespace
+
+}  // namespace gimbal_gpu
+
+using namespace gimbal_gpu;
+
+struct gimbal_online_s {
+  gimbal_stats_t window = nullptr;
+  StatsInternals si;
+  int L = 0, ne = 0, k = 0, g = 0;
+  int64_t m = 0;
+  int64_t cap = 0;  // tokens the staging buffers hold
+  uint8_t* d_ids = nullptr;
+  uint8_t* h_ids = nullptr;  // pinned
+  uint8_t* d_place = nullptr;
+  unsigned int* d_hist = nullptr;
+  unsigned long long* d_cross = nullptr;
+  unsigned long long* d_totals = nullptr;
+  OnlineOut* d_out = nullptr;
+  OnlineOut* h_out = nullptr;  // pinned
+  bool placed = false;
+  // the iteration as a graph: H2D ids -> count -> finish -> D2H result
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_finish = nullptr, n_d2h = nullptr;
+  int64_t iterations = 0;
+
+  void release() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    cudaFree(d_ids);
+    cudaFreeHost(h_ids);
+    d_ids = nullptr;
+    h_ids = nullptr;
+    cap = 0;
+  }
+};
+
+namespace {
+
+int grow(gimbal_online_t o, int64_t n) {
+  if (n <= o->cap) return GIMBAL_OK;
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(o->si.stream));
+  o->release();
+  const int64_t cap = std::max<int64_t>(n, 4096);
+  const size_t bytes = (size_t)cap * o->L * o->k;
+  GIMBAL_CUDA_TRY(cudaMalloc(&o->d_ids, bytes));
+  GIMBAL_CUDA_TRY(cudaMallocHost(&o->h_ids, bytes));
+  o->cap = cap;
+  return GIMBAL_OK;
+}
+
+int build_graph(gimbal_online_t o, int64_t n, unsigned grid) {
+  GIMBAL_CUDA_TRY(cudaGraphCreate(&o->graph, 0));
+  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&o->n_h2d, o->graph, nullptr, 0, o->d_ids, o->h_ids,
+                                           (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
+  long long nn = n;
+  int L = o->L, ne = o->ne, k = o->k, g = o->g;
+  const uint8_t* ids = o->d_ids;
+  const uint8_t* place = o->d_place;
+  unsigned long long *E = o->si.dE, *A = o->si.dA, *cross = o->d_cross, *totals = o->d_totals;
+  unsigned int* hist = o->d_hist;
+  uint32_t* flags = o->si.dflags;
+  OnlineOut* out = o->d_out;
+  void* cargs[] = {(void*)&ids, &nn, &L, &ne, &k, &g, (void*)&place, &E, &A, &hist, &cross, &flags};
+  cudaKernelNodeParams kp{};
+  kp.func = (void*)online_count_kernel;
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(kOnlineThreads);
+  kp.sharedMemBytes = (unsigned)(o->L * o->g * 4);
+  kp.kernelParams = cargs;
+  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&o->n_count, o->graph, &o->n_h2d, 1, &kp));
+  void* fargs[] = {&nn, &L, &k, &g, &hist, &cross, &totals, &out};
+  cudaKernelNodeParams fp{};
+  fp.func = (void*)online_finish_kernel;
+  fp.gridDim = dim3(1);
+  fp.blockDim = dim3(256);
+  fp.kernelParams = fargs;
+  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&o->n_finish, o->graph, &o->n_count, 1, &fp));
+  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&o->n_d2h, o->graph, &o->n_finish, 1, o->h_out, o->d_out,
+                                           sizeof(OnlineOut), cudaMemcpyDeviceToHost));
+  GIMBAL_CUDA_TRY(cudaGraphInstantiate(&o->exec, o->graph, 0));
+  return GIMBAL_OK;
+}
+
+// batch size n -> graph node parameters (copy size, kernel n and grid)
+int update_graph(gimbal_online_t o, int64_t n, unsigned grid) {
+  GIMBAL_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(o->exec, o->n_h2d, o->d_ids, o->h_ids,
+                                                     (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
+  long long nn = n;
+  int L = o->L, ne = o->ne, k = o->k, g = o->g;
+  const uint8_t* ids = o->d_ids;
+  const uint8_t* place = o->d_place;
+  unsigned long long *E = o->si.dE, *A = o->si.dA, *cross = o->d_cross, *totals = o->d_totals;
+  unsigned int* hist = o->d_hist;
+  uint32_t* flags = o->si.dflags;
+  OnlineOut* out = o->d_out;
+  void* cargs[] = {(void*)&ids, &nn, &L, &ne, &k, &g, (void*)&place, &E, &A, &hist, &cross, &flags};
+  cudaKernelNodeParams kp{};
+  kp.func = (void*)online_count_kernel;
+  kp.gridDim = dim3(grid);
+  kp.blockDim = dim3(kOnlineThreads);
+  kp.sharedMemBytes = (unsigned)(o->L * o->g * 4);
+  kp.kernelParams = cargs;
+  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(o->exec, o->n_count, &kp));
+  void* fargs[] = {&nn, &L, &k, &g, &hist, &cross, &totals, &out};
+  cudaKernelNodeParams fp{};
+  fp.func = (void*)online_finish_kernel;
+  fp.gridDim = dim3(1);
+  fp.blockDim = dim3(256);
+  fp.kernelParams = fargs;
+  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(o->exec, o->n_finish, &fp));
+  return GIMBAL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gimbal_online_create(gimbal_stats_t window, gimbal_online_t* out) {
+  if (!window || !out) return invalid("gimbal_online_create: null argument");
+  auto* o = new gimbal_online_s();
+  o->window = window;
+  o->si = stats_internals(window);
+  o->L = o->si.topo.n_layers;
+  o->ne = o->si.topo.n_experts;
+  o->k = o->si.topo.top_k;
+  o->g = o->si.topo.n_gpus;
+  o->m = (int64_t)o->L * o->ne;
+  if (o->ne > 256 || o->g > 255) {
+    delete o;
+    set_error("online hook: needs n_experts <= 256 and n_gpus <= 255 (uint8 ids / GPU ids)");
+    return GIMBAL_NOT_SUPPORTED;
+  }
+  DeviceGuard dg(o->si.device);
+  auto fail = [&](int st) {
+    gimbal_online_destroy(o);
+    return st;
+  };
+  if (cudaMalloc(&o->d_place, (size_t)o->m) != cudaSuccess ||
+      cudaMalloc(&o->d_hist, (size_t)o->L * o->g * 4) != cudaSuccess ||
+      cudaMalloc(&o->d_cross, 8) != cudaSuccess || cudaMalloc(&o->d_totals, (size_t)o->g * 8) != cudaSuccess ||
+      cudaMalloc(&o->d_out, sizeof(OnlineOut)) != cudaSuccess ||
+      cudaMallocHost(&o->h_out, sizeof(OnlineOut)) != cudaSuccess) {
+    set_error("gimbal_online_create: allocation failed");
+    return fail(GIMBAL_CUDA_ERROR);
+  }
+  if (cudaMemset(o->d_hist, 0, (size_t)o->L * o->g * 4) != cudaSuccess || cudaMemset(o->d_cross, 0, 8) != cudaSuccess ||
+      cudaMemset(o->d_totals, 0, (size_t)o->g * 8) != cudaSuccess) {
+    set_error("gimbal_online_create: init failed");
+    return fail(GIMBAL_CUDA_ERROR);
+  }
+  *out = o;
+  return GIMBAL_OK;
+}
+
+int gimbal_online_destroy(gimbal_online_t o) {
+  if (!o) return GIMBAL_OK;
+  DeviceGuard dg(o->si.device);
+  if (o->si.stream) cudaStreamSynchronize(o->si.stream);
+  o->release();
+  cudaFree(o->d_place);
+  cudaFree(o->d_hist);
+  cudaFree(o->d_cross);
+  cudaFree(o->d_totals);
+  cudaFree(o->d_out);
+  cudaFreeHost(o->h_out);
+  delete o;
+  return GIMBAL_OK;
+}
+
+int gimbal_online_set_placement(gimbal_online_t o, const int32_t* assign, int64_t m) {
+  if (!o || !assign) return invalid("online: null argument");
+  if (m != o->m) return invalid("online: placement size mismatch");
+  std::vector<uint8_t> p((size_t)m);
+  for (int64_t i = 0; i < m; ++i) {
+    if (assign[i] < 0 || assign[i] >= o->g) return invalid("online: placement GPU id out of range");
+    p[(size_t)i] = (uint8_t)assign[i];
+  }
+  std::lock_guard<std::mutex> lk(*o->si.mu);
+  DeviceGuard dg(o->si.device);
+  // pageable source: the copy has consumed `p` when the call returns
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(o->d_place, p.data(), (size_t)m, cudaMemcpyHostToDevice, o->si.stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(o->si.stream));
+  o->placed = true;
+  return GIMBAL_OK;
+}
+
+int gimbal_online_iteration(gimbal_online_t o, const void* ids, int id_bytes, int64_t n, double* excess_sum,
+                            int64_t* crossings) {
+  if (!o || !excess_sum || !crossings) return invalid("online: null argument");
+  if (id_bytes != 1 && id_bytes != 4) return invalid("online: id_bytes must be 1 or 4");
+  if (!o->placed) return invalid("online: no placement set");
+  if (n <= 0) {
+    *excess_sum = 0.0;
+    *crossings = 0;
+    return GIMBAL_OK;
+  }
+  if (!ids) return invalid("online: null ids");
+  std::lock_guard<std::mutex> lk(*o->si.mu);
+  DeviceGuard dg(o->si.device);
+  GIMBAL_TRY(stats_resolve_tokens(o->window));
+  const bool regrow = n > o->cap;
+  GIMBAL_TRY(grow(o, n));
+  const size_t cnt = (size_t)n * o->L * o->k;
+  if (id_bytes == 1) {
+    std::memcpy(o->h_ids, ids, cnt);
+  } else {  // int32 (RoutedStream::choices) -> uint8 (n_e <= 256); the reference leaves bad ids UB
+    const int32_t* s = static_cast<const int32_t*>(ids);
+    for (size_t i = 0; i < cnt; ++i) {
+      if (s[i] < 0 || s[i] >= o->ne) {
+        set_error("add_token: expert id out of range [0, n_experts)");
+        return GIMBAL_OUT_OF_RANGE;
+      }
+      o->h_ids[i] = (uint8_t)s[i];
+    }
+  }
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (n * o->L + kOnlineThreads - 1) / kOnlineThreads));
+  if (!o->exec || regrow) {
+    GIMBAL_TRY(build_graph(o, n, grid));
+  } else {
+    GIMBAL_TRY(update_graph(o, n, grid));
+  }
+  GIMBAL_CUDA_TRY(cudaGraphLaunch(o->exec, o->si.stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(o->si.stream));
+  stats_note_added(o->window, n);
+  ++o->iterations;
+  *excess_sum = o->h_out->excess_sum;
+  *crossings = o->h_out->crossings;
+  return GIMBAL_OK;
+}
+
+int gimbal_online_gpu_totals(gimbal_online_t o, int64_t* out) {
+  if (!o || !out) return invalid("online: null argument");
+  std::lock_guard<std::mutex> lk(*o->si.mu);
+  DeviceGuard dg(o->si.device);
+  std::vector<unsigned long long> t((size_t)o->g);
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(t.data(), o->d_totals, (size_t)o->g * 8, cudaMemcpyDeviceToHost, o->si.stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(o->si.stream));
+  for (int p = 0; p < o->g; ++p) out[p] = (int64_t)t[(size_t)p];
+  return GIMBAL_OK;
+}
+
+}  // extern "C"
