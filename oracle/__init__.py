@@ -226,6 +226,16 @@ class Ref:
         L.ref_mix_seed.restype = C.c_uint64
         L.ref_shuffled_balanced.argtypes = [C.c_int, C.c_int, C.c_uint64, _i32p]
         L.ref_shuffled_balanced.restype = None
+        L.ref_hook_create.argtypes = [C.c_int] * 4 + [_i32p]
+        L.ref_hook_create.restype = C.c_void_p
+        L.ref_hook_destroy.argtypes = [C.c_void_p]
+        L.ref_hook_destroy.restype = None
+        L.ref_hook_set_placement.argtypes = [C.c_void_p, _i32p]
+        L.ref_hook_set_placement.restype = None
+        L.ref_hook_reset_window.argtypes = [C.c_void_p]
+        L.ref_hook_reset_window.restype = None
+        L.ref_hook_iteration.argtypes = [C.c_void_p, _i32p, _i64, _dp, _i64p]
+        L.ref_hook_stats.argtypes = [C.c_void_p, _f64p, _f64p, _i64p]
 
     def _ok(self, st):
         if st != 0:
@@ -337,6 +347,34 @@ class Ref:
                                        threshold, top_e, anchor, alpha, beta, obj, C.byref(am), gr, t))
         return {"objectives": obj[:Cn], "argmin": am.value, "greedy": gr, "t_stats": t[0], "t_place": t[1],
                 "t_eval": t[2], "t_total": t[3]}
+
+    # ---- MoeSubsystem::iteration_cost's per-token work (sim.cpp:113-147) over the reference's
+    # RoutingStats: oracle and host-timing baseline of the GPU hook (ref_capi.cpp ref_hook_*)
+    def hook_create(self, L, ne, k, g, assign):
+        a = np.ascontiguousarray(np.asarray(assign, np.int32))
+        return C.c_void_p(self.lib.ref_hook_create(L, ne, k, g, a))
+
+    def hook_destroy(self, h):
+        self.lib.ref_hook_destroy(h)
+
+    def hook_set_placement(self, h, assign):
+        self.lib.ref_hook_set_placement(h, np.ascontiguousarray(np.asarray(assign, np.int32)))
+
+    def hook_iteration(self, h, ids):
+        a = np.ascontiguousarray(np.asarray(ids, np.int32))
+        ex, cr = C.c_double(), C.c_int64()
+        self._ok(self.lib.ref_hook_iteration(h, a, a.shape[0] if a.ndim > 1 else 0, C.byref(ex), C.byref(cr)))
+        return ex.value, cr.value
+
+    def hook_stats(self, h, L, ne, g):
+        A = np.zeros(L * ne)
+        E = np.zeros(max(L - 1, 1) * ne * ne)
+        t = np.zeros(g, np.int64)
+        self._ok(self.lib.ref_hook_stats(h, A, E, t.ctypes.data_as(_i64p)))
+        return A.reshape(L, ne), E[: (L - 1) * ne * ne].reshape(L - 1, ne, ne), t
+
+    def hook_reset_window(self, h):
+        self.lib.ref_hook_reset_window(h)
 
     def mix_seed(self, seed, stream):
         return self.lib.ref_mix_seed(seed, stream)

@@ -322,3 +322,92 @@ void ref_shuffled_balanced(int m, int g, std::uint64_t seed, std::int32_t* out) 
 }
 
 }  // extern "C"
+
+// ---- MoeSubsystem::iteration_cost's per-token work (sim.cpp:113-147, token_crossings
+// sim.cpp:183-198) restated over the reference's own RoutingStats: the oracle (and the host
+// timing baseline) for the GPU hook gimbal_online_iteration.  Routing is not part of it (the
+// caller passes the routed ids, as the GPU hook receives them).
+namespace {
+struct RefHook {
+  moe::MoeTopology topo;
+  moe::RoutingStats lifetime, window;
+  std::vector<int> assign;
+  Eigen::MatrixXd layer_gpu;
+  std::vector<std::int64_t> totals;
+  RefHook(const moe::MoeTopology& t)
+      : topo(t), lifetime(t), window(t), layer_gpu(Eigen::MatrixXd::Zero(t.n_layers, t.n_gpus)),
+        totals(static_cast<std::size_t>(t.n_gpus), 0) {}
+};
+}  // namespace
+
+extern "C" {
+
+void* ref_hook_create(int L, int ne, int k, int g, const std::int32_t* assign) {
+  auto* h = new RefHook(topo_of(L, ne, k, g));
+  h->assign.assign(assign, assign + static_cast<std::size_t>(L) * ne);
+  return h;
+}
+
+void ref_hook_destroy(void* p) { delete static_cast<RefHook*>(p); }
+
+void ref_hook_set_placement(void* p, const std::int32_t* assign) {
+  auto* h = static_cast<RefHook*>(p);
+  h->assign.assign(assign, assign + h->assign.size());
+}
+
+void ref_hook_reset_window(void* p) { static_cast<RefHook*>(p)->window.reset(); }
+
+int ref_hook_iteration(void* p, const std::int32_t* ids, std::int64_t n, double* excess_sum, std::int64_t* crossings) {
+  auto* h = static_cast<RefHook*>(p);
+  return guarded([&] {
+    const auto& topo = h->topo;
+    const int per = topo.n_layers * topo.top_k;
+    h->layer_gpu.setZero();
+    std::int64_t cross = 0;
+    std::vector<int> tok(static_cast<std::size_t>(per));
+    for (std::int64_t t = 0; t < n; ++t) {
+      for (int i = 0; i < per; ++i) tok[static_cast<std::size_t>(i)] = ids[t * per + i];
+      h->lifetime.add_token(std::span<const int>(tok));
+      h->window.add_token(std::span<const int>(tok));
+      for (int l = 0; l < topo.n_layers; ++l)
+        for (int a = 0; a < topo.top_k; ++a) {
+          const int gpu = h->assign[static_cast<std::size_t>(topo.flat_id(l, tok[static_cast<std::size_t>(l * topo.top_k + a)]))];
+          h->layer_gpu(l, gpu) += 1.0;
+          h->totals[static_cast<std::size_t>(gpu)] += 1;
+        }
+      for (int l = 0; l + 1 < topo.n_layers; ++l)
+        for (int a = 0; a < topo.top_k; ++a) {
+          const int ga = h->assign[static_cast<std::size_t>(topo.flat_id(l, tok[static_cast<std::size_t>(l * topo.top_k + a)]))];
+          for (int b = 0; b < topo.top_k; ++b)
+            if (ga != h->assign[static_cast<std::size_t>(
+                          topo.flat_id(l + 1, tok[static_cast<std::size_t>((l + 1) * topo.top_k + b)]))])
+              ++cross;
+        }
+    }
+    const double per_layer = static_cast<double>(n * topo.top_k);
+    double s = 0.0;
+    for (int l = 0; l < topo.n_layers; ++l) {
+      const double peak = h->layer_gpu.row(l).maxCoeff();
+      s += std::max(0.0, peak * topo.n_gpus / per_layer - 1.0);
+    }
+    *excess_sum = s;
+    *crossings = cross;
+  });
+}
+
+// window A [L][ne], window E [(L-1)][ne][ne] (row-major doubles, either may be NULL), GPU totals [g]
+int ref_hook_stats(void* p, double* A, double* E, std::int64_t* totals) {
+  auto* h = static_cast<RefHook*>(p);
+  return guarded([&] {
+    if (A) to_rowmajor(h->window.activation(), A);
+    if (E) {
+      const auto aff = h->window.affinity();
+      const std::size_t blk = static_cast<std::size_t>(h->topo.n_experts) * h->topo.n_experts;
+      for (std::size_t l = 0; l < aff.E.size(); ++l) to_rowmajor(aff.E[l], E + l * blk);
+    }
+    if (totals)
+      for (std::size_t i = 0; i < h->totals.size(); ++i) totals[i] = h->totals[i];
+  });
+}
+
+}  // extern "C"

@@ -10,10 +10,11 @@ from .moe import (AffinityTensor, MoeTopology, RoutedStream, RoutingParams, Rout
 from .placement import (AffinitySet, Placement, PlacementCost, PlacementProblem, Relocation, build_affinity_set,
                         eval_cost, eval_costs, greedy_place, maybe_relocate, shuffled_candidates, static_placement)
 from .pipeline import HotPath
+from .hook import OnlineHook
 
 __all__ = [
     "AffinityTensor", "MoeTopology", "RoutedStream", "RoutingParams", "RoutingStats", "comm_cost", "generate_trace",
     "generator_tables", "record_stats", "AffinitySet", "Placement", "PlacementCost", "PlacementProblem",
     "Relocation", "build_affinity_set", "eval_cost", "eval_costs", "greedy_place", "maybe_relocate",
-    "shuffled_candidates", "static_placement", "HotPath",
+    "shuffled_candidates", "static_placement", "HotPath", "OnlineHook",
 ]

@@ -64,3 +64,24 @@ def test_sim_report_byte_identical_on_gpu_shim(scenario):
     assert out.returncode == 0, out.stderr
     with open(os.path.join(GOLDEN, f"sim_report_{scenario}.json")) as f:
         assert out.stdout == f.read()
+
+
+# ---- GPU: the simulator with its expert-layer hook on the GPU (GpuMoeSubsystem) ----
+
+@pytest.mark.gpu
+def test_reference_sim_tests_pass_with_gpu_hook():
+    """proj/tests/unit/test_sim.cpp with gimbal::run's hook swapped for GpuMoeSubsystem (the
+    per-iteration loop of sim.cpp:113-147 as one CUDA graph per engine iteration)."""
+    out = _run([_bin("shim_sim_tests_gpuhook")])
+    assert out.returncode == 0 and "| 0 failed" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scenario", [0, 1, 2])
+def test_sim_report_byte_identical_with_gpu_hook(scenario):
+    """Byte-identical simulation reports with the GPU hook: latencies (which feed on the
+    bottleneck excess and crossings of every iteration), expert loads, relocations, migrations."""
+    out = _run([_bin("sim_report_gpuhook"), str(scenario)])
+    assert out.returncode == 0, out.stderr
+    with open(os.path.join(GOLDEN, f"sim_report_{scenario}.json")) as f:
+        assert out.stdout == f.read()
