@@ -116,6 +116,14 @@ int gimbal_eval_costs(gimbal_stats_t h, const uint8_t* candidates, int64_t n_can
                       int cand_mem, double alpha, double beta, double* deviation, double* cut,
                       double* objective, int64_t* argmin, int out_mem);
 
+/* Hotspot measure per candidate: the bottleneck excess sum_l max(0, peak_l * g / (T * k) - 1),
+ * peak_l = the most loaded GPU's activation count in layer l under the candidate placement, T * k
+ * = the activations per layer -- the simulator's per-iteration hotspot penalty (sim.cpp:132-144)
+ * over the handle's counted trace, in the reference's double arithmetic.  Candidates [C][m]
+ * uint8 (host or device), excess [C] doubles (host or device). */
+int gimbal_eval_excess(gimbal_stats_t h, const uint8_t* candidates, int64_t n_candidates, int cand_mem,
+                       double* excess, int out_mem);
+
 /* build_affinity_set (placement.cpp:186-238) on the handle's E: pairs with count >= threshold
  * and > 0, ordered by count desc then flat ids asc, truncated to top_e (top_e < 0 keeps all),
  * then lightest pairs dropped until the endpoint union fits `capacity`.  Writes the sorted

@@ -80,6 +80,7 @@ class Oracle:
         L.go_check_feasible.argtypes = [C.c_int, C.c_int, _i32p]
         L.go_eval_costs_mt.argtypes = [C.c_int, C.c_int, C.c_int, _u64p, _u64p, _u8p, _i64, C.c_double,
                                        C.c_double, _f64p, _f64p, _f64p, _i64p, C.c_int]
+        L.go_eval_excess.argtypes = [C.c_int, C.c_int, C.c_int, _u64p, _u8p, _i64, _f64p]
         L.go_generate_trace_mt.argtypes = [C.c_int, C.c_int, C.c_int, _u32p, C.c_uint64, C.c_uint64,
                                            C.c_uint64, _i64, _i64, _u8p, C.c_int]
 
@@ -139,6 +140,13 @@ class Oracle:
             self._ok(self.lib.go_eval_costs(L, ne, g, A, E, cands, Cn, alpha, beta, D, cut, obj, C.byref(am)),
                      "eval_costs")
         return D, cut, obj, am.value
+
+    def eval_excess(self, L, ne, g, A, cands):
+        A = np.ascontiguousarray(A, np.uint64).ravel()
+        cands = np.ascontiguousarray(cands, np.uint8)
+        out = np.zeros(cands.shape[0])
+        self._ok(self.lib.go_eval_excess(L, ne, g, A, cands, cands.shape[0], out), "eval_excess")
+        return out
 
     def eval_cost_dense(self, A, W, g, assign, alpha=1.0, beta=1.0):
         A = np.ascontiguousarray(A, np.float64)

@@ -8,13 +8,13 @@ from . import _native
 from .moe import (AffinityTensor, MoeTopology, RoutedStream, RoutingParams, RoutingStats, comm_cost,
                   generate_trace, generator_tables, record_stats)
 from .placement import (AffinitySet, Placement, PlacementCost, PlacementProblem, Relocation, build_affinity_set,
-                        eval_cost, eval_costs, greedy_place, maybe_relocate, shuffled_candidates, static_placement)
+                        eval_cost, eval_costs, eval_excess, greedy_place, maybe_relocate, shuffled_candidates, static_placement)
 from .pipeline import HotPath
 from .hook import OnlineHook
 
 __all__ = [
     "AffinityTensor", "MoeTopology", "RoutedStream", "RoutingParams", "RoutingStats", "comm_cost", "generate_trace",
     "generator_tables", "record_stats", "AffinitySet", "Placement", "PlacementCost", "PlacementProblem",
-    "Relocation", "build_affinity_set", "eval_cost", "eval_costs", "greedy_place", "maybe_relocate",
+    "Relocation", "build_affinity_set", "eval_cost", "eval_costs", "eval_excess", "greedy_place", "maybe_relocate",
     "shuffled_candidates", "static_placement", "HotPath", "OnlineHook",
 ]

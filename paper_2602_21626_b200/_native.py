@@ -53,6 +53,7 @@ SIGNATURES = [
     ("gimbal_stats_merge", C.c_int, [_P, _P, _i64, C.c_int]),
     ("gimbal_stats_count_timing", C.c_int, [_P, C.c_int, C.POINTER(_d), C.POINTER(_i64)]),
     ("gimbal_eval_costs", C.c_int, [_P, _P, _i64, C.c_int, _d, _d, _P, _P, _P, C.POINTER(_i64), C.c_int]),
+    ("gimbal_eval_excess", C.c_int, [_P, _P, _i64, C.c_int, _P, C.c_int]),
     ("gimbal_affinity_set", C.c_int, [_P, _d, _i32, _i32, _i32, _P, C.POINTER(_i32)]),
     ("gimbal_greedy_place", C.c_int, [_P, _P, _i32, _i32, _P, C.c_int, _P]),
     ("gimbal_window_place_async", C.c_int, [_P, _P, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P]),

@@ -1130,6 +1130,39 @@ int gimbal_pass_distributed_async(gimbal_stats_t h, gimbal_comm_t comm, double t
   return gimbal_dist_merge_argmin(h, comm, scores + 2 * rows + lead, n_local, cand_offset, n_total, global, argmin);
 }
 
+int gimbal_eval_excess(gimbal_stats_t h, const uint8_t* candidates, int64_t C, int cand_mem, double* excess,
+                       int out_mem) {
+  GIMBAL_TRY(check_handle(h));
+  if (C < 0) return invalid("eval_excess: negative candidate count");
+  if (C == 0) return GIMBAL_OK;
+  if (!candidates || !excess) return invalid("eval_excess: null argument");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_TRY(h->derive());
+  const int64_t m = h->m();
+  const uint8_t* dc = candidates;
+  if (cand_mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(h->cand.ensure((size_t)C * m));
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(h->cand.p, candidates, (size_t)C * m, cudaMemcpyHostToDevice, h->stream));
+    dc = h->cand.as<uint8_t>();
+  }
+  double* dx = excess;
+  if (out_mem != GIMBAL_MEM_DEVICE) {
+    GIMBAL_TRY(h->dout.ensure((size_t)C * 8 + 16));
+    dx = h->dout.as<double>();
+  }
+  GIMBAL_CUDA_TRY(cudaMemsetAsync(h->dflags + 2, 0, 4, h->stream));
+  GIMBAL_CUDA_TRY(launch_eval_excess(h->topo.n_layers, h->topo.n_experts, h->topo.n_gpus, h->dA, dc, C, dx,
+                                     h->dflags + 2, h->stream));
+  uint32_t f = 0;
+  GIMBAL_CUDA_TRY(cudaMemcpyAsync(&f, h->dflags + 2, 4, cudaMemcpyDeviceToHost, h->stream));
+  if (out_mem != GIMBAL_MEM_DEVICE)
+    GIMBAL_CUDA_TRY(cudaMemcpyAsync(excess, dx, (size_t)C * 8, cudaMemcpyDeviceToHost, h->stream));
+  GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  if (f) return invalid("eval_excess: candidate GPU id out of range [0, g)");
+  return GIMBAL_OK;
+}
+
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms) {
   GIMBAL_TRY(check_handle(h));
   std::lock_guard<std::mutex> lk(h->mu);

@@ -213,6 +213,10 @@ cudaError_t launch_eval_finish(int64_t C, int L, int ne, int k, const unsigned l
                                double beta, const unsigned long long* same, const double* D, double* cut,
                                double* obj, long long* argmin, uint32_t* flags, cudaStream_t s);
 
+// per-candidate bottleneck excess sum_l max(0, peak_l * g / (T k) - 1) over the handle's A
+cudaError_t launch_eval_excess(int L, int ne, int g, const unsigned long long* A, const uint8_t* cands, int64_t C,
+                               double* excess, uint32_t* flags, cudaStream_t s);
+
 cudaError_t launch_affinity_keys(int L, int ne, const unsigned long long* E, double threshold,
                                  unsigned long long* keys, int64_t n_pad, uint32_t* flags,
                                  cudaStream_t s);

@@ -389,6 +389,64 @@ __global__ void eval_finish_kernel(int64_t C, int L, int ne, int k, const unsign
   if (threadIdx.x == 0 && argmin) *argmin = bi[0];
 }
 
+// ---- per-candidate bottleneck excess (sim.cpp:132-144's hotspot measure over the counted trace):
+// excess_c = sum over layers, in order, of max(0, peak_l * g / (T * k) - 1), peak_l = max over
+// GPUs p of sum_{e: P_c(l, e) = p} A(l, e), T * k = sum_e A(0, e).  One CTA per candidate, one
+// warp per layer at a time; the layer terms are added in layer order by one thread (the
+// reference's double arithmetic, IEEE, no contraction).
+__global__ void __launch_bounds__(256)
+    eval_excess_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
+                       const uint8_t* __restrict__ cands, int64_t m, double* __restrict__ excess,
+                       uint32_t* __restrict__ flags) {
+  extern __shared__ unsigned long long ex_sh[];  // [warps][g] loads, then [L] terms (double)
+  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* loads = ex_sh + warp * g;
+  double* term = reinterpret_cast<double*>(ex_sh + warps * g);
+  __shared__ unsigned long long tk;
+  if (threadIdx.x == 0) tk = 0;
+  __syncthreads();
+  {
+    unsigned long long a = 0;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) a += A[e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0 && a) atomicAdd(&tk, a);
+  }
+  __syncthreads();
+  const double per_layer = (double)tk;
+  const uint8_t* P = cands + blockIdx.x * m;
+  bool bad = false;
+  for (int l = warp; l < L; l += warps) {
+    for (int p = lane; p < g; p += 32) loads[p] = 0;
+    __syncwarp();
+    for (int e = lane; e < ne; e += 32) {
+      const uint32_t p = P[(int64_t)l * ne + e];
+      if (p >= (uint32_t)g) {
+        bad = true;
+        continue;
+      }
+      atomicAdd(&loads[p], A[(int64_t)l * ne + e]);
+    }
+    __syncwarp();
+    unsigned long long peak = 0;
+    for (int p = lane; p < g; p += 32) peak = max(peak, loads[p]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) peak = max(peak, __shfl_xor_sync(0xffffffffu, peak, o));
+    if (lane == 0) {
+      const double x = __dsub_rn(__ddiv_rn(__dmul_rn((double)peak, (double)g), per_layer), 1.0);
+      term[l] = 0.0 < x ? x : 0.0;  // std::max(0.0, x)
+    }
+    __syncwarp();
+  }
+  if (bad) atomicOr(flags, (uint32_t)kFlagInfeasible);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int l = 0; l < L; ++l) s = __dadd_rn(s, term[l]);
+    excess[blockIdx.x] = s;
+  }
+}
+
 // ---- build_affinity_set: composite sort keys over E ----
 // key = (w << 24) | (2^24 - 1 - idx) for qualifying cells, else 0; sorting keys in descending
 // order yields (w desc, idx asc), and idx = (l*ne + j)*ne + k orders exactly like the
@@ -789,6 +847,16 @@ cudaError_t launch_max_cell(const unsigned long long* E, int64_t n, unsigned lon
   if (n <= 0) return cudaSuccess;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(1184, (n + 255) / 256));
   max_cell_kernel<<<grid, 256, 0, s>>>(E, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval_excess(int L, int ne, int g, const unsigned long long* A, const uint8_t* cands, int64_t C,
+                               double* excess, uint32_t* flags, cudaStream_t s) {
+  if (C <= 0) return cudaSuccess;
+  const size_t smem = (size_t)8 * g * 8 + (size_t)L * 8;
+  cudaError_t e = cudaFuncSetAttribute(eval_excess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  eval_excess_kernel<<<(unsigned)C, 256, smem, s>>>(L, ne, g, A, cands, (int64_t)L * ne, excess, flags);
   return cudaGetLastError();
 }
 

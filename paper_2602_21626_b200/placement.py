@@ -117,6 +117,27 @@ def eval_costs(stats: RoutingStats, candidates, alpha: float = 1.0, beta: float 
     return D, cut, obj, am.value
 
 
+def eval_excess(stats: RoutingStats, candidates) -> np.ndarray:
+    """Per-candidate bottleneck excess sum_l max(0, peak_l * g / (T * k) - 1) of the stats' A under
+    each placement [C][m] uint8 (numpy or CUDA): the simulator's hotspot penalty (sim.cpp:132-144)
+    over the counted trace."""
+    m = stats.topo.total_experts()
+    if hasattr(candidates, "data_ptr"):
+        cptr, cmem, n, keep = candidates.data_ptr(), (N.MEM_DEVICE if candidates.is_cuda else N.MEM_HOST), \
+            candidates.shape[0], candidates
+        if cmem == N.MEM_DEVICE:
+            stats._after_torch(candidates)
+    else:
+        keep = np.ascontiguousarray(np.asarray(candidates, np.uint8))
+        cptr, cmem, n = keep.ctypes.data, N.MEM_HOST, keep.shape[0]
+    if n and int(np.prod(getattr(keep, "shape"))) != n * m:
+        raise ValueError("placement: assignment size mismatch")
+    out = np.zeros(n)
+    N.check(N.lib().gimbal_eval_excess(stats.handle, C.c_void_p(cptr), n, cmem, out.ctypes.data, N.MEM_HOST),
+            "eval_excess")
+    return out
+
+
 def build_affinity_set(affinity, topo: MoeTopology, threshold: float, top_e: int, capacity: int,
                        anchor_gpu: int) -> AffinitySet:  # placement.cpp:186-238
     """``affinity`` is an AffinityTensor (reference form) or a RoutingStats (device E)."""

@@ -656,3 +656,25 @@ def test_run_distributed_single_rank_matches_run(G, orc):
         assert torch.equal(part, cands[5:])  # the caller's slice is not overwritten
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,T,C", [("dsv3", 30011, 70), ("qwen3", 20011, 33), ("mixtral", 9001, 300),
+                                       ("dsv2lite", 5000, 17)])
+def test_eval_excess_matches_oracle(G, orc, shape, T, C):
+    """gimbal_eval_excess: the simulator's bottleneck excess (sim.cpp:132-144) per candidate over the
+    counted trace, bit-exact against the oracle (itself pinned to the reference hook loop)."""
+    L, ne, k, g = SHAPES[shape]
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, T, model_seed=6, stream_seed=1, device=0)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(trace)
+    oA, _, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+    cands = G.shuffled_candidates(L * ne, g, 17, C)
+    cands[0] = np.asarray(G.static_placement(topo).assign, np.uint8)
+    want = orc.eval_excess(L, ne, g, oA, cands)
+    assert np.array_equal(G.eval_excess(s, cands), want)
+    assert np.array_equal(G.eval_excess(s, torch.from_numpy(cands).cuda()), want)
+    bad = cands.copy()
+    bad[1, 3] = g
+    with pytest.raises(ValueError):
+        G.eval_excess(s, bad)

@@ -206,3 +206,24 @@ def test_generator_twin_is_deterministic_and_distinct(orc):
     assert np.array_equal(a[200:300], c)
     # top_k draws without replacement: distinct ids per layer
     assert all(len(set(a[t, l])) == 4 for t in range(500) for l in range(6))
+
+
+def test_eval_excess_restatement_matches_reference_hook_loop(ref, orc):
+    """The per-candidate bottleneck excess oracle (go_eval_excess) over a batch's counts equals the
+    reference simulator's per-iteration excess (sim.cpp:132-144 via ref_hook_iteration) for that
+    batch under the same placement."""
+    import numpy as np
+
+    for L, ne, k, g, n in [(4, 8, 2, 2, 333), (6, 16, 4, 4, 4096), (32, 8, 2, 8, 77), (5, 64, 6, 8, 1000)]:
+        rng = np.random.default_rng(n)
+        ids = rng.integers(0, ne, size=(n, L, k)).astype(np.int32)
+        cands = np.stack([np.random.default_rng(c).permutation(np.arange(L * ne) % g) for c in range(5)]).astype(np.uint8)
+        A, _, _ = orc.stats(L, ne, k, ids)
+        got = orc.eval_excess(L, ne, g, A, cands)
+        for c in range(5):
+            h = ref.hook_create(L, ne, k, g, cands[c].astype(np.int32))
+            try:
+                want, _ = ref.hook_iteration(h, ids)
+            finally:
+                ref.hook_destroy(h)
+            assert got[c] == want
