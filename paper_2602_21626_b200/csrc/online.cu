@@ -280,7 +280,8 @@ int gimbal_online_create(gimbal_stats_t window, gimbal_online_t* out) {
 int gimbal_online_destroy(gimbal_online_t o) {
   if (!o) return GIMBAL_OK;
   DeviceGuard dg(o->si.device);
-  if (o->si.stream) cudaStreamSynchronize(o->si.stream);
+  // no use of the window handle here: it may already be destroyed (its destroy synchronised its
+  // stream); cudaFree / cudaFreeHost wait for outstanding work on these buffers
   o->release();
   cudaFree(o->d_place);
   cudaFree(o->d_hist);
