@@ -122,6 +122,7 @@ struct gimbal_stats_s {
   bool use_mma = false;  // tcgen05 contraction instead of shared-memory counting (n_e <= 128)
   bool use_stack = false;  // tcgen05 contraction with two 64-expert layers per operand
   bool use_fp4 = false;    // block-scaled FP4 tcgen05 contraction (256 experts, top-8)
+  bool use_fp4x2 = false;  // the same on CTA pairs (cta_group::2)
   cudaStream_t t_stream = nullptr;
   unsigned long long* lm8[kStages] = {nullptr, nullptr};
   int64_t lm8_tokens = 0;
@@ -268,6 +269,18 @@ struct gimbal_stats_s {
         return GIMBAL_OK;
       }
       cudaGetLastError();  // shape does not fit the stacked kernel: fall through (timing slot reused)
+    }
+    if (use_fp4x2 && fp4x2_count_supported(L, topo.n_experts, topo.top_k, id_bytes, ids, n) &&
+        !GIMBAL_KNOB("GIMBAL_NO_DIRECT")) {
+      // 256 experts, top-8: block-scaled FP4 on CTA pairs straight from the trace
+      GIMBAL_TRY(timing_begin());
+      const cudaError_t e = launch_count_fp4x2(L, sms, static_cast<const uint8_t*>(ids), n, dE, stream);
+      if (e != cudaErrorNotSupported) {
+        GIMBAL_CUDA_TRY(e);
+        GIMBAL_TRY(timing_end());
+        return GIMBAL_OK;
+      }
+      cudaGetLastError();  // not mappable: fall through (timing slot reused)
     }
     if (use_fp4 && fp4_count_supported(L, topo.n_experts, topo.top_k, id_bytes, ids, n) &&
         !GIMBAL_KNOB("GIMBAL_NO_DIRECT")) {
@@ -422,6 +435,7 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
     h->use_stack = want_mma && !(path && std::string(path) == "lm8");
     // opt-in: measured slower than the atomic u15 kernel at DS-V3 (fp4_count.cu header)
     h->use_fp4 = path && std::string(path) == "fp4";
+    h->use_fp4x2 = path && std::string(path) == "fp4x2";
   }
   h->smem_optin = optin;
   if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess ||

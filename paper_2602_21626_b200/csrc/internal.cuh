@@ -154,6 +154,10 @@ bool mma_stack_supported(int L, int ne, int k, int id_bytes, const void* ids);
 cudaError_t launch_count_mma_stack(int L, int ne, int k, int sms, int max_smem, const uint8_t* trace, int64_t T,
                                    unsigned long long* E, uint32_t* flags, cudaStream_t s);
 
+// Block-scaled FP4 on CTA pairs (fp4x2_count.cu): M = 256 x N = 256 per pair of SMs.
+bool fp4x2_count_supported(int L, int ne, int k, int id_bytes, const void* ids, int64_t T);
+cudaError_t launch_count_fp4x2(int L, int sms, const uint8_t* trace, int64_t T, unsigned long long* E,
+                               cudaStream_t s);
 // Block-scaled FP4 tensor-core contraction for 256-expert top-8 uint8 traces (fp4_count.cu):
 // L even, 16-byte aligned base, T < 2^31.  cudaErrorNotSupported when the trace cannot be mapped.
 bool fp4_count_supported(int L, int ne, int k, int id_bytes, const void* ids, int64_t T);

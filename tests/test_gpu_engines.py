@@ -32,9 +32,11 @@ def test_shipped_library_has_no_knobs():
     assert "getenv" not in out
 
 
-@pytest.mark.parametrize("L,T,dup", [(58, 70001, 0), (58, 129, 0), (2, 5000, 0), (58, 5000, 1)])
-def test_fp4_count_path(L, T, dup):
-    run_case({"GIMBAL_COUNT_PATH": "fp4"}, "fp4", L, T, dup)
+@pytest.mark.parametrize("path", ["fp4", "fp4x2"])
+@pytest.mark.parametrize("L,T,dup", [(58, 70001, 0), (58, 129, 0), (2, 5000, 0), (58, 5000, 1), (4, 300000, 0)])
+def test_fp4_count_path(path, L, T, dup):
+    """Block-scaled FP4 counters: one SM per M = 128 half (fp4) and CTA pairs (fp4x2)."""
+    run_case({"GIMBAL_COUNT_PATH": path}, "fp4", L, T, dup)
 
 
 @pytest.mark.parametrize("L,ne,k,g,C", [(58, 256, 8, 8, 70), (48, 128, 8, 8, 33), (26, 64, 6, 8, 70),
