@@ -166,6 +166,19 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
                       double* scores_device, int64_t* argmin_device, int32_t* placement_device,
                       int32_t* members_device, int32_t* n_members_device, uint32_t* flags_device);
 
+/* One whole pass on a device trace as a CUDA graph: reset + add_tokens (device ids) +
+ * gimbal_pass_async with the same arguments.  The first call runs eagerly (validation, scratch
+ * sizing), the second records the step on the handle's stream as a graph, and every later call
+ * with identical arguments (pointers, sizes, parameters; the data behind them may change)
+ * replays it with one launch -- for launch-bound small shapes (Mixtral class: ~10 kernels a
+ * pass).  Counting-kernel timing (gimbal_stats_count_timing) covers replays through event-record
+ * nodes.  Not for concurrent use of the handle from another thread while recording. */
+int gimbal_pass_graph(gimbal_stats_t h, const void* ids_device, int id_bytes, int64_t n_tokens, double threshold,
+                      int32_t top_e, int32_t capacity, int32_t anchor_gpu, uint8_t* candidates_device,
+                      int64_t n_candidates, double alpha, double beta, double* scores_device, int64_t* argmin_device,
+                      int32_t* placement_device, int32_t* members_device, int32_t* n_members_device,
+                      uint32_t* flags_device);
+
 /* Counting kernels of this handle run on n_sms SMs (default: all).  Leaving SMs free lets a
  * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */
 int gimbal_stats_set_count_sms(gimbal_stats_t h, int n_sms);

@@ -58,6 +58,8 @@ SIGNATURES = [
     ("gimbal_greedy_place", C.c_int, [_P, _P, _i32, _i32, _P, C.c_int, _P]),
     ("gimbal_window_place_async", C.c_int, [_P, _P, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P]),
     ("gimbal_stats_set_count_sms", C.c_int, [_P, C.c_int]),
+    ("gimbal_pass_graph", C.c_int, [_P, _P, C.c_int, _i64, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P, _P,
+                                    _P]),
     ("gimbal_pass_async", C.c_int, [_P, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P, _P, _P]),
     ("gimbal_dist_unique_id", C.c_int, [_P]),
     ("gimbal_dist_comm_init", C.c_int, [_i32, _i32, _P, C.c_int, C.POINTER(_P)]),

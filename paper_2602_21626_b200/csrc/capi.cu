@@ -134,7 +134,58 @@ struct gimbal_stats_s {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
   size_t tev_used = 0;
+  // gimbal_pass_graph: the step recorded as a CUDA graph (reset + count + pass), replayed while the
+  // arguments stay the same; its counting kernels are timed by event-record nodes (g_tev)
+  bool capturing = false;
+  struct GraphKey {
+    const void* ids = nullptr;
+    int id_bytes = 0;
+    int64_t n = 0;
+    double threshold = 0, alpha = 0, beta = 0;
+    int32_t top_e = 0, capacity = 0, anchor = 0;
+    uint8_t* cands = nullptr;
+    int64_t C = 0;
+    double* scores = nullptr;
+    int64_t* argmin = nullptr;
+    int32_t *placement = nullptr, *members = nullptr, *n_members = nullptr;
+    uint32_t* flags = nullptr;
+    int sms = 0;
+    bool operator==(const GraphKey& o) const {
+      return ids == o.ids && id_bytes == o.id_bytes && n == o.n && threshold == o.threshold && alpha == o.alpha &&
+             beta == o.beta && top_e == o.top_e && capacity == o.capacity && anchor == o.anchor && cands == o.cands &&
+             C == o.C && scores == o.scores && argmin == o.argmin && placement == o.placement &&
+             members == o.members && n_members == o.n_members && flags == o.flags && sms == o.sms;
+    }
+  };
+  GraphKey gkey;
+  int gseen = 0;  // eager runs with gkey (the first allocates every scratch buffer)
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_tev;
+  bool g_pending = false;  // a timed replay whose events are not yet harvested
+  double g_ms = 0.0;
+  int64_t g_launches = 0;
+  int harvest_graph_timing() {
+    if (!g_pending) return GIMBAL_OK;
+    for (auto& pr : g_tev) {
+      GIMBAL_CUDA_TRY(cudaEventSynchronize(pr.second));
+      float ms = 0.f;
+      GIMBAL_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      g_ms += ms;
+      ++g_launches;
+    }
+    g_pending = false;
+    return GIMBAL_OK;
+  }
+
   int timing_begin() {
+    if (capturing) {  // an event-record node in the graph, timed on every replay
+      cudaEvent_t a, b;
+      GIMBAL_CUDA_TRY(cudaEventCreate(&a));
+      GIMBAL_CUDA_TRY(cudaEventCreate(&b));
+      g_tev.emplace_back(a, b);
+      GIMBAL_CUDA_TRY(cudaEventRecordWithFlags(a, stream, cudaEventRecordExternal));
+      return GIMBAL_OK;
+    }
     if (!timing) return GIMBAL_OK;
     if (tev_used == tev.size()) {
       cudaEvent_t a, b;
@@ -146,6 +197,10 @@ struct gimbal_stats_s {
     return GIMBAL_OK;
   }
   int timing_end() {
+    if (capturing) {
+      GIMBAL_CUDA_TRY(cudaEventRecordWithFlags(g_tev.back().second, stream, cudaEventRecordExternal));
+      return GIMBAL_OK;
+    }
     if (!timing) return GIMBAL_OK;
     GIMBAL_CUDA_TRY(cudaEventRecord(tev[tev_used].second, stream));
     ++tev_used;
@@ -494,6 +549,11 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
     }
     if (h->g_stream) cudaStreamSynchronize(h->g_stream);
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    for (auto& pr : h->g_tev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
     for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints, &h->probe, &h->dscr}) b->release();
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -649,16 +709,22 @@ int gimbal_stats_count_timing(gimbal_stats_t h, int enable, double* count_ms, in
   DeviceGuard g(h->device);
   if (count_ms || launches) {
     GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    double total = 0.0;
+    GIMBAL_TRY(h->harvest_graph_timing());
+    double total = h->g_ms;
     for (size_t i = 0; i < h->tev_used; ++i) {
       float ms = 0.f;
       GIMBAL_CUDA_TRY(cudaEventElapsedTime(&ms, h->tev[i].first, h->tev[i].second));
       total += ms;
     }
     if (count_ms) *count_ms = total;
-    if (launches) *launches = (int64_t)h->tev_used;
+    if (launches) *launches = (int64_t)h->tev_used + h->g_launches;
   }
-  if (enable != (h->timing ? 1 : 0) || enable) h->tev_used = 0;
+  if (enable != (h->timing ? 1 : 0) || enable) {
+    h->tev_used = 0;
+    h->g_pending = false;
+    h->g_ms = 0.0;
+    h->g_launches = 0;
+  }
   h->timing = enable != 0;
   return GIMBAL_OK;
 }
@@ -1174,6 +1240,96 @@ int gimbal_eval_excess(gimbal_stats_t h, const uint8_t* candidates, int64_t C, i
     GIMBAL_CUDA_TRY(cudaMemcpyAsync(excess, dx, (size_t)C * 8, cudaMemcpyDeviceToHost, h->stream));
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
   if (f) return invalid("eval_excess: candidate GPU id out of range [0, g)");
+  return GIMBAL_OK;
+}
+
+int gimbal_pass_graph(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n_tokens, double threshold,
+                      int32_t top_e, int32_t capacity, int32_t anchor, uint8_t* candidates, int64_t C, double alpha,
+                      double beta, double* scores, int64_t* argmin, int32_t* placement, int32_t* members,
+                      int32_t* n_members, uint32_t* flags_out) {
+  GIMBAL_TRY(check_handle(h));
+  if (!ids || n_tokens < 1) return invalid("pass_graph: needs device ids of at least one token");
+  gimbal_stats_s::GraphKey key;
+  key.ids = ids;
+  key.id_bytes = id_bytes;
+  key.n = n_tokens;
+  key.threshold = threshold;
+  key.alpha = alpha;
+  key.beta = beta;
+  key.top_e = top_e;
+  key.capacity = capacity;
+  key.anchor = anchor;
+  key.cands = candidates;
+  key.C = C;
+  key.scores = scores;
+  key.argmin = argmin;
+  key.placement = placement;
+  key.members = members;
+  key.n_members = n_members;
+  key.flags = flags_out;
+  key.sms = h->sms;
+  if (h->gexec && key == h->gkey) {
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard g(h->device);
+    if (h->timing) GIMBAL_TRY(h->harvest_graph_timing());
+    GIMBAL_CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+    h->g_pending = h->timing && !h->g_tev.empty();
+    // host-side effects of reset + add_tokens + pass: the counts are the trace's, A derived
+    h->tokens = n_tokens;
+    h->tokens_on_device = false;
+    ++h->count_version;
+    h->derived = true;
+    h->w_derived = h->topo.n_layers < 2;
+    h->m_cached_buf = nullptr;
+    return GIMBAL_OK;
+  }
+  auto eager = [&]() -> int {
+    GIMBAL_TRY(gimbal_stats_reset(h));
+    GIMBAL_TRY(gimbal_stats_add_tokens(h, ids, id_bytes, n_tokens, GIMBAL_MEM_DEVICE));
+    return gimbal_pass_async(h, threshold, top_e, capacity, anchor, candidates, C, alpha, beta, scores, argmin,
+                             placement, members, n_members, flags_out);
+  };
+  if (!(key == h->gkey) || h->gseen == 0) {
+    // first run with these arguments: eager (validates, sizes every scratch buffer)
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+    h->gkey = key;
+    h->gseen = 0;
+    GIMBAL_TRY(eager());
+    h->gseen = 1;
+    return GIMBAL_OK;
+  }
+  // second run: record the step as a graph, then launch it
+  {
+    DeviceGuard g(h->device);
+    GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (auto& pr : h->g_tev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    h->g_tev.clear();
+    h->g_pending = false;
+    GIMBAL_CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+    h->capturing = true;
+    const int st = eager();
+    h->capturing = false;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+    if (st != GIMBAL_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    GIMBAL_CUDA_TRY(ce);
+    const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    GIMBAL_CUDA_TRY(ie);
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard g(h->device);
+  GIMBAL_CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
+  h->g_pending = h->timing && !h->g_tev.empty();
   return GIMBAL_OK;
 }
 

@@ -16,8 +16,9 @@
 // per chunk), which puts those 32 words on 32 different banks (a hot expert shared by the warp's
 // tokens costs one wavefront, not eight).  A and B use the same token -> K mapping, so the
 // contraction is unchanged.  Each builder thread owns one token: two id words from the TMA-staged
-// trace rows, atomicOr of a nibble for each of its ids that falls in this CTA's half (about 4 of
-// 8 per layer), then a 16-byte-store share of zeroing the stage two tiles ahead.
+// trace rows (two-layer [256][2] boxes: one 16-byte load for even l, two conflict-free 8-byte loads
+// for odd l), a predicated red.shared.or of a nibble for each of its ids that falls in this CTA's
+// half (about 4 of 8 per layer), then a 16-byte-store share of zeroing the stage two tiles ahead.
 //
 // Warp roles (320 threads per CTA): warp 0 lane 0 = TMA producer of the id tiles (each CTA loads
 // its own), warp 1 = TMEM allocation + (leader CTA) the MMA issuer, warps 2-9 = builders (warp
@@ -52,8 +53,8 @@ constexpr int kLbo = 144;                        // 32-token K chunk stride (128
 constexpr int kSbo = 7 * kLbo + 128;             // 8-expert row group stride (1136 B)
 constexpr int kHalfBytes = (128 / 8) * kSbo;     // 128 rows x 256 tokens, 18176 B
 constexpr int kStageBytes = 2 * kHalfBytes;      // A half + B half
-constexpr int kIdCols = 4;                       // TMA box: layers (l & ~1) .. +3 (16-B aligned start)
-constexpr int kIdSlotBytes = kTok * kIdCols * 8; // 8 KB
+constexpr int kIdCols = 2;                       // TMA box: two layers (16 B per token; 16-B aligned start)
+constexpr int kIdSlotBytes = 2 * kTok * kIdCols * 8;  // 8 KB: one box (even l) or two (odd l)
 constexpr int kSmemBytes = kStages * kStageBytes + kIdSlots * kIdSlotBytes;
 constexpr uint32_t kSfCol = 256;                 // scale factors: columns 256 .. 319
 constexpr int64_t kMaxRangeTokens = (1 << 24) - kTok;
@@ -91,8 +92,19 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
   return r;
 }
+// Arrive on a (possibly remote) barrier of the pair without a release fence: a cluster-scope
+// release compiles to MEMBAR.ALL.GPU (measured: a fifth of all stall samples).  What the waiter needs
+// ordered is this CTA's own completed work -- operand stores made visible to the tensor core by
+// each writer's fence.proxy.async, or TMEM reads retired by tcgen05.wait::ld -- before the arrive
+// is issued, which those fences already guarantee.
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// predicated shared-memory OR without a return value (no branch per id slot)
+__device__ __forceinline__ void or_if(bool p, uint32_t saddr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
+               "r"((uint32_t)p)
+               : "memory");
 }
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -213,8 +225,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int64_t t0 = t_begin; t0 < t_end; t0 += kTok, ++f) {
           const uint32_t s = f % kIdSlots;
           if (f >= kIdSlots) mbar_wait(&id_empty[s], ((f / kIdSlots) - 1) & 1);
-          mbar_arrive_expect_tx(&id_full[s], kIdSlotBytes);
+          // even l: layers (l, l + 1) as one [256][2] box; odd l: (l - 1, l) and (l + 1, l + 2)
+          mbar_arrive_expect_tx(&id_full[s], kTok * 16 * ((l & 1) + 1));
           tma_load_2d(ids_base + s * kIdSlotBytes, &tmap, &id_full[s], l & ~1, (int)t0);
+          if (l & 1) tma_load_2d(ids_base + s * kIdSlotBytes + kTok * 16, &tmap, &id_full[s], l + 1, (int)t0);
         }
       }
     }
@@ -259,9 +273,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (uint32_t i = 0; i < n_tiles; ++i, ++it) {
         const uint32_t slot = it % kIdSlots, s = it % kStages;
         mbar_wait(&id_full[slot], (it / kIdSlots) & 1);
-        const unsigned long long* row =
-            reinterpret_cast<const unsigned long long*>(ids_base + slot * kIdSlotBytes) + bt * kIdCols;
-        const unsigned long long cur = row[l & 1], nxt = row[(l & 1) + 1];
+        const unsigned long long* box = reinterpret_cast<const unsigned long long*>(ids_base + slot * kIdSlotBytes);
+        unsigned long long cur, nxt;
+        if (l & 1) {  // 16-byte row stride: two conflict-free 8-byte loads
+          cur = box[bt * 2 + 1];
+          nxt = box[kTok * 2 + bt * 2];
+        } else {      // one 16-byte load
+          const ulonglong2 v = reinterpret_cast<const ulonglong2*>(box)[bt];
+          cur = v.x;
+          nxt = v.y;
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&id_empty[slot]);
         uint8_t* A = smem + s * kStageBytes;
@@ -276,15 +297,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int b = 0; b < 8; ++b) atomicAdd(El + j * kNe + id_byte(nxt, b), 1ull);
             }
           } else {
+            const uint32_t a_s = smem_u32(A), b_s = smem_u32(B);
 #pragma unroll
             for (int a = 0; a < 8; ++a) {
               const uint32_t j = id_byte(cur, a);
-              if ((j >> 7) == rank) atomicOr(reinterpret_cast<uint32_t*>(A + word_off(j & 127u, lane)), nib);
+              or_if((j >> 7) == rank, a_s + word_off(j & 127u, lane), nib);
             }
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
               const uint32_t k = id_byte(nxt, b);
-              if ((k >> 7) == rank) atomicOr(reinterpret_cast<uint32_t*>(B + word_off(k & 127u, lane)), nib);
+              or_if((k >> 7) == rank, b_s + word_off(k & 127u, lane), nib);
             }
           }
         }

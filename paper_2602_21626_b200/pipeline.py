@@ -195,11 +195,42 @@ class HotPath:
         out, am = eval_costs(self.stats, candidates, self.alpha, self.beta, out=self._scores(candidates.shape[0]))
         return HotPathResult(affinity=M, greedy=gp.assign, argmin=am)
 
-    def run(self, trace, candidates, greedy_row: bool = True) -> HotPathResult:
-        """One full pass over a trace (CUDA uint8 [T][L][k] or host array)."""
+    def run(self, trace, candidates, greedy_row: bool = True, graph: bool = True) -> HotPathResult:
+        """One full pass over a trace (CUDA uint8 [T][L][k] or host array).  With a device trace and
+        device candidates the step goes through gimbal_pass_graph: recorded once as a CUDA graph
+        and replayed while the buffers stay the same (their contents may change)."""
+        if (graph and greedy_row and getattr(trace, "is_cuda", False) and getattr(candidates, "is_cuda", False)
+                and candidates.shape[0] > 0 and self.topo.n_gpus <= 255 and trace.is_contiguous()
+                and str(trace.dtype) in ("torch.uint8", "torch.int32") and trace.numel() > 0):
+            return self._run_graph(trace, candidates)
         self.stats.reset()
         self.stats.add_tokens(trace)
         return self.place(candidates, greedy_row)
+
+    def _run_graph(self, trace, candidates) -> HotPathResult:
+        import torch
+
+        topo = self.topo
+        m, C_ = topo.total_experts(), int(candidates.shape[0])
+        per = topo.n_layers * topo.top_k
+        if trace.numel() % per:
+            raise ValueError("add_token: choice span size mismatch")
+        self._ensure_pk()
+        scores = self._scores(C_)
+        st = self.stats
+        st._after_torch(trace)
+        st._after_torch(candidates)
+        base = self._pk.data_ptr()
+        N.check(N.lib().gimbal_pass_graph(
+            st.handle, C.c_void_p(trace.data_ptr()), 1 if trace.dtype == torch.uint8 else 4, trace.numel() // per,
+            self.threshold, self.top_e, m // topo.n_gpus, self.anchor_gpu, C.c_void_p(candidates.data_ptr()), C_,
+            self.alpha, self.beta, C.c_void_p(scores.data_ptr()), C.c_void_p(base), C.c_void_p(base + 24 + 4 * m),
+            C.c_void_p(base + 24), C.c_void_p(base + 8), C.c_void_p(base + 16)), "pass_graph")
+        st._keep_until_done(trace, N.MEM_DEVICE)
+        h = self._read_pk()
+        n = int(h[2])
+        return HotPathResult(affinity=AffinitySet(experts=h[6:6 + n].tolist(), anchor_gpu=self.anchor_gpu),
+                             greedy=h[6 + m:6 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
 
     def calibrate(self, trace) -> AffinitySet:
         """Offline calibration (sim.cpp:91-106): stats over a calibration trace -> strong-pair set."""

@@ -678,3 +678,34 @@ def test_eval_excess_matches_oracle(G, orc, shape, T, C):
     bad[1, 3] = g
     with pytest.raises(ValueError):
         G.eval_excess(s, bad)
+
+
+@pytest.mark.parametrize("shape", ["mixtral", "dsv2lite", "dsv3"])
+def test_graph_replayed_pass_matches_oracle(G, orc, shape):
+    """HotPath.run's graph path (gimbal_pass_graph): eager on the first call, recorded on the second,
+    replayed after; new trace / candidate contents in the same buffers give the oracle's answers on
+    every call, and the counting kernel stays timed through the replays."""
+    L, ne, k, g = SHAPES[shape]
+    topo = G.MoeTopology(L, ne, k, g)
+    T, C = 12001, 40
+    trace = torch.empty((T, L, k), dtype=torch.uint8, device="cuda")
+    cands = torch.empty((C, L * ne), dtype=torch.uint8, device="cuda")
+    hp = G.HotPath(topo, 0)
+    hp.stats.count_timing(True)
+    for it in range(4):
+        trace.copy_(G.generate_trace(topo, T, model_seed=1, stream_seed=10 + it, device=0))
+        cands.copy_(torch.from_numpy(G.shuffled_candidates(L * ne, g, 50 + it, C)))
+        want_cands = cands.cpu().numpy()
+        res = hp.run(trace, cands)
+        oA, oE, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+        M = list(orc.affinity_set(L, ne, g, oE, 0.0, 4, L * ne // g, 0))
+        greedy = orc.greedy_place(L, ne, g, oA, M, 0)
+        want_cands[0] = greedy
+        D, cut, obj, am = orc.eval_costs(L, ne, g, oA, oE, want_cands)
+        assert res.affinity.experts == M and res.greedy == list(greedy) and res.argmin == am, f"call {it}"
+        sc = hp._out.cpu().numpy()
+        assert np.array_equal(sc[0], D) and np.array_equal(sc[1], cut) and np.array_equal(sc[2], obj)
+        A, E, _ = hp.stats.read()
+        assert np.array_equal(A, oA) and np.array_equal(E, oE) and hp.stats.tokens() == T
+    ms, launches = hp.stats.count_timing(False)
+    assert launches == 4 and ms > 0
