@@ -16,13 +16,14 @@
 // per chunk), which puts those 32 words on 32 different banks (a hot expert shared by the warp's
 // tokens costs one wavefront, not eight).  A and B use the same token -> K mapping, so the
 // contraction is unchanged.  Each builder thread owns one token: two id words from the TMA-staged
-// trace rows (two-layer [256][2] boxes: one 16-byte load for even l, two conflict-free 8-byte loads
-// for odd l), a predicated red.shared.or of a nibble for each of its ids that falls in this CTA's
-// half (about 4 of 8 per layer), then a 16-byte-store share of zeroing the stage two tiles ahead.
+// trace rows (two-layer [256][2] boxes: one 16-byte load for even l, two 8-byte loads for odd l);
+// builder warps 2-9 OR a nibble into the A half for each of the token's layer-l ids that falls in
+// this CTA's half (about 4 of 8), warps 10-17 the same for layer l + 1 into the B half, and all 16
+// take a 16-byte-store share of zeroing the stage two tiles ahead.
 //
-// Warp roles (320 threads per CTA): warp 0 lane 0 = TMA producer of the id tiles (each CTA loads
-// its own), warp 1 = TMEM allocation + (leader CTA) the MMA issuer, warps 2-9 = builders (warp
-// 2 + q builds nibble q of every word), of which warps 2-5 (one per TMEM lane quarter) also drain
+// Warp roles (576 threads per CTA): warp 0 lane 0 = TMA producer of the id tiles (each CTA loads
+// its own), warp 1 = TMEM allocation + (leader CTA) the MMA issuer, warps 2-17 = builders (warps
+// 2 + q and 10 + q build nibble q of every word), of which warps 2-5 (one per TMEM lane quarter) also drain
 // the accumulator into the u64 tensor at the end of each unit.  Barriers: id_full / id_empty
 // (TMA ring, per CTA), stage_full (both CTAs' builders -> the leader's issuer, remote arrives),
 // stage_empty (tcgen05.commit multicast to both CTAs), acc_full (commit multicast, last tile of a
@@ -47,11 +48,11 @@ constexpr int kNe = 256;
 constexpr int kTok = 256;                        // tokens per tile (four K = 64 MMAs)
 constexpr int kStages = 4;                       // operand stages
 constexpr int kIdSlots = 4;                      // id tile ring
-constexpr int kBuilders = 8;                     // builder warps (one nibble slot each)
+constexpr int kBuilders = 16;                    // builder warps: 8 for A (layer l), 8 for B (layer l + 1)
 constexpr int kThreads = (2 + kBuilders) * 32;
-constexpr int kLbo = 144;                        // 32-token K chunk stride (128 B + 16 B gap)
-constexpr int kSbo = 7 * kLbo + 128;             // 8-expert row group stride (1136 B)
-constexpr int kHalfBytes = (128 / 8) * kSbo;     // 128 rows x 256 tokens, 18176 B
+constexpr int kSbo = 128;                        // 8-expert row groups adjacent: row r at r * 16
+constexpr int kLbo = 16 * 128 + 16;              // 32-token K chunk stride (2048 B + a 16 B gap)
+constexpr int kHalfBytes = 8 * kLbo;             // 128 rows x 256 tokens, 16512 B
 constexpr int kStageBytes = 2 * kHalfBytes;      // A half + B half
 constexpr int kIdCols = 2;                       // TMA box: two layers (16 B per token; 16-B aligned start)
 constexpr int kIdSlotBytes = 2 * kTok * kIdCols * 8;  // 8 KB: one box (even l) or two (odd l)
@@ -99,12 +100,6 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
 // is issued, which those fences already guarantee.
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// predicated shared-memory OR without a return value (no branch per id slot)
-__device__ __forceinline__ void or_if(bool p, uint32_t saddr, uint32_t v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v),
-               "r"((uint32_t)p)
-               : "memory");
 }
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -161,9 +156,25 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, uint32_t v) {
       : "memory");
 }
 
-// byte offset of word w (tokens w + 32 q) of expert row r in a half tile
-__device__ __forceinline__ uint32_t word_off(uint32_t r, uint32_t w) {
-  return (r >> 3) * kSbo + (w >> 2) * kLbo + (r & 7) * 16 + (w & 3) * 4;
+// byte offset of word w (tokens w + 32 q) of expert row r < 128 in a half tile: r * 16 plus a
+// per-lane constant; the 16-byte gap per chunk puts word w of a row on bank (c + w) mod 32
+__device__ __forceinline__ uint32_t lane_off(uint32_t w) { return (w >> 2) * kLbo + (w & 3) * 4; }
+
+// For each of the 8 id bytes of w: x = id ^ (rank << 7) is < 128 exactly when the id falls in
+// this CTA's half; min(x, 128) turns the other ids into "row 128", whose word at `base` + 2048 is the
+// 16-byte gap after the chunk -- never read by the MMA -- so every lane issues its 8 ORs without a
+// branch or predicate (ptxas turns predicated shared atomics into branch regions).
+__device__ __forceinline__ void or_ids(unsigned long long w, uint32_t rank_bits, uint32_t base, uint32_t nib) {
+  asm volatile(
+      "{\n\t.reg .b32 lo, hi, x, a;\n\t"
+      "mov.b64 {lo, hi}, %0;\n\t"
+#define GIMBAL_OR_ONE(SRC, SEL) \
+  "prmt.b32 x, " SRC ", 0, " SEL "; xor.b32 x, x, %1; min.u32 x, x, 128; mad.lo.u32 a, x, 16, %2; red.shared.or.b32 [a], %3;\n\t"
+      GIMBAL_OR_ONE("lo", "0x4440") GIMBAL_OR_ONE("lo", "0x4441") GIMBAL_OR_ONE("lo", "0x4442") GIMBAL_OR_ONE("lo", "0x4443")
+      GIMBAL_OR_ONE("hi", "0x4440") GIMBAL_OR_ONE("hi", "0x4441") GIMBAL_OR_ONE("hi", "0x4442") GIMBAL_OR_ONE("hi", "0x4443")
+#undef GIMBAL_OR_ONE
+      "}" ::"l"(w), "r"(rank_bits), "r"(base), "r"(nib)
+      : "memory");
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -258,9 +269,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- builders (+ accumulator drain on warps 2-5) ----------------
-    const int q = warp - 2;
+    // warps 2-9 set layer l's ids in the A half, warps 10-17 layer l + 1's in the B half
+    const bool role_b = warp >= 2 + kBuilders / 2;
+    const int q = (warp - 2) & (kBuilders / 2 - 1);
     const uint32_t nib = 2u << (4 * q);  // e2m1 1.0 at nibble q of the word
     const int bt = q * 32 + lane;        // this thread's token within a tile
+    const int btid = tid - 64;           // 0 .. 511 among the builders
+    const uint32_t rank_bits = rank << 7;
     const uint32_t leader_full0 = leader_addr(&stage_full[0]);
     const uint32_t leader_acc_empty = leader_addr(&acc_empty);
     uint32_t it = 0, units = 0;
@@ -285,29 +300,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&id_empty[slot]);
-        uint8_t* A = smem + s * kStageBytes;
-        uint8_t* B = A + kHalfBytes;
+        const uint32_t half = smem_u32(smem + s * kStageBytes) + (role_b ? kHalfBytes : 0u);
         if (t_begin + (int64_t)i * kTok + bt < t_end) {
-          if (has_dup8(cur) | has_dup8(nxt)) {  // multiplicity: straight to the u64 tensor
+          if (has_dup8(cur) | has_dup8(nxt)) {  // multiplicity: straight to the u64 tensor (A role)
+            if (!role_b) {
 #pragma unroll 1
-            for (int a = 0; a < 8; ++a) {
-              const uint32_t j = id_byte(cur, a);
-              if ((j >> 7) != rank) continue;
+              for (int a = 0; a < 8; ++a) {
+                const uint32_t j = id_byte(cur, a);
+                if ((j >> 7) != rank) continue;
 #pragma unroll 1
-              for (int b = 0; b < 8; ++b) atomicAdd(El + j * kNe + id_byte(nxt, b), 1ull);
+                for (int b = 0; b < 8; ++b) atomicAdd(El + j * kNe + id_byte(nxt, b), 1ull);
+              }
             }
           } else {
-            const uint32_t a_s = smem_u32(A), b_s = smem_u32(B);
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-              const uint32_t j = id_byte(cur, a);
-              or_if((j >> 7) == rank, a_s + word_off(j & 127u, lane), nib);
-            }
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-              const uint32_t k = id_byte(nxt, b);
-              or_if((k >> 7) == rank, b_s + word_off(k & 127u, lane), nib);
-            }
+            or_ids(role_b ? nxt : cur, rank_bits, half + lane_off((uint32_t)lane), nib);
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -318,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t g2 = it + 2, s2 = g2 % kStages;
           if (g2 >= kStages) mbar_wait(&stage_empty[s2], ((g2 / kStages) - 1) & 1);
           uint4* z = reinterpret_cast<uint4*>(smem + s2 * kStageBytes);
-          for (int w = bt; w < kStageBytes / 16; w += kBuilders * 32) z[w] = make_uint4(0, 0, 0, 0);
+          for (int w = btid; w < kStageBytes / 16; w += kBuilders * 32) z[w] = make_uint4(0, 0, 0, 0);
         }
         named_sync(1, kBuilders * 32);
       }
