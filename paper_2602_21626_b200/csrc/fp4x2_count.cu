@@ -101,6 +101,18 @@ __device__ __forceinline__ uint32_t leader_addr(const void* p) {
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Zero the operand bytes of a stage (the 2048-byte chunk bodies of both halves; the 16-byte gaps
+// only ever receive the out-of-half ORs and are never read): 4 x 16 B per builder thread.
+__device__ __forceinline__ void zero_stage(uint8_t* stage, int btid) {
+  static_assert(2 * 8 * 2048 / 16 == 4 * kBuilders * 32, "exact split");
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int v = btid + r * kBuilders * 32;       // 16-byte vector 0 .. 2047
+    const int h = v >> 10, c = (v >> 7) & 7, o = v & 127;
+    *reinterpret_cast<uint4*>(stage + h * kHalfBytes + c * kLbo + o * 16) = make_uint4(0, 0, 0, 0);
+  }
+}
+
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
@@ -181,7 +193,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     count_fp4x2_kernel(const __grid_constant__ CUtensorMap tmap, Fp4x2Params prm, unsigned long long* __restrict__ E) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t id_full[kIdSlots], id_empty[kIdSlots];
-  __shared__ uint64_t stage_full[kStages], stage_empty[kStages];
+  __shared__ uint64_t stage_full[kStages], stage_empty[kStages], zeroed[kStages];
   __shared__ uint64_t acc_full, acc_empty;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -196,6 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&stage_full[s], 2 * kBuilders);  // both CTAs' builder warps (leader's copy is used)
       mbar_init(&stage_empty[s], 1);
+      mbar_init(&zeroed[s], kBuilders);  // every builder warp's share of zeroing the stage is done
     }
     mbar_init(&acc_full, 1);
     mbar_init(&acc_empty, 2 * 4);  // the four drain warps of both CTAs
@@ -206,8 +219,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
-  // stages 0 and 1 start zeroed; every later stage is zeroed two tiles ahead of its use
-  for (int i = tid; i < 2 * kStageBytes / 16; i += kThreads) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -277,6 +288,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int btid = tid - 64;           // 0 .. 511 among the builders
     const uint32_t rank_bits = rank << 7;
     const uint32_t leader_full0 = leader_addr(&stage_full[0]);
+    for (int s0 = 0; s0 < 2; ++s0) {  // the first two stages; later ones two tiles ahead of use
+      zero_stage(smem + s0 * kStageBytes, btid);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&zeroed[s0]);
+    }
     const uint32_t leader_acc_empty = leader_addr(&acc_empty);
     uint32_t it = 0, units = 0;
     for (int64_t u = cl; u < prm.n_units; u += ncl, ++units) {
@@ -289,31 +305,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t slot = it % kIdSlots, s = it % kStages;
         mbar_wait(&id_full[slot], (it / kIdSlots) & 1);
         const unsigned long long* box = reinterpret_cast<const unsigned long long*>(ids_base + slot * kIdSlotBytes);
-        unsigned long long cur, nxt;
-        if (l & 1) {  // 16-byte row stride: two conflict-free 8-byte loads
+        unsigned long long cur = 0, nxt;
+        if (role_b) {  // layer l + 1 only
+          nxt = (l & 1) ? box[kTok * 2 + bt * 2] : box[bt * 2 + 1];
+        } else if (l & 1) {  // 16-byte row stride: two 8-byte loads
           cur = box[bt * 2 + 1];
           nxt = box[kTok * 2 + bt * 2];
-        } else {      // one 16-byte load
+        } else {             // one 16-byte load
           const ulonglong2 v = reinterpret_cast<const ulonglong2*>(box)[bt];
           cur = v.x;
           nxt = v.y;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&id_empty[slot]);
+        // this tile's stage was zeroed during tile it - 2 (the first two at the start)
+        mbar_wait(&zeroed[s], (it / kStages) & 1);
         const uint32_t half = smem_u32(smem + s * kStageBytes) + (role_b ? kHalfBytes : 0u);
         if (t_begin + (int64_t)i * kTok + bt < t_end) {
-          if (has_dup8(cur) | has_dup8(nxt)) {  // multiplicity: straight to the u64 tensor (A role)
-            if (!role_b) {
+          if (role_b) {
+            // a token the A role sends to the u64 path contributes A row 0 to the MMA, so its
+            // B nibbles are harmless: no duplicate check here
+            or_ids(nxt, rank_bits, half + lane_off((uint32_t)lane), nib);
+          } else if (has_dup8(cur) | has_dup8(nxt)) {  // multiplicity: straight to the u64 tensor
 #pragma unroll 1
-              for (int a = 0; a < 8; ++a) {
-                const uint32_t j = id_byte(cur, a);
-                if ((j >> 7) != rank) continue;
+            for (int a = 0; a < 8; ++a) {
+              const uint32_t j = id_byte(cur, a);
+              if ((j >> 7) != rank) continue;
 #pragma unroll 1
-                for (int b = 0; b < 8; ++b) atomicAdd(El + j * kNe + id_byte(nxt, b), 1ull);
-              }
+              for (int b = 0; b < 8; ++b) atomicAdd(El + j * kNe + id_byte(nxt, b), 1ull);
             }
           } else {
-            or_ids(role_b ? nxt : cur, rank_bits, half + lane_off((uint32_t)lane), nib);
+            or_ids(cur, rank_bits, half + lane_off((uint32_t)lane), nib);
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -323,10 +345,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         {
           const uint32_t g2 = it + 2, s2 = g2 % kStages;
           if (g2 >= kStages) mbar_wait(&stage_empty[s2], ((g2 / kStages) - 1) & 1);
-          uint4* z = reinterpret_cast<uint4*>(smem + s2 * kStageBytes);
-          for (int w = btid; w < kStageBytes / 16; w += kBuilders * 32) z[w] = make_uint4(0, 0, 0, 0);
+          zero_stage(smem + s2 * kStageBytes, btid);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&zeroed[s2]);
         }
-        named_sync(1, kBuilders * 32);
       }
       if (warp < 6) {
         // drain: this CTA's 128 rows (experts 128 rank + TMEM lane) x 256 columns -> u64 E
