@@ -514,12 +514,12 @@ int gimbal_stats_create(const gimbal_topology* topo, int device, gimbal_stats_t*
   const int64_t nW = (int64_t)topo->n_experts * topo->n_experts;
   const int64_t nE = std::max<int64_t>(h->nE(), 1);
   if (cudaMalloc(&h->dE, nE * 8) != cudaSuccess || cudaMalloc(&h->dA, nA * 8) != cudaSuccess ||
-      cudaMalloc(&h->dW, nW * 8) != cudaSuccess || cudaMalloc(&h->dflags, 64) != cudaSuccess) {
+      cudaMalloc(&h->dW, nW * 8) != cudaSuccess || cudaMalloc(&h->dflags, kFlagAllocBytes) != cudaSuccess) {
     set_error("gimbal_stats_create: device allocation failed");
     return fail(GIMBAL_CUDA_ERROR);
   }
   *out = h;
-  if (cudaMemset(h->dflags, 0, 64) != cudaSuccess) {
+  if (cudaMemset(h->dflags, 0, kFlagAllocBytes) != cudaSuccess) {
     *out = nullptr;
     set_error("gimbal_stats_create: flag init failed");
     return fail(GIMBAL_CUDA_ERROR);

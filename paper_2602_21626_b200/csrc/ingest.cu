@@ -658,6 +658,11 @@ bool encode_trace_map(CUtensorMap* map, const uint8_t* trace, int64_t T, int L, 
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+int pace_tiles(int dflt) {
+  if (const char* e = GIMBAL_KNOB("GIMBAL_PACE")) return std::max(0, std::atoi(e));
+  return dflt;
+}
+
 bool direct_u15_supported(const Lm8Plan& plan, int id_bytes, const void* ids) {
   return plan.u15 && plan.k == 8 && plan.ne == 256 && id_bytes == 1 &&
          (reinterpret_cast<uintptr_t>(ids) & 7) == 0;

@@ -30,6 +30,17 @@ enum KernelFlag : uint32_t {
   kFlagDuplicates = 8u,  // not an error: some token-layer repeats an id (multiplicity > 1)
 };
 
+// A handle's flag words (64 B) are followed by the pacing counters of its counting kernels
+// (ptx.cuh pace_arrive_wait): flags + kPaceOffset, kPaceWords of them, zeroed by the launcher
+// before each kernel that paces its CTAs.
+constexpr int kPaceOffset = 16;
+constexpr int kPaceWords = 1024;
+constexpr size_t kFlagAllocBytes = (size_t)(kPaceOffset + kPaceWords) * 4;
+constexpr uint64_t kPaceTimeoutNs = 300000;
+// Tiles (or blocks) per pacing epoch for a counting kernel: `dflt`, or the AB knob GIMBAL_PACE
+// (0 = no pacing) in the test/tool build.
+int pace_tiles(int dflt);
+
 #define GIMBAL_CUDA_TRY(expr)                                                          \
   do {                                                                                 \
     cudaError_t e_ = (expr);                                                           \

@@ -56,6 +56,8 @@ struct MmaParams {
   int64_t T, ld;
   uint32_t idesc;
   uint32_t* flags;  // LM8: kFlagDuplicates from the transposition; token-major: id errors raised here
+  uint32_t* pace;   // per-range pacing counters (token-major path), or null
+  int pace_tiles;   // tiles per pacing epoch
 };
 
 // Shared-memory matrix descriptor: no swizzle, MN-major.  Core matrix = 8 K-rows of 16 bytes;
@@ -141,6 +143,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     auto fetch = [&](int it) {
       const uint32_t slot = fill_count % kIdSlots;
       if (TM && threadIdx.x == 0) {
+        // the groups of one token range read the same trace rows: keep them within an epoch of
+        // each other so every row is fetched from HBM once and served to the others from L2
+        if (prm.pace != nullptr && it > 0 && it % prm.pace_tiles == 0)
+          pace_arrive_wait(prm.pace + range, (uint32_t)(prm.n_groups * (it / prm.pace_tiles)), kPaceTimeoutNs);
         const int64_t t0 = t_begin + (int64_t)it * kTok;
         mbar_arrive_expect_tx(&id_bars[slot], kTok * kIdCols * 8);
         tma_load_2d(ids + slot * kIdSlotWords, &tmap, &id_bars[slot], l0 & ~1, (int)t0);
@@ -271,6 +277,8 @@ MmaParams make_params(int L, int ne, int k, int sms, int64_t T, int64_t ld, uint
   prm.T = T;
   prm.ld = ld;
   prm.flags = flags;
+  prm.pace = nullptr;
+  prm.pace_tiles = 0;
   // c = s32, a = b = u8, a and b MN-major, N >> 3 at bit 17, M >> 4 at bit 24
   prm.idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(prm.N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
   int64_t ranges = std::max<int64_t>(1, kCtasPerSm * sms / prm.n_groups);
@@ -318,7 +326,16 @@ cudaError_t launch_count_mma_direct(int L, int ne, int sms, const uint8_t* trace
   if (!mma_count_supported(L, ne, 8) || !encode_trace_map(&tmap, trace, T, L, kIdCols, kTok))
     return cudaErrorNotSupported;
   int grid = 0;
-  const MmaParams prm = make_params(L, ne, 8, sms, T, 0, flags, &grid);
+  MmaParams prm = make_params(L, ne, 8, sms, T, 0, flags, &grid);
+  // pacing needs every group of a range resident together: whole ranges per wave of units
+  const int64_t ranges = prm.n_units / prm.n_groups;
+  const int pt = pace_tiles(0);  // off: profiles/r2_pacing_ab.md
+  if (pt > 0 && grid % prm.n_groups == 0 && ranges <= kPaceWords && prm.range_tokens >= 2 * pt * kTok) {
+    prm.pace = flags + kPaceOffset;
+    prm.pace_tiles = pt;
+    cudaError_t e = cudaMemsetAsync(prm.pace, 0, (size_t)ranges * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   return launch_k<8, true>(tmap, prm, nullptr, E, s, grid);
 }
 

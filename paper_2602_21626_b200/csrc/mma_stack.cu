@@ -54,6 +54,8 @@ struct StackParams {
   int64_t n_units, range_tokens, T;
   uint32_t idesc;
   uint32_t* flags;
+  uint32_t* pace;  // per-range pacing counters (the groups of a range read the same rows), or null
+  int pace_tiles;
 };
 
 __device__ __forceinline__ uint64_t operand_desc(uint32_t saddr, uint32_t k_stride) {
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
     auto fetch = [&](int it) {  // called by every thread (fills stays uniform)
       if (threadIdx.x == 0) {
+        if (prm.pace != nullptr && it > 0 && it % prm.pace_tiles == 0)
+          pace_arrive_wait(prm.pace + range, (uint32_t)(prm.n_groups * (it / prm.pace_tiles)), kPaceTimeoutNs);
         const uint32_t slot = fills % kIdSlots;
         uint8_t* dst = ids + slot * prm.id_slot_bytes;
         const int64_t t0 = t_begin + (int64_t)it * kTok;
@@ -272,6 +276,8 @@ bool make_params(int L, int k, int sms, int max_smem, int64_t T, uint32_t* flags
   }
   prm->T = T;
   prm->flags = flags;
+  prm->pace = nullptr;
+  prm->pace_tiles = 0;
   // c = s32, a = b = u8, both MN-major; N >> 3 at bit 17, M >> 4 at bit 24
   prm->idesc = (2u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(kNe >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   // ranges x groups ~ 2 waves of units; s32 accumulators hold tokens * k^2 < 2^31 per unit
@@ -312,6 +318,16 @@ cudaError_t launch_count_mma_stack(int L, int ne, int k, int sms, int max_smem, 
   int grid = 0;
   size_t smem = 0;
   if (!make_params(L, k, sms, max_smem, T, flags, &prm, &grid, &smem)) return cudaErrorNotSupported;
+  // pacing needs every group of a range resident together: whole ranges per wave of units
+  const int64_t ranges = prm.n_units / prm.n_groups;
+  const int pt = pace_tiles(0);  // off: profiles/r2_pacing_ab.md
+  if (pt > 0 && prm.n_groups > 1 && grid % prm.n_groups == 0 && ranges <= kPaceWords &&
+      prm.range_tokens >= 2 * pt * kTok) {
+    prm.pace = flags + kPaceOffset;
+    prm.pace_tiles = pt;
+    cudaError_t e = cudaMemsetAsync(prm.pace, 0, (size_t)ranges * 4, s);
+    if (e != cudaSuccess) return e;
+  }
   switch (k) {
     case 1: return launch_k<1>(prm, trace, E, s, grid, smem);
     case 2: return launch_k<2>(prm, trace, E, s, grid, smem);

@@ -45,6 +45,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Pacing barrier among the CTAs that read the same trace rows (the units of one token range):
+// arrive on the counter, then wait until `target` arrivals, so no CTA runs more than one epoch
+// ahead of the others and the rows they share are still in L2 when the last one reads them.  No
+// data passes through it (relaxed ordering suffices), so it is only a speed hint: the wait gives
+// up after `timeout_ns` (co-residency is not guaranteed when other kernels share the GPU).
+__device__ __forceinline__ void pace_arrive_wait(uint32_t* ctr, uint32_t target, uint64_t timeout_ns) {
+  atomicAdd(ctr, 1u);
+  if (*reinterpret_cast<volatile uint32_t*>(ctr) >= target) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (*reinterpret_cast<volatile uint32_t*>(ctr) < target) {
+    if (globaltimer_ns() - t0 > timeout_ns) break;
+    __nanosleep(256);
+  }
+}
+
 // ---- packed top-8 uint8 id words (one u64 per token-layer) ----
 
 __device__ __forceinline__ uint32_t id_byte(unsigned long long w, int a) {
