@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define GIMBAL_ABI_VERSION 3
+#define GIMBAL_ABI_VERSION 4
 
 typedef enum gimbal_status {
   GIMBAL_OK = 0,
@@ -178,6 +178,24 @@ int gimbal_pass_graph(gimbal_stats_t h, const void* ids_device, int id_bytes, in
                       int64_t n_candidates, double alpha, double beta, double* scores_device, int64_t* argmin_device,
                       int32_t* placement_device, int32_t* members_device, int32_t* n_members_device,
                       uint32_t* flags_device);
+
+/* gimbal_pass_graph as one queued unit for back-to-back passes from a host that owns another
+ * stream (a framework's current stream): the handle's stream first waits for caller_stream (the
+ * inputs may still be being written there), the pass replays, its packed results
+ *   [argmin (int64) | |M| (int32) | pad | error words 0-1 (uint32) | M (m x int32) | greedy (m x int32)]
+ * (6 + 2m int32 words; the pass writes them into packed_device) reach host memory, and
+ * caller_stream then waits for all of it (so memory the caller frees afterwards is reused only
+ * behind the pass).  *results_host says where they will be: packed_host (pinned or registered,
+ * same size) after a device-to-host copy queued behind the pass, or -- for the fused small-shape
+ * pass, which writes them into mapped host memory itself -- a slot of the handle's 64-slot ring,
+ * valid until 64 more passes are queued on the handle.  No host synchronisation: the caller
+ * records an event on caller_stream after this returns and reads *results_host once that event has
+ * completed; nonzero error words mean gimbal_stats_sync reports the deferred error.  caller_stream
+ * may be 0 (the legacy default stream) or the handle's own stream (no joins). */
+int gimbal_pass_enqueue(gimbal_stats_t h, const void* ids_device, int id_bytes, int64_t n_tokens, double threshold,
+                        int32_t top_e, int32_t capacity, int32_t anchor_gpu, uint8_t* candidates_device,
+                        int64_t n_candidates, double alpha, double beta, double* scores_device,
+                        int32_t* packed_device, int32_t* packed_host, void* caller_stream, int32_t** results_host);
 
 /* Counting kernels of this handle run on n_sms SMs (default: all).  Leaving SMs free lets a
  * latency-bound kernel on another stream (the previous window's greedy walk) run alongside. */

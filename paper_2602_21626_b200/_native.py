@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GIMBAL_LIB") or os.path.join(HERE, "lib", "libgimbal_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "gimbal_gpu.h")
 
-ABI_VERSION = 3  # include/gimbal_gpu.h GIMBAL_ABI_VERSION
+ABI_VERSION = 4  # include/gimbal_gpu.h GIMBAL_ABI_VERSION
 OK, INVALID_ARGUMENT, CUDA_ERROR, NCCL_ERROR, OVERFLOW, OUT_OF_RANGE, NOT_SUPPORTED = range(7)
 MEM_HOST, MEM_DEVICE = 0, 1
 
@@ -61,6 +61,8 @@ SIGNATURES = [
     ("gimbal_pass_graph", C.c_int, [_P, _P, C.c_int, _i64, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P, _P,
                                     _P]),
     ("gimbal_pass_async", C.c_int, [_P, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P, _P, _P]),
+    ("gimbal_pass_enqueue", C.c_int, [_P, _P, C.c_int, _i64, _d, _i32, _i32, _i32, _P, _i64, _d, _d, _P, _P, _P, _P,
+                                      C.POINTER(_P)]),
     ("gimbal_dist_unique_id", C.c_int, [_P]),
     ("gimbal_dist_comm_init", C.c_int, [_i32, _i32, _P, C.c_int, C.POINTER(_P)]),
     ("gimbal_dist_comm_destroy", C.c_int, [_P]),

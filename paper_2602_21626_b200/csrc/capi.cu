@@ -160,21 +160,62 @@ struct gimbal_stats_s {
   GraphKey gkey;
   int gseen = 0;  // eager runs with gkey (the first allocates every scratch buffer)
   cudaGraphExec_t gexec = nullptr;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_tev;
-  bool g_pending = false;  // a timed replay whose events are not yet harvested
+  cudaGraph_t graph = nullptr;  // kept: its event-record nodes are re-pointed per timed replay
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_tev;        // recorded at capture
+  std::vector<std::pair<cudaGraphNode_t, cudaGraphNode_t>> g_nodes;  // their record nodes
+  // timed replays: every replay records into a fresh event pair (the exec's record nodes are
+  // re-pointed before the launch), so no replay waits on the host for the previous one's timing;
+  // the pairs are read when the timing is collected (or when too many are outstanding)
+  using EvPair = std::pair<cudaEvent_t, cudaEvent_t>;
+  std::vector<EvPair> g_pool, g_inflight;
   double g_ms = 0.0;
   int64_t g_launches = 0;
-  int harvest_graph_timing() {
-    if (!g_pending) return GIMBAL_OK;
-    for (auto& pr : g_tev) {
-      GIMBAL_CUDA_TRY(cudaEventSynchronize(pr.second));
-      float ms = 0.f;
-      GIMBAL_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
-      g_ms += ms;
-      ++g_launches;
+  int harvest_graph_timing(bool accumulate = true) {
+    for (auto& pr : g_inflight) {
+      if (accumulate) {
+        GIMBAL_CUDA_TRY(cudaEventSynchronize(pr.second));
+        float ms = 0.f;
+        GIMBAL_CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+        g_ms += ms;
+        ++g_launches;
+      }
+      g_pool.push_back(pr);
     }
-    g_pending = false;
+    g_inflight.clear();
     return GIMBAL_OK;
+  }
+  // before a timed replay: fresh event pairs into the exec's record nodes
+  int arm_graph_timing() {
+    if (g_inflight.size() >= 4096) GIMBAL_TRY(harvest_graph_timing());
+    for (auto& nd : g_nodes) {
+      EvPair pr;
+      if (!g_pool.empty()) {
+        pr = g_pool.back();
+        g_pool.pop_back();
+      } else {
+        GIMBAL_CUDA_TRY(cudaEventCreate(&pr.first));
+        GIMBAL_CUDA_TRY(cudaEventCreate(&pr.second));
+      }
+      GIMBAL_CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(gexec, nd.first, pr.first));
+      GIMBAL_CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(gexec, nd.second, pr.second));
+      g_inflight.push_back(pr);
+    }
+    return GIMBAL_OK;
+  }
+  void drop_graph() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
+    for (auto* v : {&g_tev, &g_pool, &g_inflight})
+      for (auto& pr : *v) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+      }
+    g_tev.clear();
+    g_pool.clear();
+    g_inflight.clear();
+    g_nodes.clear();
   }
 
   int timing_begin() {
@@ -211,6 +252,31 @@ struct gimbal_stats_s {
   // side stream of gimbal_pass_async: the greedy walk runs there beside the candidate scoring
   cudaStream_t g_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_caller = nullptr, ev_back = nullptr;  // gimbal_pass_enqueue's stream joins
+  // the fused small-shape pass leaves its ticket / bad index ready in `same`: set once per buffer
+  const unsigned long long* tiny_ready_same = nullptr;
+  int64_t tiny_ready_C = -1;
+  bool last_pass_tiny = false;  // the latest gimbal_pass_async took the fused small-shape path
+  // the fused pass writes its packed results into a mapped host ring (slot = device counter
+  // dflags[8] modulo the slots); host_seq mirrors that counter (every executed fused pass, never a
+  // capture), ran_tiny / ring_slot describe the latest executed pass
+  static constexpr int kRingSlots = 64;
+  int32_t* ring_host = nullptr;
+  int32_t* ring_dev = nullptr;
+  uint64_t host_seq = 0;
+  int ring_slot = 0;
+  bool ran_tiny = false;
+  void note_tiny_run() {
+    ring_slot = (int)(host_seq % kRingSlots);
+    ++host_seq;
+    ran_tiny = true;
+  }
+  bool g_uses_tiny = false;     // ... while the replayed graph was being recorded
+  // scratch buffers the recorded graph points into; a replay needs all of them unchanged
+  std::vector<const void*> scratch_snapshot() const {
+    return {cand.p, same.p, dout.p, keys.p, misc.p, ints.p, probe.p, dscr.p, lm8[0], lm8[1]};
+  }
+  std::vector<const void*> g_scratch;
   std::mutex mu;
   // strong-pair set resident in `ints` for the asynchronous window path (streaming windows keep
   // M fixed, sim.cpp:94-104, so it is uploaded once): valid while ints.p == m_cached_buf
@@ -549,13 +615,12 @@ int gimbal_stats_destroy(gimbal_stats_t h) {
       if (h->ev_consumed[b]) cudaEventDestroy(h->ev_consumed[b]);
     }
     if (h->g_stream) cudaStreamSynchronize(h->g_stream);
-    if (h->gexec) cudaGraphExecDestroy(h->gexec);
-    for (auto& pr : h->g_tev) {
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
-    }
+    h->drop_graph();
     for (DevBuf* b : {&h->cand, &h->same, &h->dout, &h->keys, &h->misc, &h->ints, &h->probe, &h->dscr}) b->release();
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_caller) cudaEventDestroy(h->ev_caller);
+    if (h->ring_host) cudaFreeHost(h->ring_host);
+    if (h->ev_back) cudaEventDestroy(h->ev_back);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->t_stream) cudaStreamSynchronize(h->t_stream);
     for (int b = 0; b < gimbal_stats_s::kStages; ++b) {
@@ -720,8 +785,11 @@ int gimbal_stats_count_timing(gimbal_stats_t h, int enable, double* count_ms, in
     if (launches) *launches = (int64_t)h->tev_used + h->g_launches;
   }
   if (enable != (h->timing ? 1 : 0) || enable) {
+    if (!count_ms && !launches) {
+      GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      GIMBAL_TRY(h->harvest_graph_timing(false));  // replays before this point are not counted
+    }
     h->tev_used = 0;
-    h->g_pending = false;
     h->g_ms = 0.0;
     h->g_launches = 0;
   }
@@ -777,6 +845,7 @@ int enqueue_eval(gimbal_stats_t h, const uint8_t* dc, int64_t C, double alpha, d
                  double* dcut, double* dobj, long long* darg, uint32_t* flags) {
   const int L = h->topo.n_layers, ne = h->topo.n_experts, gg = h->topo.n_gpus, k = h->topo.top_k;
   GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
+  h->tiny_ready_same = nullptr;  // the evaluators overwrite the fused pass's ticket words
   GIMBAL_TRY(pick_cell_width(h));
   GIMBAL_CUDA_TRY(launch_eval_costs(L, ne, gg, h->dA, h->dE, dc, C, alpha, beta,
                                     h->same.as<unsigned long long>(), dD, dcut, dobj, darg,
@@ -1072,6 +1141,39 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   }
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard dg(h->device);
+  // small shapes (Mixtral class): the whole pass in one launch when every E cell fits 32 bits
+  // (the token count bounds it: a token adds at most k^2 to a cell)
+  const unsigned long long kk2 = (unsigned long long)h->topo.top_k * (unsigned long long)h->topo.top_k;
+  if (!h->tokens_on_device && h->tokens >= 0 && (unsigned long long)h->tokens * kk2 < (1ull << 32)) {
+    GIMBAL_TRY(h->same.ensure(tiny_scratch_bytes(C)));
+    unsigned long long* same = h->same.as<unsigned long long>();
+    const bool init = h->tiny_ready_same != same || h->tiny_ready_C != C;
+    if (!h->ring_host) {
+      void* host = nullptr;
+      GIMBAL_CUDA_TRY(cudaHostAlloc(&host, (size_t)gimbal_stats_s::kRingSlots * (size_t)(6 + 2 * m) * 4,
+                                    cudaHostAllocMapped));
+      h->ring_host = static_cast<int32_t*>(host);
+      void* dev = nullptr;
+      GIMBAL_CUDA_TRY(cudaHostGetDevicePointer(&dev, host, 0));
+      h->ring_dev = static_cast<int32_t*>(dev);
+    }
+    const cudaError_t e = launch_tiny_pass(
+        h->topo.n_layers, h->topo.n_experts, h->topo.n_gpus, h->topo.top_k, threshold, top_e, capacity, anchor, h->dE,
+        h->dA, candidates, C, alpha, beta, scores, reinterpret_cast<long long*>(argmin), placement, members, n_members,
+        h->dflags, same, init, flags_out, h->ring_dev, h->dflags + 8, gimbal_stats_s::kRingSlots, h->stream);
+    if (e != cudaErrorNotSupported) {
+      GIMBAL_CUDA_TRY(e);
+      h->tiny_ready_same = same;
+      h->tiny_ready_C = C;
+      h->last_pass_tiny = true;
+      if (!h->capturing) h->note_tiny_run();
+      h->derived = true;  // the pass wrote A
+      return GIMBAL_OK;
+    }
+    cudaGetLastError();
+  }
+  h->last_pass_tiny = false;
+  h->ran_tiny = false;
   GIMBAL_TRY(h->derive());
   // scratch sized before anything is queued (a regrown buffer is freed, not stream-ordered)
   GreedyScratch gs{};
@@ -1107,6 +1209,7 @@ int gimbal_pass_async(gimbal_stats_t h, double threshold, int32_t top_e, int32_t
   // The greedy walk (latency-bound, one CTA) runs on the side stream while candidates 1..C-1 are
   // scored on the handle's stream; candidate 0 (the greedy row it writes) is scored after the join.
   GIMBAL_TRY(h->same.ensure(eval_scratch_bytes(C)));
+  h->tiny_ready_same = nullptr;  // the evaluators overwrite the fused pass's ticket words
   GIMBAL_TRY(pick_cell_width(h));
   GIMBAL_CUDA_TRY(cudaEventRecord(h->ev_fork, h->stream));
   GIMBAL_CUDA_TRY(cudaStreamWaitEvent(h->g_stream, h->ev_fork, 0));
@@ -1268,12 +1371,21 @@ int gimbal_pass_graph(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n
   key.n_members = n_members;
   key.flags = flags_out;
   key.sms = h->sms;
-  if (h->gexec && key == h->gkey) {
+  if (h->gexec && key == h->gkey && h->scratch_snapshot() == h->g_scratch) {
     std::lock_guard<std::mutex> lk(h->mu);
     DeviceGuard g(h->device);
-    if (h->timing) GIMBAL_TRY(h->harvest_graph_timing());
+    if (h->g_uses_tiny && (h->tiny_ready_same != h->same.as<unsigned long long>() || h->tiny_ready_C != C)) {
+      // another evaluator call reused the scratch: restore the fused pass's ticket / bad index
+      GIMBAL_CUDA_TRY(cudaMemsetAsync(h->same.as<unsigned long long>() + C, 0x7f, 16, h->stream));
+      h->tiny_ready_same = h->same.as<unsigned long long>();
+      h->tiny_ready_C = C;
+    }
+    if (h->timing) GIMBAL_TRY(h->arm_graph_timing());
     GIMBAL_CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
-    h->g_pending = h->timing && !h->g_tev.empty();
+    if (h->g_uses_tiny)
+      h->note_tiny_run();
+    else
+      h->ran_tiny = false;
     // host-side effects of reset + add_tokens + pass: the counts are the trace's, A derived
     h->tokens = n_tokens;
     h->tokens_on_device = false;
@@ -1289,12 +1401,9 @@ int gimbal_pass_graph(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n
     return gimbal_pass_async(h, threshold, top_e, capacity, anchor, candidates, C, alpha, beta, scores, argmin,
                              placement, members, n_members, flags_out);
   };
-  if (!(key == h->gkey) || h->gseen == 0) {
+  if (!(key == h->gkey) || h->gseen == 0 || (h->gexec && h->scratch_snapshot() != h->g_scratch)) {
     // first run with these arguments: eager (validates, sizes every scratch buffer)
-    if (h->gexec) {
-      cudaGraphExecDestroy(h->gexec);
-      h->gexec = nullptr;
-    }
+    h->drop_graph();
     h->gkey = key;
     h->gseen = 0;
     GIMBAL_TRY(eager());
@@ -1305,12 +1414,7 @@ int gimbal_pass_graph(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n
   {
     DeviceGuard g(h->device);
     GIMBAL_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    for (auto& pr : h->g_tev) {
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
-    }
-    h->g_tev.clear();
-    h->g_pending = false;
+    h->drop_graph();
     GIMBAL_CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
     h->capturing = true;
     const int st = eager();
@@ -1322,14 +1426,82 @@ int gimbal_pass_graph(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n
       return st;
     }
     GIMBAL_CUDA_TRY(ce);
-    const cudaError_t ie = cudaGraphInstantiate(&h->gexec, graph, 0);
-    cudaGraphDestroy(graph);
-    GIMBAL_CUDA_TRY(ie);
+    h->graph = graph;
+    // the record nodes of each timed counting launch (timing_begin / timing_end, in order)
+    size_t n_nodes = 0;
+    GIMBAL_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &n_nodes));
+    std::vector<cudaGraphNode_t> nodes(n_nodes);
+    GIMBAL_CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &n_nodes));
+    h->g_nodes.assign(h->g_tev.size(), {nullptr, nullptr});
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      GIMBAL_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+      if (ty != cudaGraphNodeTypeEventRecord) continue;
+      cudaEvent_t ev = nullptr;
+      GIMBAL_CUDA_TRY(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+      for (size_t i = 0; i < h->g_tev.size(); ++i) {
+        if (h->g_tev[i].first == ev) h->g_nodes[i].first = nd;
+        if (h->g_tev[i].second == ev) h->g_nodes[i].second = nd;
+      }
+    }
+    for (auto& nd : h->g_nodes)
+      if (!nd.first || !nd.second) {
+        set_error("pass_graph: timing record node not found in the captured graph");
+        return GIMBAL_CUDA_ERROR;
+      }
+    // the capture-time events become the first replay's pair
+    for (auto& pr : h->g_tev) h->g_pool.push_back(pr);
+    h->g_tev.clear();
+    h->g_uses_tiny = h->last_pass_tiny;
+    h->g_scratch = h->scratch_snapshot();
+    GIMBAL_CUDA_TRY(cudaGraphInstantiate(&h->gexec, graph, 0));
   }
   std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard g(h->device);
+  if (h->timing) GIMBAL_TRY(h->arm_graph_timing());
   GIMBAL_CUDA_TRY(cudaGraphLaunch(h->gexec, h->stream));
-  h->g_pending = h->timing && !h->g_tev.empty();
+  if (h->g_uses_tiny)
+    h->note_tiny_run();
+  else
+    h->ran_tiny = false;
+  return GIMBAL_OK;
+}
+
+int gimbal_pass_enqueue(gimbal_stats_t h, const void* ids, int id_bytes, int64_t n_tokens, double threshold,
+                        int32_t top_e, int32_t capacity, int32_t anchor, uint8_t* candidates, int64_t C,
+                        double alpha, double beta, double* scores, int32_t* packed, int32_t* packed_host,
+                        void* caller_stream, int32_t** results_host) {
+  GIMBAL_TRY(check_handle(h));
+  if (!packed || !packed_host || !results_host) return invalid("pass_enqueue: null packed result buffer");
+  const int64_t m = h->m();
+  cudaStream_t caller = static_cast<cudaStream_t>(caller_stream);
+  const bool join = caller != h->stream;
+  {
+    DeviceGuard g(h->device);
+    if (join) {
+      if (!h->ev_caller) GIMBAL_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_caller, cudaEventDisableTiming));
+      GIMBAL_CUDA_TRY(cudaEventRecord(h->ev_caller, caller));
+      GIMBAL_CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_caller, 0));
+    }
+  }
+  // packed layout (int32 words): [0:2] argmin, [2] |M|, [3] pad, [4:6] error words, [6:6+m] M,
+  // [6+m:6+2m] greedy
+  GIMBAL_TRY(gimbal_pass_graph(h, ids, id_bytes, n_tokens, threshold, top_e, capacity, anchor, candidates, C, alpha,
+                               beta, scores, reinterpret_cast<int64_t*>(packed), packed + 6 + m, packed + 6,
+                               packed + 2, reinterpret_cast<uint32_t*>(packed + 4)));
+  DeviceGuard g(h->device);
+  if (h->ran_tiny) {  // the fused pass wrote its results into the mapped ring already
+    *results_host = h->ring_host + (size_t)h->ring_slot * (size_t)(6 + 2 * m);
+  } else {
+    GIMBAL_CUDA_TRY(
+        cudaMemcpyAsync(packed_host, packed, (size_t)(6 + 2 * m) * 4, cudaMemcpyDeviceToHost, h->stream));
+    *results_host = packed_host;
+  }
+  if (join) {
+    if (!h->ev_back) GIMBAL_CUDA_TRY(cudaEventCreateWithFlags(&h->ev_back, cudaEventDisableTiming));
+    GIMBAL_CUDA_TRY(cudaEventRecord(h->ev_back, h->stream));
+    GIMBAL_CUDA_TRY(cudaStreamWaitEvent(caller, h->ev_back, 0));
+  }
   return GIMBAL_OK;
 }
 

@@ -254,6 +254,16 @@ cudaError_t launch_greedy_walk(int L, int ne, int g, const unsigned long long* A
 
 // Sort uint64 keys descending in place (bitonic; n must be a power of two).
 cudaError_t sort_u64_desc(unsigned long long* keys, int64_t n, cudaStream_t s);
+// The whole placement pass for small shapes in one launch (placement.cu tiny_pass_kernel):
+// cudaErrorNotSupported when the shape does not fit it.  Every E cell must be < 2^32; `same` holds
+// tiny_scratch_bytes(C).
+size_t tiny_scratch_bytes(int64_t C);
+cudaError_t launch_tiny_pass(int L, int ne, int g, int k, double threshold, int top_e, int capacity, int anchor,
+                             const unsigned long long* E, unsigned long long* A_out, uint8_t* cands, int64_t C,
+                             double alpha, double beta, double* scores, long long* argmin, int32_t* placement,
+                             int32_t* members, int32_t* n_members, uint32_t* flags, unsigned long long* same,
+                             bool init_scratch, uint32_t* flags_out, int32_t* ring, uint32_t* ring_seq,
+                             int ring_slots, cudaStream_t s);
 
 cudaError_t launch_comm_cost(int L, int ne, int k, const void* ids, int id_bytes, int64_t T,
                              const int32_t* assign, unsigned long long* out, uint32_t* flags,

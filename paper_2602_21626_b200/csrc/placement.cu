@@ -21,7 +21,9 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "greedy_block.cuh"
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace gimbal_gpu {
 
@@ -189,31 +191,38 @@ __global__ void max_cell_kernel(const unsigned long long* __restrict__ E, int64_
 // candidate's GPU ids of layers l and l+1 (NE bytes each), adds E_l(j, k) for every same-GPU (j, k)
 // pair, and forms layer l's per-GPU loads, |load - ideal_l| and per-GPU expert counts; the warp
 // reduces them.  Replaces eval_same_kernel + eval_dev_kernel (4096 CTAs each) for small n_e.
+// Shared-memory tables of the small-shape evaluators: E as u32 cells ((L-1) x NE x NE), ideal
+// loads (L doubles), A (L x NE u64).  Returns the bytes used.
+template <int NE>
+__host__ __device__ constexpr size_t small_tables_bytes(int L) {
+  return (((size_t)(L - 1) * NE * NE * 4 + 15) & ~(size_t)15) + (size_t)L * 8 + (size_t)L * NE * 8;
+}
+
+// ideal_l = A.row(l).sum() / g (placement.cpp:68); integer rowsum < 2^53 is exact in fp64
 template <int NE, int G>
-__global__ void __launch_bounds__(256)
-    eval_small_kernel(int L, const unsigned long long* __restrict__ A, const unsigned long long* __restrict__ E,
-                      const uint8_t* __restrict__ cands, int64_t C, int64_t base, unsigned long long* __restrict__ same,
-                      double* __restrict__ D, uint32_t* __restrict__ flags, long long* __restrict__ bad_index) {
-  extern __shared__ __align__(16) unsigned char sm_small[];
-  uint32_t* sE = reinterpret_cast<uint32_t*>(sm_small);                       // (L-1) * NE * NE
-  double* sIdeal = reinterpret_cast<double*>(sm_small + (((L - 1) * NE * NE * 4 + 15) & ~15));  // L
-  unsigned long long* sA = reinterpret_cast<unsigned long long*>(sIdeal + L);  // L * NE
-  const int m = L * NE;
-  for (int i = threadIdx.x; i < (L - 1) * NE * NE; i += blockDim.x) sE[i] = (uint32_t)E[i];
-  for (int i = threadIdx.x; i < L * NE; i += blockDim.x) sA[i] = A[i];
-  __syncthreads();
+__device__ __forceinline__ void small_ideal(int L, const unsigned long long* sA, double* sIdeal) {
   for (int l = threadIdx.x; l < L; l += blockDim.x) {
     unsigned long long r = 0;
 #pragma unroll
     for (int j = 0; j < NE; ++j) r += sA[l * NE + j];
-    // ideal_l = A.row(l).sum() / g (placement.cpp:68); integer rowsum < 2^53 is exact in fp64
     sIdeal[l] = __ddiv_rn((double)r, (double)G);
   }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  if (c >= C) return;
-  const uint8_t* P = cands + c * m;
+}
+
+struct SmallScore {
+  unsigned long long same;  // sum of E over same-GPU (j, k) pairs
+  double dev;               // max_l,p |loads - ideal_l|
+};
+
+// One candidate by one warp (lane per layer): same-GPU pair weight and deviation (every lane gets
+// them), feasibility flagged here (check_feasible, placement.cpp:30-50).
+template <int NE, int G>
+__device__ __forceinline__ SmallScore small_candidate(int L, const uint32_t* sE, const unsigned long long* sA,
+                                                      const double* sIdeal, const uint8_t* __restrict__ P, int64_t c,
+                                                      int64_t base, uint32_t* __restrict__ flags,
+                                                      long long* __restrict__ bad_index) {
+  const int lane = threadIdx.x & 31;
+  const int m = L * NE;
   unsigned long long sm = 0;
   double dev = 0.0;
   uint32_t cnt[G];
@@ -261,8 +270,6 @@ __global__ void __launch_bounds__(256)
   }
   bad = __any_sync(0xffffffffu, bad);
   if (lane == 0) {
-    same[c] = sm;
-    D[c] = dev;
     bool infeasible = bad;
 #pragma unroll
     for (int q = 0; q < G; ++q) infeasible |= cnt[q] != (uint32_t)(m / G);
@@ -270,6 +277,31 @@ __global__ void __launch_bounds__(256)
       atomicOr(flags, (uint32_t)kFlagInfeasible);
       atomicMin(bad_index, (long long)(base + c));
     }
+  }
+  return SmallScore{sm, dev};
+}
+
+template <int NE, int G>
+__global__ void __launch_bounds__(256)
+    eval_small_kernel(int L, const unsigned long long* __restrict__ A, const unsigned long long* __restrict__ E,
+                      const uint8_t* __restrict__ cands, int64_t C, int64_t base, unsigned long long* __restrict__ same,
+                      double* __restrict__ D, uint32_t* __restrict__ flags, long long* __restrict__ bad_index) {
+  extern __shared__ __align__(16) unsigned char sm_small[];
+  uint32_t* sE = reinterpret_cast<uint32_t*>(sm_small);                       // (L-1) * NE * NE
+  double* sIdeal = reinterpret_cast<double*>(sm_small + (((L - 1) * NE * NE * 4 + 15) & ~15));  // L
+  unsigned long long* sA = reinterpret_cast<unsigned long long*>(sIdeal + L);  // L * NE
+  for (int i = threadIdx.x; i < (L - 1) * NE * NE; i += blockDim.x) sE[i] = (uint32_t)E[i];
+  for (int i = threadIdx.x; i < L * NE; i += blockDim.x) sA[i] = A[i];
+  __syncthreads();
+  small_ideal<NE, G>(L, sA, sIdeal);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (c >= C) return;
+  const SmallScore r = small_candidate<NE, G>(L, sE, sA, sIdeal, cands + c * (int64_t)L * NE, c, base, flags, bad_index);
+  if ((threadIdx.x & 31) == 0) {
+    same[c] = r.same;
+    D[c] = r.dev;
   }
 }
 
@@ -531,9 +563,9 @@ __device__ __forceinline__ void topk_insert(unsigned long long (&r)[K], unsigned
 }
 
 template <int K>
-__device__ __forceinline__ void topk_warp_merge(unsigned long long (&r)[K]) {
+__device__ __forceinline__ void topk_warp_merge(unsigned long long (&r)[K], int first = 16) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = first; o > 0; o >>= 1) {
     unsigned long long other[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) other[i] = __shfl_xor_sync(0xffffffffu, r[i], o);
@@ -710,6 +742,382 @@ __global__ void bitonic_small_kernel(unsigned long long* keys, int n) {
       __syncthreads();
     }
   for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = s[i];
+}
+
+// ---- the whole placement pass for small shapes in one launch (Mixtral class) ----
+// gimbal_pass_async queues ~10 dependent launches (derive A, top-K, select, greedy keys, sort,
+// walk, evaluator, finish); at m = 256 each runs a few microseconds and the step is launch-bound.
+// Here CTA 0 derives A, builds the strong-pair set (register top-K + the reference's endpoint
+// union), sorts the greedy keys in shared memory, runs the greedy walk (greedy_block.cuh) into
+// candidate row 0 and scores that row, while CTAs 1.. score candidates 1..C-1 (one warp each, as
+// eval_small_kernel); the last CTA to finish (completion ticket) forms cut / objective and the
+// argmin.  Every step follows the standalone kernels' arithmetic, so the results are identical.
+struct TinyPass {
+  int L, k;
+  double threshold;
+  int top_e, capacity, anchor;
+  int n2;                // greedy keys sorted in shared memory (next power of two >= m)
+  int greedy_parallel;   // greedy_smem_bytes: layer-parallel walk fits
+  const unsigned long long* E;
+  unsigned long long* A_out;
+  uint8_t* cands;
+  int64_t C;
+  double alpha, beta;
+  double* scores;        // [3][C]: deviation, cut, objective
+  long long* argmin;
+  int32_t* placement;
+  int32_t* members;
+  int32_t* n_members;
+  uint32_t* flags;       // handle flag words: [0] pass errors, [1] deferred evaluator errors
+  unsigned long long* same;
+  long long* bad_index;  // 0x7f7f.. before the launch (set once, restored by the last CTA)
+  uint32_t* ticket;      // 0x7f7f7f7f before the launch (set once, restored by the last CTA)
+  long long* best;       // per CTA: best objective (bits), its candidate index
+  uint32_t* flags_out;   // copy of flag words 0-1 at the end, or null
+  int32_t* ring;         // mapped host ring of packed results (slots x (6 + 2m) words), or null
+  uint32_t* ring_seq;    // device pass counter: this pass writes slot ring_seq % ring_slots
+  int ring_slots;
+};
+
+// bytes of CTA 0's scratch after the shared tables (keep in step with tiny_pass_kernel)
+inline size_t tiny_prep_bytes(int n2, int KT, int m) {
+  return (size_t)n2 * 16 + (size_t)64 * KT + (((size_t)(m + 31) / 32 * 4 + 15) & ~(size_t)15) +
+         (((size_t)m + 15) & ~(size_t)15);
+}
+
+constexpr int kTinyThreads = 256;
+constexpr uint32_t kTicketBase = 0x7f7f7f7fu;
+
+#ifdef GIMBAL_AB_KNOBS
+// phase timestamps of the fused pass's CTA 0 and last CTA (test/tool build only)
+__device__ unsigned long long g_tiny_prof[16];
+#define TINY_MARK(i)                                                              \
+  do {                                                                           \
+    if (threadIdx.x == 0) g_tiny_prof[i] = globaltimer_ns();                     \
+  } while (0)
+#else
+#define TINY_MARK(i) \
+  do {               \
+  } while (0)
+#endif
+
+template <int NE>
+__host__ __device__ constexpr size_t tiny_extra_offset(int L) {
+  return (small_tables_bytes<NE>(L) + 15) & ~(size_t)15;
+}
+
+template <int NE, int G, int KT>
+__global__ void __launch_bounds__(kTinyThreads) tiny_pass_kernel(const TinyPass p) {
+  extern __shared__ __align__(16) unsigned char sm_tiny[];
+  const int L = p.L;
+  const int m = L * NE;
+  const int nE = (L - 1) * NE * NE;
+  uint32_t* sE = reinterpret_cast<uint32_t*>(sm_tiny);
+  double* sIdeal = reinterpret_cast<double*>(sm_tiny + ((nE * 4 + 15) & ~15));
+  unsigned long long* sA = reinterpret_cast<unsigned long long*>(sIdeal + L);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (blockIdx.x == 0) TINY_MARK(0);
+  for (int i = tid; i < nE; i += kTinyThreads) sE[i] = (uint32_t)p.E[i];
+  __syncthreads();
+  // derive_activation_kernel: A_l(j) = sum_k E_l(j, k) / k, A_{L-1}(k) = sum_j E_{L-2}(j, k) / k
+  for (int r = tid; r < m; r += kTinyThreads) {
+    const int l = r / NE, x = r - l * NE;
+    unsigned long long s = 0;
+    if (l < L - 1) {
+#pragma unroll
+      for (int c = 0; c < NE; ++c) s += sE[(l * NE + x) * NE + c];
+    } else {
+#pragma unroll
+      for (int j = 0; j < NE; ++j) s += sE[((L - 2) * NE + j) * NE + x];
+    }
+    sA[r] = s / (unsigned long long)p.k;
+  }
+  __syncthreads();
+  small_ideal<NE, G>(L, sA, sIdeal);
+  __syncthreads();
+  double* D = p.scores;
+  // CTA 0's scratch (tiny_prep_bytes): greedy keys, rank-sorted keys, top-K lists, member bits,
+  // the greedy row, then greedy_walk_block's shared memory
+  unsigned char* extra = sm_tiny + tiny_extra_offset<NE>(L);
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(extra);   // n2
+  unsigned long long* keys2 = keys + p.n2;                                   // n2
+  unsigned long long* lists = keys2 + p.n2;                                  // 8 x KT
+  uint32_t* bits = reinterpret_cast<uint32_t*>(lists + 8 * KT);              // (m + 31) / 32
+  uint8_t* row0 = reinterpret_cast<uint8_t*>(bits) + (((m + 31) / 32 * 4 + 15) & ~15);
+  unsigned long long* gsm = reinterpret_cast<unsigned long long*>(row0 + ((m + 15) & ~15));
+  __shared__ unsigned long long s_same0, s_dev0;  // row 0's score (CTA 0)
+  __shared__ int s_bad0;
+  if (blockIdx.x == 0) {
+    __shared__ int s_nM;
+    TINY_MARK(1);
+    for (int r = tid; r < m; r += kTinyThreads) p.A_out[r] = sA[r];
+    // build_affinity_set (placement.cpp:186-238): top_e heaviest (w desc, a asc, b asc) pairs
+    // with w >= threshold and w > 0 -- composite keys as topk_reg_kernel, one CTA
+    unsigned long long r[KT];
+#pragma unroll
+    for (int i = 0; i < KT; ++i) r[i] = 0ull;
+    for (int idx = tid; idx < nE; idx += kTinyThreads) {
+      const unsigned long long w = sE[idx];
+      const double wd = (double)w;
+      topk_insert<KT>(r, (wd >= p.threshold && wd > 0.0) ? (w << 24) | (unsigned long long)(0xffffff - idx) : 0ull);
+    }
+    topk_warp_merge<KT>(r);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < KT; ++i) lists[warp * KT + i] = r[i];
+    }
+    for (int w = tid; w < (m + 31) / 32; w += kTinyThreads) bits[w] = 0u;
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < KT; ++i) r[i] = lane < kTinyThreads / 32 ? lists[lane * KT + i] : 0ull;
+      topk_warp_merge<KT>(r, kTinyThreads / 64);  // lists in lanes 0-7 only
+      if (lane == 0) {  // affinity_select_kernel: endpoint union of the longest prefix within capacity
+        int members = 0;
+        for (int i = 0; i < p.top_e; ++i) {
+          const unsigned long long key = r[0];
+#pragma unroll
+          for (int q = 0; q + 1 < KT; ++q) r[q] = r[q + 1];  // pop the front (registers, static indices)
+          r[KT - 1] = 0ull;
+          if (key == 0ull) break;
+          const int idx = 0xffffff - (int)(key & 0xffffffull);
+          const int a = idx / NE;
+          const int b = (idx / (NE * NE) + 1) * NE + (idx % NE);
+          const bool na = !((bits[a >> 5] >> (a & 31)) & 1u);
+          const bool nb = !((bits[b >> 5] >> (b & 31)) & 1u);
+          const int grown = members + (na ? 1 : 0) + (nb ? 1 : 0);
+          if (grown > p.capacity) break;
+          if (na) bits[a >> 5] |= 1u << (a & 31);
+          if (nb) bits[b >> 5] |= 1u << (b & 31);
+          members = grown;
+        }
+        int n = 0;
+        for (int w = 0; w < (m + 31) / 32; ++w) {
+          uint32_t v = bits[w];
+          while (v) {
+            p.members[n++] = w * 32 + (__ffs(v) - 1);
+            v &= v - 1;
+          }
+        }
+        *p.n_members = n;
+        s_nM = n;
+      }
+    }
+    __syncthreads();
+    TINY_MARK(2);
+    // greedy_keys_kernel: (A << 24) | (2^24 - 1 - e) for unanchored experts, 0 otherwise
+    for (int i = tid; i < p.n2; i += kTinyThreads)
+      keys[i] = (i < m && !((bits[i >> 5] >> (i & 31)) & 1u)) ? (sA[i] << 24) | (unsigned long long)(0xffffff - i)
+                                                            : 0ull;
+    __syncthreads();
+    unsigned long long* sorted = keys;
+    if (p.n2 <= 512) {
+      // rank sort (descending; equal keys -- only zeros -- by position): one pass, no barriers
+      for (int i = tid; i < p.n2; i += kTinyThreads) {
+        const unsigned long long ki = keys[i];
+        int rank = 0;
+#pragma unroll 8
+        for (int j = 0; j < p.n2; ++j) {
+          const unsigned long long kj = keys[j];
+          rank += (kj > ki) | ((kj == ki) & (j < i));
+        }
+        keys2[rank] = ki;
+      }
+      sorted = keys2;
+    } else {  // bitonic_small_kernel
+      for (int kk = 2; kk <= p.n2; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int t = tid; t < p.n2 / 2; t += kTinyThreads) {
+            const int i = 2 * j * (t / j) + (t % j);
+            const bool desc = ((i & kk) == 0);
+            const unsigned long long a = keys[i], b = keys[i + j];
+            if (desc ? (a < b) : (a > b)) {
+              keys[i] = b;
+              keys[i + j] = a;
+            }
+          }
+          __syncthreads();
+        }
+    }
+    __syncthreads();
+    TINY_MARK(3);
+    // greedy_place (placement.cpp:240-299) into the placement and the shared copy of row 0
+    if (p.greedy_parallel)
+      greedy_detail::greedy_walk_block<G>(L, NE, G, sA, p.members, s_nM, nullptr, p.anchor, sorted, m, p.placement,
+                                          row0, nullptr, gsm);
+    else
+      greedy_detail::greedy_walk_block<0>(L, NE, G, sA, p.members, s_nM, nullptr, p.anchor, sorted, m, p.placement,
+                                          row0, nullptr, gsm);
+    __syncthreads();
+    TINY_MARK(4);
+    for (int i = tid; i < m; i += kTinyThreads) p.cands[i] = row0[i];
+    // row 0 scored by the whole CTA, with small_candidate's arithmetic: same-GPU pair weight,
+    // per-layer GPU loads (shared u64 atomics, exact), max |load - ideal|, feasibility
+    unsigned long long* ld = keys;                         // [L][G] (the sort's keys are spent)
+    uint32_t* cnt0 = reinterpret_cast<uint32_t*>(lists);   // [G]
+    for (int i = tid; i < L * G; i += kTinyThreads) ld[i] = 0ull;
+    if (tid < G) cnt0[tid] = 0u;
+    if (tid == 0) {
+      s_same0 = 0ull;
+      s_dev0 = 0ull;
+      s_bad0 = 0;
+    }
+    __syncthreads();
+    unsigned long long sm0 = 0;
+    bool bad0 = false;
+    for (int r = tid; r < m; r += kTinyThreads) {
+      const int l = r / NE, j = r - l * NE;
+      const uint32_t pj = row0[r];
+      if (pj < (uint32_t)G) {
+        atomicAdd(&ld[l * G + pj], sA[r]);
+        atomicAdd(&cnt0[pj], 1u);
+      } else {
+        bad0 = true;
+      }
+      if (l + 1 < L) {
+        const uint32_t* Er = sE + (l * NE + j) * NE;
+#pragma unroll
+        for (int kk = 0; kk < NE; ++kk) sm0 += row0[(l + 1) * NE + kk] == pj ? (unsigned long long)Er[kk] : 0ull;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sm0 += __shfl_xor_sync(0xffffffffu, sm0, o);
+    if (lane == 0 && sm0) atomicAdd(&s_same0, sm0);
+    if (bad0) s_bad0 = 1;
+    __syncthreads();
+    double dv = 0.0;
+    for (int r = tid; r < L * G; r += kTinyThreads) dv = fmax(dv, fabs(__dsub_rn((double)ld[r], sIdeal[r / G])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dv = fmax(dv, __shfl_xor_sync(0xffffffffu, dv, o));
+    if (lane == 0) atomicMax(&s_dev0, (unsigned long long)__double_as_longlong(dv));  // dv >= 0: bits order
+    __syncthreads();
+    if (tid == 0) {
+      bool infeasible = s_bad0 != 0;
+      for (int q = 0; q < G; ++q) infeasible |= cnt0[q] != (uint32_t)(m / G);
+      if (infeasible) {
+        atomicOr(p.flags + 1, (uint32_t)kFlagInfeasible);
+        atomicMin(p.bad_index, 0ll);
+      }
+    }
+  }
+  // score this CTA's candidates (CTA 0: the greedy row), cut and objective included
+  // (eval_finish_kernel: cut = tokens * k * (L-1) * k - same; objective = alpha * D + beta * cut,
+  // placement.cpp:83, two roundings, no FMA contraction), then the CTA's best (objective, index)
+  __shared__ double w_best[kTinyThreads / 32];
+  __shared__ long long w_idx[kTinyThreads / 32];
+  unsigned long long tot = 0;  // tokens * k = sum_j A(0, j)
+#pragma unroll
+  for (int j = 0; j < NE; ++j) tot += sA[j];
+  const unsigned long long total = tot * (unsigned long long)(L - 1) * (unsigned long long)p.k;
+  const int64_t c = blockIdx.x == 0 ? (warp == 0 ? 0 : -1) : 1 + (int64_t)(blockIdx.x - 1) * (kTinyThreads / 32) + warp;
+  long long my_idx = -1;
+  double my_obj = 0.0;
+  if (c >= 0 && c < p.C) {
+    const SmallScore r = blockIdx.x == 0 ? SmallScore{s_same0, __longlong_as_double((long long)s_dev0)}
+                                         : small_candidate<NE, G>(L, sE, sA, sIdeal, p.cands + c * m, c, 0,
+                                                                  p.flags + 1, p.bad_index);
+    const unsigned long long cu = total - r.same;
+    const double cd = (double)cu;
+    my_obj = __dadd_rn(__dmul_rn(p.alpha, r.dev), __dmul_rn(p.beta, cd));
+    my_idx = c;
+    if (lane == 0) {
+      if (cu > (1ull << 53)) atomicOr(p.flags + 1, (uint32_t)kFlagOverflow);
+      D[c] = r.dev;
+      p.scores[p.C + c] = cd;
+      p.scores[2 * p.C + c] = my_obj;
+    }
+  }
+  if (blockIdx.x == 0) TINY_MARK(5);
+  if (lane == 0) {
+    w_best[warp] = my_obj;
+    w_idx[warp] = my_idx;
+  }
+  __syncthreads();
+  __shared__ int s_last;
+  if (tid == 0) {
+    double b = 0.0;
+    long long bi = -1;
+    for (int w = 0; w < kTinyThreads / 32; ++w)  // ascending candidate order: strict < keeps the lowest index
+      if (w_idx[w] >= 0 && (bi < 0 || w_best[w] < b)) {
+        b = w_best[w];
+        bi = w_idx[w];
+      }
+    p.best[2 * blockIdx.x] = __double_as_longlong(b);
+    p.best[2 * blockIdx.x + 1] = bi;
+    __threadfence();
+    s_last = (atomicAdd(p.ticket, 1u) - kTicketBase) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  TINY_MARK(6);
+  __threadfence();
+  // the last CTA: argmin over the CTAs' bests (lowest index among minima), flags read back
+  __shared__ double bv[kTinyThreads];
+  __shared__ long long bix[kTinyThreads];
+  double best = 0.0;
+  long long besti = -1;
+  for (int b = tid; b < (int)gridDim.x; b += kTinyThreads) {
+    const long long i2 = __ldcg(p.best + 2 * b + 1);
+    const double v2 = __longlong_as_double(__ldcg(p.best + 2 * b));
+    if (i2 >= 0 && (besti < 0 || v2 < best || (v2 == best && i2 < besti))) {
+      best = v2;
+      besti = i2;
+    }
+  }
+  bv[tid] = best;
+  bix[tid] = besti;
+  __syncthreads();
+  for (int s = kTinyThreads / 2; s > 0; s >>= 1) {
+    if (tid < s) {
+      const double v2 = bv[tid + s];
+      const long long i2 = bix[tid + s];
+      const long long i1 = bix[tid];
+      if (i2 >= 0 && (i1 < 0 || v2 < bv[tid] || (v2 == bv[tid] && i2 < i1))) {
+        bv[tid] = v2;
+        bix[tid] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  TINY_MARK(7);
+  if (p.ring) {
+    // the packed results straight into mapped host memory ([argmin | |M| | pad | error words |
+    // M | greedy], gimbal_pass_enqueue): no device-to-host copy on the stream behind the pass
+    __shared__ int32_t* slot;
+    __shared__ uint32_t f0, f1;
+    if (tid == 0) {
+      const uint32_t seq = *p.ring_seq;
+      *p.ring_seq = seq + 1;
+      slot = p.ring + (size_t)(seq % (uint32_t)p.ring_slots) * (size_t)(6 + 2 * m);
+      f0 = atomicOr(p.flags, 0u);
+      f1 = atomicOr(p.flags + 1, 0u);
+    }
+    __syncthreads();
+    const int nM = __ldcg(p.n_members);
+    if (tid == 0) {
+      const long long am = bix[0];
+      slot[0] = (int32_t)(am & 0xffffffffll);
+      slot[1] = (int32_t)(am >> 32);
+      slot[2] = nM;
+      slot[3] = 0;
+      slot[4] = (int32_t)f0;
+      slot[5] = (int32_t)f1;
+    }
+    for (int i = tid; i < nM; i += kTinyThreads) slot[6 + i] = __ldcg(p.members + i);
+    for (int i = tid; i < m; i += kTinyThreads) slot[6 + m + i] = __ldcg(p.placement + i);
+    __threadfence_system();
+  }
+  if (tid == 0) {
+    *p.argmin = bix[0];
+    // ready for the next launch: no memset node per pass
+    *p.bad_index = 0x7f7f7f7f7f7f7f7fll;
+    *p.ticket = kTicketBase;
+    if (p.flags_out) {
+      __threadfence();
+      p.flags_out[0] = atomicOr(p.flags, 0u);
+      p.flags_out[1] = atomicOr(p.flags + 1, 0u);
+    }
+  }
 }
 
 }  // namespace
@@ -935,5 +1343,94 @@ cudaError_t launch_greedy_keys(int64_t m, const unsigned long long* A, const uin
   greedy_keys_kernel<<<grid, 256, 0, s>>>(m, A, anchored, keys, n_pad, flags);
   return cudaGetLastError();
 }
+
+size_t tiny_scratch_bytes(int64_t C) {
+  return eval_scratch_bytes(C) + (size_t)16 * (size_t)(2 + (C - 1 + kTinyThreads / 32 - 1) / (kTinyThreads / 32));
+}
+
+// The fused small-shape pass (tiny_pass_kernel), or cudaErrorNotSupported when the shape does not
+// fit it (n_e in {8, 16} with a matching n_gpus, (L-1) n_e^2 u32 cells <= 32 KB, m <= 2048,
+// 0 <= top_e <= 8).  `same` holds tiny_scratch_bytes(C); the caller guarantees every E cell < 2^32.
+cudaError_t launch_tiny_pass(int L, int ne, int g, int k, double threshold, int top_e, int capacity, int anchor,
+                             const unsigned long long* E, unsigned long long* A_out, uint8_t* cands, int64_t C,
+                             double alpha, double beta, double* scores, long long* argmin, int32_t* placement,
+                             int32_t* members, int32_t* n_members, uint32_t* flags, unsigned long long* same,
+                             bool init_scratch, uint32_t* flags_out, int32_t* ring, uint32_t* ring_seq,
+                             int ring_slots, cudaStream_t s) {
+  const int64_t m = (int64_t)L * ne;
+  if (L < 2 || L > 256 || m > 2048 || (int64_t)(L - 1) * ne * ne * 4 > 32 * 1024 || top_e < 0 ||
+      top_e > kRegTopK || C < 1 || GIMBAL_KNOB("GIMBAL_NO_TINY_PASS"))
+    return cudaErrorNotSupported;
+  TinyPass p;
+  p.L = L;
+  p.k = k;
+  p.threshold = threshold;
+  p.top_e = top_e;
+  p.capacity = capacity;
+  p.anchor = anchor;
+  int n2 = 1;
+  while (n2 < m) n2 <<= 1;
+  p.n2 = n2;
+  bool parallel = false;
+  const size_t gbytes = greedy_detail::greedy_smem_bytes(L, g, m, &parallel);
+  p.greedy_parallel = parallel ? 1 : 0;
+  p.E = E;
+  p.A_out = A_out;
+  p.cands = cands;
+  p.C = C;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.scores = scores;
+  p.argmin = argmin;
+  p.placement = placement;
+  p.members = members;
+  p.n_members = n_members;
+  p.flags = flags;
+  p.same = same;
+  p.bad_index = reinterpret_cast<long long*>(same + C);
+  p.ticket = reinterpret_cast<uint32_t*>(same + C + 1);
+  p.best = reinterpret_cast<long long*>(same + C + 2);  // 2 words per CTA (tiny_scratch_words)
+  p.flags_out = flags_out;
+  p.ring = ring;
+  p.ring_seq = ring_seq;
+  p.ring_slots = ring_slots;
+  cudaError_t e = cudaSuccess;
+  if (init_scratch) {  // bad index and ticket; every launch leaves them so for the next one
+    e = cudaMemsetAsync(same + C, 0x7f, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+  }
+  const int KT = top_e <= 4 ? 4 : kRegTopK;
+  auto pick = [&](auto k4, auto k8) { return KT == 4 ? k4 : k8; };
+  void (*kern)(const TinyPass) = nullptr;
+  size_t tables = 0;
+  if (ne == 8) {
+    tables = tiny_extra_offset<8>(L);
+    kern = g == 8   ? pick(tiny_pass_kernel<8, 8, 4>, tiny_pass_kernel<8, 8, kRegTopK>)
+         : g == 4   ? pick(tiny_pass_kernel<8, 4, 4>, tiny_pass_kernel<8, 4, kRegTopK>)
+         : g == 2   ? pick(tiny_pass_kernel<8, 2, 4>, tiny_pass_kernel<8, 2, kRegTopK>)
+                    : nullptr;
+  } else if (ne == 16) {
+    tables = tiny_extra_offset<16>(L);
+    kern = g == 8   ? pick(tiny_pass_kernel<16, 8, 4>, tiny_pass_kernel<16, 8, kRegTopK>)
+         : g == 4   ? pick(tiny_pass_kernel<16, 4, 4>, tiny_pass_kernel<16, 4, kRegTopK>)
+         : g == 16  ? pick(tiny_pass_kernel<16, 16, 4>, tiny_pass_kernel<16, 16, kRegTopK>)
+                    : nullptr;
+  }
+  if (!kern) return cudaErrorNotSupported;
+  const size_t smem = tables + tiny_prep_bytes(n2, KT, (int)m) + gbytes;
+  if (smem > 160 * 1024) return cudaErrorNotSupported;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)(1 + (C - 1 + kTinyThreads / 32 - 1) / (kTinyThreads / 32));
+  kern<<<grid, kTinyThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+
+#ifdef GIMBAL_AB_KNOBS
+extern "C" int gimbal_debug_tiny_profile(unsigned long long* out16) {
+  return cudaMemcpyFromSymbol(out16, gimbal_gpu::g_tiny_prof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // namespace gimbal_gpu

@@ -24,10 +24,88 @@ namespace {
 constexpr int kSmallThreads = 256;
 constexpr int kSmallMaxTable = 48 * 1024;  // bytes of u32 cells per CTA (several CTAs per SM)
 
+// The k x k increments of one token's layer pairs, ids checked per token-layer (a pair with an
+// out-of-range id on either side is left out and flagged).
 template <int K>
-__global__ void __launch_bounds__(kSmallThreads)
+__device__ __forceinline__ bool small_count_row(const uint8_t* row, int L, int ne, uint32_t* tab) {
+  bool bad = false;
+  uint32_t cur[K];
+  bool ok_cur = true;
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    cur[a] = row[a];
+    ok_cur &= cur[a] < (uint32_t)ne;
+  }
+  bad |= !ok_cur;
+  for (int l = 0; l + 1 < L; ++l) {
+    uint32_t nxt[K];
+    bool ok_nxt = true;
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      nxt[b] = row[(l + 1) * K + b];
+      ok_nxt &= nxt[b] < (uint32_t)ne;
+    }
+    bad |= !ok_nxt;
+    if (ok_cur && ok_nxt) {
+      uint32_t* El = tab + l * ne * ne;
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) atomicAdd(El + cur[a] * ne + nxt[b], 1u);
+    }
+#pragma unroll
+    for (int b = 0; b < K; ++b) cur[b] = nxt[b];
+    ok_cur = ok_nxt;
+  }
+  return bad;
+}
+
+// Top-2 rows with a compile-time expert count NE (8 or 16; L even): the row is read as 32-bit
+// words (two layers each), all ids checked at once, and each pair's four cell addresses are one
+// add of precomputed row / column offsets (half the instructions of the byte-wise loop, which is
+// issue-bound at Mixtral).  Rows with an out-of-range id take small_count_row.
+template <int NE>
+__device__ __forceinline__ bool small_count_row2(const uint32_t* row, int L, uint32_t* tab) {
+  constexpr uint32_t kBad = 0x01010101u * (uint32_t)(0x100 - NE);  // any id byte >= NE
+  constexpr int kShift = NE == 8 ? 3 : 4;
+  uint32_t acc = 0;
+  for (int w = 0; w < L / 2; ++w) acc |= row[w];
+  if (acc & kBad) return small_count_row<2>(reinterpret_cast<const uint8_t*>(row), L, NE, tab);
+  const uint32_t tab_s = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+  uint32_t w = row[0];
+  // byte offsets: column k -> 4k, row j -> 4 NE j
+  uint32_t j0 = (w & 0xffu) << (2 + kShift), j1 = ((w >> 8) & 0xffu) << (2 + kShift);
+  uint32_t base = tab_s;
+  for (int lw = 0; lw < L / 2; ++lw) {
+    // pair (2 lw, 2 lw + 1): columns from the high half of word lw
+    const uint32_t k0 = ((w >> 16) & 0xffu) << 2, k1 = (w >> 24) << 2;
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + j0 + k0) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + j0 + k1) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + j1 + k0) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + j1 + k1) : "memory");
+    base += NE * NE * 4;
+    if (lw + 1 == L / 2) break;
+    // pair (2 lw + 1, 2 lw + 2): rows = those columns, columns from the low half of word lw + 1
+    w = row[lw + 1];
+    const uint32_t n0 = (w & 0xffu) << 2, n1 = ((w >> 8) & 0xffu) << 2;
+    const uint32_t r0 = k0 << kShift, r1 = k1 << kShift;
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + r0 + n0) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + r0 + n1) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + r1 + n0) : "memory");
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base + r1 + n1) : "memory");
+    base += NE * NE * 4;
+    j0 = n0 << kShift;
+    j1 = n1 << kShift;
+  }
+  return false;
+}
+
+// NE = 0: runtime expert count, byte-wise rows; NE > 0 (K = 2 only): small_count_row2.
+template <int K, int NE, int THREADS>
+__global__ void __launch_bounds__(THREADS)
     count_small_tm_kernel(int L, int ne, const uint8_t* __restrict__ trace, int64_t T, int row_bytes,
                           int stride, unsigned long long* __restrict__ E, uint32_t* __restrict__ flags) {
+  constexpr int kSmallThreads = THREADS;
   extern __shared__ __align__(16) uint8_t sm[];
   const int cells = (L - 1) * ne * ne;
   uint32_t* tab = reinterpret_cast<uint32_t*>(sm);
@@ -35,57 +113,73 @@ __global__ void __launch_bounds__(kSmallThreads)
   for (int i = threadIdx.x; i < cells; i += blockDim.x) tab[i] = 0u;
   bool bad = false;
   const bool vec = (row_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(trace) & 15) == 0;
-  for (int64_t t0 = (int64_t)blockIdx.x * kSmallThreads; t0 < T; t0 += (int64_t)gridDim.x * kSmallThreads) {
-    const int n = (int)min((int64_t)kSmallThreads, T - t0);
-    __syncthreads();  // the previous block's rows are consumed (and the table is zeroed)
-    const uint8_t* src = trace + t0 * row_bytes;
-    if (vec) {
-      const int q = row_bytes >> 4;  // 16-byte words per row
-      for (int i = threadIdx.x; i < n * q; i += blockDim.x) {
-        const int r = i / q, w = i - r * q;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
-        uint32_t* d = reinterpret_cast<uint32_t*>(rows + r * stride + w * 16);
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
+  if constexpr (NE > 0) {
+    // 16-byte rows (checked by the launcher): the next block's chunks are prefetched into
+    // registers while this block is counted, so one CTA per SM keeps its loads in flight
+    constexpr int kPf = 8;
+    const int q = row_bytes >> 4;
+    const int64_t step = (int64_t)gridDim.x * kSmallThreads;
+    uint4 pre[kPf];
+    auto load = [&](int64_t t0) {
+      const int n = (int)min((int64_t)kSmallThreads, T - t0);
+      const uint4* src = reinterpret_cast<const uint4*>(trace + t0 * row_bytes);
+#pragma unroll
+      for (int r = 0; r < kPf; ++r) {
+        const int i = threadIdx.x + r * kSmallThreads;
+        if (i < n * q) pre[r] = __ldcs(src + i);
       }
-    } else {
-      for (int i = threadIdx.x; i < n * row_bytes; i += blockDim.x) {
-        const int r = i / row_bytes;
-        rows[r * stride + (i - r * row_bytes)] = __ldg(src + i);
+    };
+    int64_t t0 = (int64_t)blockIdx.x * kSmallThreads;
+    if (t0 < T) load(t0);
+    for (; t0 < T; t0 += step) {
+      const int n = (int)min((int64_t)kSmallThreads, T - t0);
+      __syncthreads();  // the previous block's rows are consumed (and the table is zeroed)
+#pragma unroll
+      for (int r = 0; r < kPf; ++r) {
+        const int i = threadIdx.x + r * kSmallThreads;
+        if (i < n * q) {
+          const int rr = i / q, w = i - rr * q;
+          uint32_t* d = reinterpret_cast<uint32_t*>(rows + rr * stride + w * 16);
+          d[0] = pre[r].x;
+          d[1] = pre[r].y;
+          d[2] = pre[r].z;
+          d[3] = pre[r].w;
+        }
       }
+      __syncthreads();
+      if (t0 + step < T) load(t0 + step);
+      if (threadIdx.x < n)
+        bad |= small_count_row2<NE>(reinterpret_cast<const uint32_t*>(rows + threadIdx.x * stride), L, tab);
     }
-    __syncthreads();
-    if (threadIdx.x < n) {
-      const uint8_t* row = rows + threadIdx.x * stride;
-      uint32_t cur[K];
-      bool ok_cur = true;
-#pragma unroll
-      for (int a = 0; a < K; ++a) {
-        cur[a] = row[a];
-        ok_cur &= cur[a] < (uint32_t)ne;
+  } else {
+    for (int64_t t0 = (int64_t)blockIdx.x * kSmallThreads; t0 < T; t0 += (int64_t)gridDim.x * kSmallThreads) {
+      const int n = (int)min((int64_t)kSmallThreads, T - t0);
+      __syncthreads();  // the previous block's rows are consumed (and the table is zeroed)
+      const uint8_t* src = trace + t0 * row_bytes;
+      if (vec) {
+        const int q = row_bytes >> 4;  // 16-byte words per row
+        for (int i = threadIdx.x; i < n * q; i += blockDim.x) {
+          const int r = i / q, w = i - r * q;
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(src) + i);
+          uint32_t* d = reinterpret_cast<uint32_t*>(rows + r * stride + w * 16);
+          d[0] = v.x;
+          d[1] = v.y;
+          d[2] = v.z;
+          d[3] = v.w;
+        }
+      } else {
+        for (int i = threadIdx.x; i < n * row_bytes; i += blockDim.x) {
+          const int r = i / row_bytes;
+          rows[r * stride + (i - r * row_bytes)] = __ldg(src + i);
+        }
       }
-      bad |= !ok_cur;
-      for (int l = 0; l + 1 < L; ++l) {
-        uint32_t nxt[K];
-        bool ok_nxt = true;
-#pragma unroll
-        for (int b = 0; b < K; ++b) {
-          nxt[b] = row[(l + 1) * K + b];
-          ok_nxt &= nxt[b] < (uint32_t)ne;
-        }
-        bad |= !ok_nxt;
-        if (ok_cur && ok_nxt) {
-          uint32_t* El = tab + l * ne * ne;
-#pragma unroll
-          for (int a = 0; a < K; ++a)
-#pragma unroll
-            for (int b = 0; b < K; ++b) atomicAdd(El + cur[a] * ne + nxt[b], 1u);
-        }
-#pragma unroll
-        for (int b = 0; b < K; ++b) cur[b] = nxt[b];
-        ok_cur = ok_nxt;
+      __syncthreads();
+      if (threadIdx.x < n) {
+        const uint8_t* row = rows + threadIdx.x * stride;
+        if constexpr (NE > 0)
+          bad |= small_count_row2<NE>(reinterpret_cast<const uint32_t*>(row), L, tab);
+        else
+          bad |= small_count_row<K>(row, L, ne, tab);
       }
     }
   }
@@ -95,9 +189,19 @@ __global__ void __launch_bounds__(kSmallThreads)
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
 }
 
-size_t small_smem(int L, int ne, int k) {
+size_t small_smem(int L, int ne, int k, int threads = kSmallThreads) {
   const size_t table = ((size_t)(L - 1) * ne * ne * 4 + 15) & ~(size_t)15;
-  return table + (size_t)kSmallThreads * ((size_t)L * k + 4);
+  return table + (size_t)threads * ((size_t)L * k + 4);
+}
+
+// Top-2 rows of 8 or 16 experts, L even, row stride an odd number of words: the word-wise kernel,
+// 1024 threads and one CTA per SM (its flush adds every cell of the CTA's table to E with a global
+// atomic, so fewer, larger CTAs mean fewer same-address atomics: 148 x 1984 at Mixtral instead of
+// 1184 x 1984 with 256-thread CTAs).
+constexpr int kSmall2Threads = 1024;
+bool small2_applies(int L, int ne, int k, const uint8_t* trace) {
+  return k == 2 && (ne == 8 || ne == 16) && (L * 2) % 16 == 0 && L * 2 <= 8 * 16 && ((L * 2 + 4) / 4) % 2 == 1 &&
+         (reinterpret_cast<uintptr_t>(trace) & 15) == 0 && small_smem(L, ne, k, kSmall2Threads) <= 200 * 1024;
 }
 
 }  // namespace
@@ -113,6 +217,17 @@ bool small_count_supported(int L, int ne, int k, int id_bytes, int64_t T) {
 cudaError_t launch_count_small(int L, int ne, int k, int sms, const uint8_t* trace, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
+  if (small2_applies(L, ne, k, trace) && !GIMBAL_KNOB("GIMBAL_SMALL_BYTEWISE")) {
+    const size_t smem = small_smem(L, ne, k, kSmall2Threads);
+    int64_t grid = std::min<int64_t>(sms, (T + kSmall2Threads - 1) / kSmall2Threads);
+    const int64_t min_grid = T * k * k / ((int64_t)1 << 31) + 1;  // u32 cells per CTA
+    grid = std::max<int64_t>(grid, std::min<int64_t>(min_grid, (T + kSmall2Threads - 1) / kSmall2Threads));
+    auto kern = ne == 8 ? count_small_tm_kernel<2, 8, kSmall2Threads> : count_small_tm_kernel<2, 16, kSmall2Threads>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)grid, kSmall2Threads, smem, s>>>(L, ne, trace, T, L * k, L * k + 4, E, flags);
+    return cudaGetLastError();
+  }
   const size_t smem = small_smem(L, ne, k);
   const int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / smem)));
   int64_t grid = std::min<int64_t>((int64_t)per_sm * sms, (T + kSmallThreads - 1) / kSmallThreads);
@@ -128,14 +243,14 @@ cudaError_t launch_count_small(int L, int ne, int k, int sms, const uint8_t* tra
     return cudaGetLastError();
   };
   switch (k) {
-    case 1: return go(count_small_tm_kernel<1>);
-    case 2: return go(count_small_tm_kernel<2>);
-    case 3: return go(count_small_tm_kernel<3>);
-    case 4: return go(count_small_tm_kernel<4>);
-    case 5: return go(count_small_tm_kernel<5>);
-    case 6: return go(count_small_tm_kernel<6>);
-    case 7: return go(count_small_tm_kernel<7>);
-    case 8: return go(count_small_tm_kernel<8>);
+    case 1: return go(count_small_tm_kernel<1, 0, kSmallThreads>);
+    case 2: return go(count_small_tm_kernel<2, 0, kSmallThreads>);
+    case 3: return go(count_small_tm_kernel<3, 0, kSmallThreads>);
+    case 4: return go(count_small_tm_kernel<4, 0, kSmallThreads>);
+    case 5: return go(count_small_tm_kernel<5, 0, kSmallThreads>);
+    case 6: return go(count_small_tm_kernel<6, 0, kSmallThreads>);
+    case 7: return go(count_small_tm_kernel<7, 0, kSmallThreads>);
+    case 8: return go(count_small_tm_kernel<8, 0, kSmallThreads>);
     default: return cudaErrorInvalidValue;
   }
 }

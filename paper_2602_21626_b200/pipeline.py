@@ -104,6 +104,25 @@ class HotPathResult:
     objective: Optional[float] = None
 
 
+class PendingPass:
+    """A queued pass (HotPath.run_async); result() waits for it and decodes its packed results."""
+
+    def __init__(self, hp: "HotPath", host, event):
+        self._hp, self._host, self._event, self._res = hp, host, event, None
+
+    def done(self) -> bool:
+        return self._res is not None or self._event.query()
+
+    def result(self) -> HotPathResult:
+        if self._res is None:
+            self._event.synchronize()
+            h = self._host.copy()  # the slot is reused by a later pass
+            if h[4] or h[5]:
+                self._hp.stats.sync()  # raises (and clears) the deferred device-side error
+            self._res = self._hp._decode_pk(h)
+        return self._res
+
+
 class HotPath:
     """One stats handle + device scratch for repeated passes of the same topology."""
 
@@ -207,7 +226,7 @@ class HotPath:
         self.stats.add_tokens(trace)
         return self.place(candidates, greedy_row)
 
-    def _run_graph(self, trace, candidates) -> HotPathResult:
+    def _queue_graph(self, trace, candidates) -> None:
         import torch
 
         topo = self.topo
@@ -227,10 +246,70 @@ class HotPath:
             self.alpha, self.beta, C.c_void_p(scores.data_ptr()), C.c_void_p(base), C.c_void_p(base + 24 + 4 * m),
             C.c_void_p(base + 24), C.c_void_p(base + 8), C.c_void_p(base + 16)), "pass_graph")
         st._keep_until_done(trace, N.MEM_DEVICE)
-        h = self._read_pk()
+
+    def _decode_pk(self, h) -> HotPathResult:
+        m = self.topo.total_experts()
         n = int(h[2])
         return HotPathResult(affinity=AffinitySet(experts=h[6:6 + n].tolist(), anchor_gpu=self.anchor_gpu),
                              greedy=h[6 + m:6 + 2 * m].tolist(), argmin=int(h[0:2].view(np.int64)[0]))
+
+    def _run_graph(self, trace, candidates) -> HotPathResult:
+        self._queue_graph(trace, candidates)
+        return self._decode_pk(self._read_pk())
+
+    def run_async(self, trace, candidates) -> "PendingPass":
+        """run() without waiting (gimbal_pass_enqueue): the pass joins torch's current stream both
+        ways, replays as a graph, and its packed results ([argmin | |M| | error words | M | greedy])
+        reach host memory (a copy into one of a ring of registered slots owned by this object, or,
+        for the fused small-shape pass, the handle's mapped result ring written by the kernel); the
+        host returns at once and PendingPass.result() waits for that pass only (at most 8 are kept
+        in flight: the ninth call reads the oldest out).  Back-to-back passes therefore
+        keep the GPU busy instead of paying a host round trip each (the scores stay in `self._out`,
+        which the next pass overwrites).  Device trace and candidates only."""
+        import torch
+
+        if not (getattr(trace, "is_cuda", False) and getattr(candidates, "is_cuda", False)
+                and candidates.shape[0] > 0 and self.topo.n_gpus <= 255 and trace.is_contiguous()
+                and trace.dtype in (torch.uint8, torch.int32) and trace.numel() > 0):
+            raise ValueError("run_async: needs a contiguous CUDA uint8/int32 trace and CUDA candidates")
+        topo = self.topo
+        per = topo.n_layers * topo.top_k
+        if trace.numel() % per:
+            raise ValueError("add_token: choice span size mismatch")
+        self._ensure_pk()
+        if getattr(self, "_ring", None) is None:
+            ring = np.zeros((8, self._pk.numel()), np.int32)
+            torch.cuda.cudart().cudaHostRegister(ring.ctypes.data, ring.nbytes, 0)
+            self._ring, self._ring_ev, self._ring_next = ring, [None] * 8, 0
+            import weakref
+
+            def _unregister(ptr=ring.ctypes.data, keep=ring):
+                try:
+                    torch.cuda.cudart().cudaHostUnregister(ptr)
+                except Exception:
+                    pass
+
+            weakref.finalize(self, _unregister)
+        i = self._ring_next
+        self._ring_next = (i + 1) % 8
+        prev = self._ring_ev[i]
+        if prev is not None:  # at most 8 passes in flight: the slot's previous pass is read out first
+            prev.result()
+        m, C_ = topo.total_experts(), int(candidates.shape[0])
+        scores = self._scores(C_)
+        cur = torch.cuda.current_stream(torch.device("cuda", self.device))
+        where = C.c_void_p()
+        N.check(N.lib().gimbal_pass_enqueue(
+            self.stats.handle, trace.data_ptr(), 1 if trace.dtype == torch.uint8 else 4, trace.numel() // per,
+            self.threshold, self.top_e, m // topo.n_gpus, self.anchor_gpu, candidates.data_ptr(), C_, self.alpha,
+            self.beta, scores.data_ptr(), self._pk.data_ptr(), self._ring[i].ctypes.data, cur.cuda_stream,
+            C.byref(where)), "pass_enqueue")
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        host = np.ctypeslib.as_array(C.cast(where.value, C.POINTER(C.c_int32)), shape=(6 + 2 * m,))
+        pp = PendingPass(self, host, ev)
+        self._ring_ev[i] = pp
+        return pp
 
     def calibrate(self, trace) -> AffinitySet:
         """Offline calibration (sim.cpp:91-106): stats over a calibration trace -> strong-pair set."""

@@ -80,6 +80,27 @@ def case_count(L: str, ne: str, k: str, T: str) -> None:
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+def case_pass(L: str, ne: str, k: str, g: str, C: str) -> None:
+    """GIMBAL_NO_TINY_PASS: small shapes through the multi-launch pass (topk, select, greedy keys,
+    sort, walk, evaluator, finish) instead of the fused kernel: same answers as the oracle."""
+    G, orc, torch = _setup()
+    L, ne, k, g, C = int(L), int(ne), int(k), int(g), int(C)
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 20011, model_seed=4, stream_seed=2, device=0)
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 41, C)).cuda()
+    hp = G.HotPath(topo, 0)
+    res = hp.run(trace, cands)
+    oA, oE, _ = orc.stats(L, ne, k, trace.cpu().numpy())
+    M = list(orc.affinity_set(L, ne, g, oE, 0.0, 4, L * ne // g, 0))
+    greedy = orc.greedy_place(L, ne, g, oA, M, 0)
+    want = cands.cpu().numpy()
+    assert np.array_equal(want[0], greedy.astype(np.uint8))
+    D, cut, obj, am = orc.eval_costs(L, ne, g, oA, oE, want)
+    sc = hp._out.cpu().numpy()
+    assert res.affinity.experts == M and res.greedy == list(greedy) and res.argmin == am
+    assert np.array_equal(sc[0], D) and np.array_equal(sc[1], cut) and np.array_equal(sc[2], obj)
+
+
 if __name__ == "__main__":
     globals()["case_" + sys.argv[1]](*sys.argv[2:])
     print("ok")

@@ -50,6 +50,11 @@ def test_eval_generic_for_small_shapes(L, ne, k, g, C):
     run_case({"GIMBAL_EVAL_NO_SMALL": "1"}, "eval", L, ne, k, g, C, 1.5, 0.25)
 
 
+@pytest.mark.parametrize("L,ne,k,g,C", [(32, 8, 2, 8, 4096), (7, 16, 4, 8, 33)])
+def test_unfused_pass_for_small_shapes(L, ne, k, g, C):
+    run_case({"GIMBAL_NO_TINY_PASS": "1"}, "pass", L, ne, k, g, C)
+
+
 @pytest.mark.parametrize("knobs,L,ne,k,T", [
     ({"GIMBAL_TMA_MODE": "u15"}, 58, 256, 8, 70001),
     ({"GIMBAL_NO_TMA": "1"}, 58, 256, 8, 70001),
@@ -57,6 +62,7 @@ def test_eval_generic_for_small_shapes(L, ne, k, g, C):
     ({"GIMBAL_COUNT_PATH": "atomic"}, 48, 128, 8, 30001),
     ({"GIMBAL_NO_DIRECT": "1"}, 26, 64, 6, 30001),
     ({"GIMBAL_NO_SMALL": "1"}, 32, 8, 2, 30001),
+    ({"GIMBAL_SMALL_BYTEWISE": "1"}, 32, 8, 2, 30001),
 ])
 def test_alternate_counters(knobs, L, ne, k, T):
     run_case(knobs, "count", L, ne, k, T)

@@ -159,6 +159,38 @@ def test_mma_stack_out_of_range(G, bad):
         s.read()
 
 
+@pytest.mark.parametrize("L,ne,T,offset,dup,bad", [(32, 8, 70001, 0, False, None), (32, 8, 1, 0, False, None),
+                                                  (32, 8, 5000, 0, True, None), (16, 16, 9001, 0, True, None),
+                                                  (32, 8, 3000, 0, False, (2999, 31, 1, 8)),
+                                                  (32, 16, 3000, 0, False, (5, 0, 0, 200)),
+                                                  (32, 8, 3000, 8, False, None), (30, 8, 3000, 0, False, None)])
+def test_small2_count_layouts(G, orc, L, ne, T, offset, dup, bad):
+    """Top-2 traces of 8 / 16 experts are counted word-wise (small_count.cu small_count_row2):
+    ragged blocks, one token, repeated ids, an out-of-range id (that row falls back to the
+    byte-wise loop and the call reports the error), an unaligned base and L = 30 (even row stride:
+    the byte-wise kernel)."""
+    k = 2
+    topo = G.MoeTopology(L, ne, k, 8)
+    rng = np.random.default_rng(T + 7 * L + ne)
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    if dup:
+        ids[::3, :, 1] = ids[::3, :, 0]
+    if bad is not None:
+        ids[bad[0], bad[1], bad[2]] = bad[3]
+    buf = torch.empty(T * L * k + offset, dtype=torch.uint8, device="cuda")
+    dev = buf[offset:].view(T, L, k)
+    dev.copy_(torch.from_numpy(ids))
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(dev)
+    if bad is not None:
+        with pytest.raises(IndexError):
+            s.read()
+        return
+    A, E, W = s.read()
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
+
+
 @pytest.mark.parametrize("ne,bad", [(128, 128), (128, 255), (100, 100)])
 def test_mma_direct_out_of_range(G, ne, bad):
     L, k = 6, 8

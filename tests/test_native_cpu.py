@@ -43,7 +43,7 @@ def test_library_is_sm100a_only(G):
 
 
 def test_abi_version(G):
-    assert G._native.lib().gimbal_abi_version() == G._native.ABI_VERSION == 3
+    assert G._native.lib().gimbal_abi_version() == G._native.ABI_VERSION == 4
 
 
 def test_topology_validation_messages(G):
@@ -148,4 +148,5 @@ def test_bench_entry_points_exist():
 
     for cfg, (L, ne, k, g, T, C, _) in bench.CONFIGS.items():
         n = bench.kernel_launches_per_step(G.MoeTopology(L, ne, k, g), 1, tokens=T)
-        assert 8 <= n <= 40, (cfg, n)
+        # Mixtral: counting + the fused small-shape pass; the others: the multi-kernel pass
+        assert (n == 2) if cfg == "mixtral" else (8 <= n <= 40), (cfg, n)
