@@ -2,16 +2,17 @@
 // token_crossings (sim.cpp:183-198), one engine iteration at a time.
 //
 // Per iteration the routed ids of the batch ([n][L][k], packed to uint8 on the host) go to the
-// device in one copy, and two kernels do the whole per-token loop of the reference:
-//   online_count_kernel  every (token, layer) unit: the window statistics (all k x k pairings into
-//                        E, as RoutingStats::add_token, moe.cpp:169-191), the layer x GPU load
-//                        histogram under the current placement (layer_gpu_tokens_) and the
-//                        cross-GPU transitions (token_crossings);
+// device in one copy, and three kernels do the whole per-token loop of the reference:
+//   online_count_kernel  every (token, layer) unit: the layer x GPU load histogram under the
+//                        current placement (layer_gpu_tokens_) and the id checks;
+//   online_pairs_kernel  (beside it) the window statistics (all k x k pairings into E, as
+//                        RoutingStats::add_token, moe.cpp:169-191) in shared-memory tables of a
+//                        block of E rows per CTA, and the cross-GPU transitions (token_crossings);
 //   online_finish_kernel per-layer peaks, the bottleneck excess sum_l max(0, peak_l g / (n k) - 1)
 //                        in the reference's double arithmetic and layer order, the lifetime
 //                        per-GPU activation totals (gpu_activation_total_), and the reset of the
 //                        per-iteration accumulators.
-// The copy, both kernels and the 16-byte read-back of {excess_sum, crossings} are one CUDA graph
+// The copy, the kernels and the 16-byte read-back of {excess_sum, crossings} are one CUDA graph
 // (node parameters updated per launch for the batch size); the host turns them into seconds with
 // the reference's own expression.  Statistics stay device-resident: the window handle is the
 // caller's gimbal_stats_t (its E/A feed maybe_relocate's greedy on the GPU).
@@ -36,11 +37,13 @@ struct OnlineOut {
   long long crossings;
 };
 
+// with_pairs = 0: the layer pairs (E, crossings) are online_pairs_kernel's; this kernel does the
+// histogram, the id checks and (L = 1) the activation only.
 __global__ void __launch_bounds__(kOnlineThreads)
     online_count_kernel(const uint8_t* __restrict__ ids, long long n, int L, int ne, int k, int g,
                         const uint8_t* __restrict__ place, unsigned long long* __restrict__ E,
                         unsigned long long* __restrict__ A, unsigned int* __restrict__ hist,
-                        unsigned long long* __restrict__ crossings, uint32_t* __restrict__ flags) {
+                        unsigned long long* __restrict__ crossings, uint32_t* __restrict__ flags, int with_pairs) {
   extern __shared__ unsigned int sh_hist[];  // [L][g]
   for (int i = threadIdx.x; i < L * g; i += blockDim.x) sh_hist[i] = 0u;
   __syncthreads();
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(kOnlineThreads)
       atomicAdd(&sh_hist[l * g + pl[e]], 1u);
       if (L == 1) atomicAdd(A + e, 1ull);  // no layer pairs: activation is the counted buffer
     }
-    if (l + 1 < L) {
+    if (with_pairs && l + 1 < L) {
       const uint8_t* nxt = row + k;
       const uint8_t* pn = pl + ne;
       unsigned long long* El = E + (long long)l * nE;
@@ -88,6 +91,71 @@ __global__ void __launch_bounds__(kOnlineThreads)
   __syncthreads();
   for (int i = threadIdx.x; i < L * g; i += blockDim.x)
     if (sh_hist[i]) atomicAdd(hist + i, sh_hist[i]);
+}
+
+// The window's E for one iteration, one CTA per (layer pair l, block of `rows` rows of E_l): the
+// CTA counts every token's k x k pairings whose layer-l id falls in its rows into shared u32
+// cells, then adds them to E (it is the only writer of those cells in this launch: plain
+// read-modify-write, no global atomics) and counts the pairings that cross GPUs under the current
+// placement (token_crossings, sim.cpp:183-198: the same sum, grouped by cell).  Invalid ids are
+// skipped one by one, as in online_count_kernel (which flags them).
+__global__ void __launch_bounds__(kOnlineThreads)
+    online_pairs_kernel(const uint8_t* __restrict__ ids, long long n, int L, int ne, int k, int rows, int parts,
+                        const uint8_t* __restrict__ place, unsigned long long* __restrict__ E,
+                        unsigned long long* __restrict__ crossings) {
+  extern __shared__ unsigned int tab[];  // [rows][ne]
+  const int l = blockIdx.x / parts;
+  const int r0 = (blockIdx.x - l * parts) * rows;
+  const int r1 = min(ne, r0 + rows);
+  const int cells = (r1 - r0) * ne;
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) tab[i] = 0u;
+  __syncthreads();
+  if (k == 8) {  // top-8 rows: one 8-byte load per token-layer (the staging buffer is 256-B aligned)
+    for (long long t = threadIdx.x; t < n; t += blockDim.x) {
+      const unsigned long long* row = reinterpret_cast<const unsigned long long*>(ids) + t * L + l;
+      const unsigned long long cw = __ldg(row), nw = __ldg(row + 1);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        const int j = (int)((cw >> (8 * a)) & 0xffu);
+        if (j < r0 || j >= r1) continue;
+        unsigned int* trow = tab + (j - r0) * ne;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const int kk = (int)((nw >> (8 * b)) & 0xffu);
+          if (kk < ne) atomicAdd(trow + kk, 1u);
+        }
+      }
+    }
+  } else {
+    for (long long t = threadIdx.x; t < n; t += blockDim.x) {
+      const uint8_t* cur = ids + (t * L + l) * k;
+      const uint8_t* nxt = cur + k;
+      for (int a = 0; a < k; ++a) {
+        const int j = cur[a];
+        if (j < r0 || j >= r1) continue;  // also every id >= ne
+        unsigned int* trow = tab + (j - r0) * ne;
+        for (int b = 0; b < k; ++b) {
+          const int kk = nxt[b];
+          if (kk < ne) atomicAdd(trow + kk, 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  unsigned long long cross = 0;
+  const uint8_t* pl = place + (long long)l * ne;
+  const uint8_t* pn = pl + ne;
+  unsigned long long* El = E + ((long long)l * ne + r0) * ne;
+  for (int i = threadIdx.x; i < cells; i += blockDim.x) {
+    const unsigned int v = tab[i];
+    if (v == 0u) continue;
+    const int jr = i / ne, kk = i - jr * ne;
+    El[i] += v;
+    cross += pl[r0 + jr] != pn[kk] ? v : 0u;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cross += __shfl_xor_sync(0xffffffffu, cross, o);
+  if ((threadIdx.x & 31) == 0 && cross) atomicAdd(crossings, cross);
 }
 
 __global__ void online_finish_kernel(long long n, int L, int k, int g, unsigned int* __restrict__ hist,
@@ -140,17 +208,22 @@ struct gimbal_online_s {
   OnlineOut* d_out = nullptr;
   OnlineOut* h_out = nullptr;  // pinned
   bool placed = false;
-  // the iteration as a graph: H2D ids -> count -> finish -> D2H result
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_finish = nullptr, n_d2h = nullptr;
+  // the iteration as a graph: H2D ids -> count [+ pairs] -> finish -> D2H result; two variants
+  // (mode 0: online_count_kernel counts E with global atomics -- small batches; mode 1: the
+  // shared-memory pair tables of online_pairs_kernel -- large batches)
+  struct Graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_pairs = nullptr, n_finish = nullptr, n_d2h = nullptr;
+  } gr[2];
   int64_t iterations = 0;
 
   void release() {
-    if (exec) cudaGraphExecDestroy(exec);
-    if (graph) cudaGraphDestroy(graph);
-    exec = nullptr;
-    graph = nullptr;
+    for (Graph& x : gr) {
+      if (x.exec) cudaGraphExecDestroy(x.exec);
+      if (x.graph) cudaGraphDestroy(x.graph);
+      x = Graph{};
+    }
     cudaFree(d_ids);
     cudaFreeHost(h_ids);
     d_ids = nullptr;
@@ -173,66 +246,125 @@ int grow(gimbal_online_t o, int64_t n) {
   return GIMBAL_OK;
 }
 
-int build_graph(gimbal_online_t o, int64_t n, unsigned grid) {
-  GIMBAL_CUDA_TRY(cudaGraphCreate(&o->graph, 0));
-  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&o->n_h2d, o->graph, nullptr, 0, o->d_ids, o->h_ids,
-                                           (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
-  long long nn = n;
-  int L = o->L, ne = o->ne, k = o->k, g = o->g;
-  const uint8_t* ids = o->d_ids;
-  const uint8_t* place = o->d_place;
-  unsigned long long *E = o->si.dE, *A = o->si.dA, *cross = o->d_cross, *totals = o->d_totals;
-  unsigned int* hist = o->d_hist;
-  uint32_t* flags = o->si.dflags;
-  OnlineOut* out = o->d_out;
-  void* cargs[] = {(void*)&ids, &nn, &L, &ne, &k, &g, (void*)&place, &E, &A, &hist, &cross, &flags};
-  cudaKernelNodeParams kp{};
+// Pair kernel geometry: rows of E_l per CTA so that a CTA's u32 cells fit 96 KB of shared memory
+// (every CTA of a pair reads the pair's two id columns of the whole batch: fewer, larger CTAs).
+struct PairGrid {
+  int rows, parts;
+  unsigned ctas;
+  unsigned smem;
+};
+PairGrid pair_grid(const gimbal_online_s* o) {
+  PairGrid pg;
+  pg.rows = std::max(1, std::min(o->ne, (96 * 1024 / 4) / o->ne));
+  pg.parts = (o->ne + pg.rows - 1) / pg.rows;
+  pg.ctas = (unsigned)((o->L - 1) * pg.parts);
+  pg.smem = (unsigned)(pg.rows * o->ne * 4);
+  return pg;
+}
+
+// the iteration's kernel node parameters for batch size n (the argument arrays live in `a`)
+struct NodeArgs {
+  long long nn;
+  int L, ne, k, g, with_pairs, rows, parts;
+  const uint8_t* ids;
+  const uint8_t* place;
+  unsigned long long *E, *A, *cross, *totals;
+  unsigned int* hist;
+  uint32_t* flags;
+  OnlineOut* out;
+  void* cargs[13];
+  void* pargs[10];
+  void* fargs[8];
+};
+
+void node_params(gimbal_online_t o, int mode, int64_t n, unsigned grid, NodeArgs& a, cudaKernelNodeParams& kp,
+                 cudaKernelNodeParams& pp, cudaKernelNodeParams& fp) {
+  const PairGrid pg = pair_grid(o);
+  a.nn = n;
+  a.L = o->L;
+  a.ne = o->ne;
+  a.k = o->k;
+  a.g = o->g;
+  a.with_pairs = mode == 1 ? 0 : 1;  // mode 1: online_pairs_kernel counts E and the crossings
+  a.rows = pg.rows;
+  a.parts = pg.parts;
+  a.ids = o->d_ids;
+  a.place = o->d_place;
+  a.E = o->si.dE;
+  a.A = o->si.dA;
+  a.cross = o->d_cross;
+  a.totals = o->d_totals;
+  a.hist = o->d_hist;
+  a.flags = o->si.dflags;
+  a.out = o->d_out;
+  void* c[] = {(void*)&a.ids, &a.nn, &a.L, &a.ne, &a.k, &a.g, (void*)&a.place, &a.E, &a.A, &a.hist, &a.cross,
+               &a.flags, &a.with_pairs};
+  std::copy(c, c + 13, a.cargs);
+  void* q[] = {(void*)&a.ids, &a.nn, &a.L, &a.ne, &a.k, &a.rows, &a.parts, (void*)&a.place, &a.E, &a.cross};
+  std::copy(q, q + 10, a.pargs);
+  void* f[] = {&a.nn, &a.L, &a.k, &a.g, &a.hist, &a.cross, &a.totals, &a.out};
+  std::copy(f, f + 8, a.fargs);
+  kp = cudaKernelNodeParams{};
   kp.func = (void*)online_count_kernel;
   kp.gridDim = dim3(grid);
   kp.blockDim = dim3(kOnlineThreads);
   kp.sharedMemBytes = (unsigned)(o->L * o->g * 4);
-  kp.kernelParams = cargs;
-  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&o->n_count, o->graph, &o->n_h2d, 1, &kp));
-  void* fargs[] = {&nn, &L, &k, &g, &hist, &cross, &totals, &out};
-  cudaKernelNodeParams fp{};
+  kp.kernelParams = a.cargs;
+  pp = cudaKernelNodeParams{};
+  pp.func = (void*)online_pairs_kernel;
+  pp.gridDim = dim3(std::max(1u, pg.ctas));
+  pp.blockDim = dim3(kOnlineThreads);
+  pp.sharedMemBytes = pg.smem;
+  pp.kernelParams = a.pargs;
+  fp = cudaKernelNodeParams{};
   fp.func = (void*)online_finish_kernel;
   fp.gridDim = dim3(1);
   fp.blockDim = dim3(256);
-  fp.kernelParams = fargs;
-  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&o->n_finish, o->graph, &o->n_count, 1, &fp));
-  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&o->n_d2h, o->graph, &o->n_finish, 1, o->h_out, o->d_out,
+  fp.kernelParams = a.fargs;
+}
+
+// Mode 1 (pair tables) when the batch's pairings outnumber the pair tables' cells: below that the
+// tables' zeroing and read-out cost more than global atomics into the L2-resident E.
+int online_mode(const gimbal_online_s* o, int64_t n) {
+  return o->L > 1 && n * (int64_t)o->k * o->k >= (int64_t)o->ne * o->ne / 4 && n >= 256 ? 1 : 0;
+}
+
+// H2D ids -> {histogram kernel, pair kernel} (mode 1) or the combined kernel (mode 0) -> finish
+// -> D2H result
+int build_graph(gimbal_online_t o, int mode, int64_t n, unsigned grid) {
+  GIMBAL_CUDA_TRY(cudaFuncSetAttribute(online_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+  gimbal_online_s::Graph& x = o->gr[mode];
+  GIMBAL_CUDA_TRY(cudaGraphCreate(&x.graph, 0));
+  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&x.n_h2d, x.graph, nullptr, 0, o->d_ids, o->h_ids,
+                                           (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
+  NodeArgs a;
+  cudaKernelNodeParams kp, pp, fp;
+  node_params(o, mode, n, grid, a, kp, pp, fp);
+  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_count, x.graph, &x.n_h2d, 1, &kp));
+  cudaGraphNode_t before_finish[2] = {x.n_count, nullptr};
+  int n_before = 1;
+  if (mode == 1) {
+    GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_pairs, x.graph, &x.n_h2d, 1, &pp));
+    before_finish[n_before++] = x.n_pairs;
+  }
+  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_finish, x.graph, before_finish, n_before, &fp));
+  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&x.n_d2h, x.graph, &x.n_finish, 1, o->h_out, o->d_out,
                                            sizeof(OnlineOut), cudaMemcpyDeviceToHost));
-  GIMBAL_CUDA_TRY(cudaGraphInstantiate(&o->exec, o->graph, 0));
+  GIMBAL_CUDA_TRY(cudaGraphInstantiate(&x.exec, x.graph, 0));
   return GIMBAL_OK;
 }
 
 // batch size n -> graph node parameters (copy size, kernel n and grid)
-int update_graph(gimbal_online_t o, int64_t n, unsigned grid) {
-  GIMBAL_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(o->exec, o->n_h2d, o->d_ids, o->h_ids,
+int update_graph(gimbal_online_t o, int mode, int64_t n, unsigned grid) {
+  gimbal_online_s::Graph& x = o->gr[mode];
+  GIMBAL_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(x.exec, x.n_h2d, o->d_ids, o->h_ids,
                                                      (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
-  long long nn = n;
-  int L = o->L, ne = o->ne, k = o->k, g = o->g;
-  const uint8_t* ids = o->d_ids;
-  const uint8_t* place = o->d_place;
-  unsigned long long *E = o->si.dE, *A = o->si.dA, *cross = o->d_cross, *totals = o->d_totals;
-  unsigned int* hist = o->d_hist;
-  uint32_t* flags = o->si.dflags;
-  OnlineOut* out = o->d_out;
-  void* cargs[] = {(void*)&ids, &nn, &L, &ne, &k, &g, (void*)&place, &E, &A, &hist, &cross, &flags};
-  cudaKernelNodeParams kp{};
-  kp.func = (void*)online_count_kernel;
-  kp.gridDim = dim3(grid);
-  kp.blockDim = dim3(kOnlineThreads);
-  kp.sharedMemBytes = (unsigned)(o->L * o->g * 4);
-  kp.kernelParams = cargs;
-  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(o->exec, o->n_count, &kp));
-  void* fargs[] = {&nn, &L, &k, &g, &hist, &cross, &totals, &out};
-  cudaKernelNodeParams fp{};
-  fp.func = (void*)online_finish_kernel;
-  fp.gridDim = dim3(1);
-  fp.blockDim = dim3(256);
-  fp.kernelParams = fargs;
-  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(o->exec, o->n_finish, &fp));
+  NodeArgs a;
+  cudaKernelNodeParams kp, pp, fp;
+  node_params(o, mode, n, grid, a, kp, pp, fp);
+  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(x.exec, x.n_count, &kp));
+  if (mode == 1) GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(x.exec, x.n_pairs, &pp));
+  GIMBAL_CUDA_TRY(cudaGraphExecKernelNodeSetParams(x.exec, x.n_finish, &fp));
   return GIMBAL_OK;
 }
 
@@ -324,29 +456,34 @@ int gimbal_online_iteration(gimbal_online_t o, const void* ids, int id_bytes, in
   std::lock_guard<std::mutex> lk(*o->si.mu);
   DeviceGuard dg(o->si.device);
   GIMBAL_TRY(stats_resolve_tokens(o->window));
-  const bool regrow = n > o->cap;
   GIMBAL_TRY(grow(o, n));
   const size_t cnt = (size_t)n * o->L * o->k;
   if (id_bytes == 1) {
     std::memcpy(o->h_ids, ids, cnt);
   } else {  // int32 (RoutedStream::choices) -> uint8 (n_e <= 256); the reference leaves bad ids UB
+    // branch-free (vectorisable) conversion with one range verdict for the whole batch
     const int32_t* s = static_cast<const int32_t*>(ids);
+    const uint32_t ne = (uint32_t)o->ne;
+    uint32_t bad = 0;
     for (size_t i = 0; i < cnt; ++i) {
-      if (s[i] < 0 || s[i] >= o->ne) {
-        set_error("add_token: expert id out of range [0, n_experts)");
-        return GIMBAL_OUT_OF_RANGE;
-      }
-      o->h_ids[i] = (uint8_t)s[i];
+      const uint32_t v = (uint32_t)s[i];  // negative ids wrap above n_e
+      bad |= v >= ne ? 1u : 0u;
+      o->h_ids[i] = (uint8_t)v;
+    }
+    if (bad) {
+      set_error("add_token: expert id out of range [0, n_experts)");
+      return GIMBAL_OUT_OF_RANGE;
     }
   }
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (n * o->L + kOnlineThreads - 1) / kOnlineThreads));
-  if (!o->exec || regrow) {
-    GIMBAL_TRY(build_graph(o, n, grid));
+  const int mode = online_mode(o, n);
+  if (!o->gr[mode].exec) {  // (grow() drops both graphs when the staging buffers move)
+    GIMBAL_TRY(build_graph(o, mode, n, grid));
   } else {
-    GIMBAL_TRY(update_graph(o, n, grid));
+    GIMBAL_TRY(update_graph(o, mode, n, grid));
   }
-  GIMBAL_CUDA_TRY(cudaGraphLaunch(o->exec, o->si.stream));
+  GIMBAL_CUDA_TRY(cudaGraphLaunch(o->gr[mode].exec, o->si.stream));
   GIMBAL_CUDA_TRY(cudaStreamSynchronize(o->si.stream));
   stats_note_added(o->window, n);
   ++o->iterations;

@@ -44,7 +44,7 @@ class OnlineHook:
         returns (excess_sum, crossings) — sum over layers of max(0, peak * g / (n * k) - 1) and
         the cross-GPU transition count (sim.cpp:132-146 turns them into seconds)."""
         a = np.asarray(ids)
-        a = np.ascontiguousarray(a if a.dtype == np.uint8 else a.astype(np.int32))
+        a = np.ascontiguousarray(a if a.dtype == np.uint8 else a.astype(np.int32, copy=False))
         per = self.topo.n_layers * self.topo.top_k
         if a.size % per:
             raise ValueError("add_token: choice span size mismatch")

@@ -44,8 +44,12 @@ def main():
             for i in range(args.iters):
                 hook.iteration(batches[i % 8])
             gpu_us = (time.perf_counter() - t0) / args.iters * 1e6
+            b32 = [b.astype(np.int32) for b in batches]  # RoutedStream::choices as the engine passes them
+            t0 = time.perf_counter()
+            for i in range(args.iters):
+                hook.iteration(b32[i % 8])
+            gpu32_us = (time.perf_counter() - t0) / args.iters * 1e6
             rh = ref.hook_create(L, ne, k, g, assign)
-            b32 = [b.astype(np.int32) for b in batches]
             ref.hook_iteration(rh, b32[0])
             iters = max(3, min(args.iters, int(2.0 / max(1e-6, 1e-7 * n * L * k * k))))
             t0 = time.perf_counter()
@@ -54,7 +58,7 @@ def main():
             cpu_us = (time.perf_counter() - t0) / iters * 1e6
             ref.hook_destroy(rh)
             rows.append({"shape": name, "L": L, "n_e": ne, "k": k, "g": g, "tokens_per_iteration": n,
-                         "gpu_hook_us": gpu_us, "reference_host_loop_us": cpu_us, "speedup": cpu_us / gpu_us,
+                         "gpu_hook_us": gpu_us, "gpu_hook_int32_ids_us": gpu32_us, "reference_host_loop_us": cpu_us, "speedup": cpu_us / gpu_us,
                          "gpu_iters": args.iters, "host_iters": iters})
             print(json.dumps(rows[-1]), flush=True)
 
