@@ -47,15 +47,17 @@ METRIC = "routed tokens/s (expert load+affinity stats, placement eval)"
 # atomic increments to random addresses of a 128 KB table, 148 CTAs x 1024 threads.
 ATOMS_RANDOM_PEAK = 2.553e12
 # dram__bytes_read.sum + dram__bytes_write.sum per counting launch from one `ncu --set full`
-# capture (profiles/r1c_ncu_count_<config>.md), bytes / launch, with the tokens of that launch.
-TRAFFIC = {"dsv3": {"bytes": 52.823845e9 + 1.497470e9, "tokens_in_launch": 67108864,
-                    "source": "profiles/r1f_ncu_count_dsv3.md"},
-           "qwen3": {"bytes": 35.337853e9 + 18.544128e6, "tokens_in_launch": 33554432,
-                     "source": "profiles/r1f_ncu_count_qwen3.md"},
-           "dsv2lite": {"bytes": 4.358883e9 + 5.723648e6, "tokens_in_launch": 16777216,
-                        "source": "profiles/r1f_ncu_count_dsv2lite.md"},
-           "mixtral": {"bytes": 67.134720e6 + 344.576e3, "tokens_in_launch": 1048576,
-                       "source": "profiles/r1f_ncu_count_mixtral.md"}}
+# capture (profiles/r2b/ncu_count_r2b_<config>.txt, tools/gpu_profile_r2b.sh), bytes / launch, with
+# the tokens of that launch; for the tensor-core counters also the tensor pipe's active cycles
+# (sm__pipe_tensor_cycles_active, % of elapsed) from the same capture.
+TRAFFIC = {"dsv3": {"bytes": 63.036018e9 + 1.761288e9, "tokens_in_launch": 67108864,
+                    "source": "profiles/r2b/ncu_count_r2b_dsv3.txt"},
+           "qwen3": {"bytes": 60.180595e9 + 25.665280e6, "tokens_in_launch": 33554432,
+                     "source": "profiles/r2b/ncu_count_r2b_qwen3.txt", "tensor_pipe_active_pct": 35.057135},
+           "dsv2lite": {"bytes": 3.962039e9 + 6.150656e6, "tokens_in_launch": 16777216,
+                        "source": "profiles/r2b/ncu_count_r2b_dsv2lite.txt", "tensor_pipe_active_pct": 15.320577},
+           "mixtral": {"bytes": 67.141888e6 + 429.056e3, "tokens_in_launch": 1048576,
+                       "source": "profiles/r2b/ncu_count_r2b_mixtral.txt"}}
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 REASON_BITS = {
@@ -486,7 +488,10 @@ def make_roofline(args, topo, T, count_total_ms, count_launches, ms, traffic=Tru
                 "frac": ops / tpeak,
                 "peak_source": ("2 x measured bf16 dense (MEASURED_PEAKS.json bf16_tflops; int8 dense = 2x bf16 "
                                 "on sm_100)" if bf16 else "B200_PROFILING.md fallback 4.5 POP/s"),
-                "useful_updates_per_s": upd}
+                "useful_updates_per_s": upd,
+                # the op model above, cross-checked by the tensor pipe's own counter (ncu capture)
+                "tensor_pipe_active_pct_ncu": TRAFFIC.get(args.config, {}).get("tensor_pipe_active_pct"),
+                "tensor_pipe_source": TRAFFIC.get(args.config, {}).get("source")}
         else:
             roof["atomic_ceiling"] = {"bound": "shared-memory atomics", "achieved": upd, "peak": ATOMS_RANDOM_PEAK,
                                       "unit": "E pair-updates/s", "frac": upd / ATOMS_RANDOM_PEAK,

@@ -13,7 +13,8 @@ KEYS = [
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
     "launch__shared_mem_per_block_dynamic", "launch__grid_size", "launch__block_size",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-    "sm__cycles_elapsed.avg.per_second",
+    "sm__cycles_elapsed.avg.per_second", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_tensor.sum",
 ]
 
 
