@@ -34,17 +34,31 @@ namespace gimbal_gpu {
 namespace {
 
 constexpr int kNe = 64;              // experts per layer (one half of the M = 128 operand)
-constexpr int kTok = 64;             // tokens per tile (two K = 32 MMA steps)
+#ifndef GIMBAL_STACK_TOK
+#define GIMBAL_STACK_TOK 64
+#endif
+constexpr int kTok = GIMBAL_STACK_TOK;  // tokens per tile (K = 32 MMA steps), a power of two
 constexpr int kSlotBytes = 512;      // one layer's 64 experts x 8 tokens (4 core matrices)
 #ifndef GIMBAL_STACK_CTAS
 #define GIMBAL_STACK_CTAS 1  // 2 (half the pairs per group, 2 stages): 4.95 vs 4.75 ms at DS-V2-Lite
 #endif
 constexpr int kCtasPerSm = GIMBAL_STACK_CTAS;             // CTAs per SM (TMEM and smem split)
-constexpr int kMaxPairs = 16 / kCtasPerSm;               // 8 / kCtasPerSm accumulators of 64 TMEM columns
+#ifndef GIMBAL_STACK_MAXPAIRS
+#define GIMBAL_STACK_MAXPAIRS (16 / GIMBAL_STACK_CTAS)
+#endif
+#ifndef GIMBAL_STACK_STAGES
+#define GIMBAL_STACK_STAGES (GIMBAL_STACK_CTAS > 1 ? 2 : 3)
+#endif
+#ifndef GIMBAL_STACK_THREADS
+#define GIMBAL_STACK_THREADS 512
+#endif
+constexpr int kMaxPairs = GIMBAL_STACK_MAXPAIRS;          // kMaxPairs / 2 accumulators of 64 TMEM columns
 constexpr int kTmemCols = 512 / kCtasPerSm;
-constexpr int kStages = kCtasPerSm > 1 ? 2 : 3;
+constexpr int kStages = GIMBAL_STACK_STAGES;
 constexpr int kIdSlots = 3;
-constexpr int kThreads = 512;
+constexpr int kThreads = GIMBAL_STACK_THREADS;
+constexpr int kTokShift = kTok == 128 ? 7 : 6;
+static_assert(kTok == 64 || kTok == 128, "tile of 64 or 128 tokens");
 
 struct StackParams {
   int L, k, row_bytes;    // trace row = L * k bytes per token
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       uint8_t* odd = stage + even_tile;
       const int64_t t0 = t_begin + (int64_t)it * kTok;
       for (int r = threadIdx.x; r < n_rows; r += kThreads) {
-        const int q = r >> 6, tt = r & (kTok - 1);  // layer offset, token in tile
+        const int q = r >> kTokShift, tt = r & (kTok - 1);  // layer offset, token in tile
         uint8_t* row = ((q & 1) ? odd + (tt >> 3) * odd_k : stage + (tt >> 3) * even_k) + (q >> 1) * kSlotBytes +
                        (tt & 7) * 16;
         const uint4 z = make_uint4(0, 0, 0, 0);
