@@ -105,21 +105,33 @@ class HotPathResult:
 
 
 class PendingPass:
-    """A queued pass (HotPath.run_async); result() waits for it and decodes its packed results."""
+    """A queued pass (HotPath.run_async); result() waits for it and decodes its packed results
+    (raising the pass's deferred device-side error, if any)."""
 
     def __init__(self, hp: "HotPath", host, event):
-        self._hp, self._host, self._event, self._res = hp, host, event, None
+        self._hp, self._host, self._event = hp, host, event
+        self._res, self._err = None, None
 
     def done(self) -> bool:
-        return self._res is not None or self._event.query()
+        return self._res is not None or self._err is not None or self._event.query()
+
+    def _resolve(self) -> None:
+        if self._res is not None or self._err is not None:
+            return
+        self._event.synchronize()
+        h = self._host.copy()  # the slot is reused by a later pass
+        if h[4] or h[5]:
+            try:
+                self._hp.stats.sync()  # raises (and clears) the deferred device-side error
+            except Exception as ex:  # kept for result(); a later pass's run_async must not raise it
+                self._err = ex
+                return
+        self._res = self._hp._decode_pk(h)
 
     def result(self) -> HotPathResult:
-        if self._res is None:
-            self._event.synchronize()
-            h = self._host.copy()  # the slot is reused by a later pass
-            if h[4] or h[5]:
-                self._hp.stats.sync()  # raises (and clears) the deferred device-side error
-            self._res = self._hp._decode_pk(h)
+        self._resolve()
+        if self._err is not None:
+            raise self._err
         return self._res
 
 
@@ -294,7 +306,7 @@ class HotPath:
         self._ring_next = (i + 1) % 8
         prev = self._ring_ev[i]
         if prev is not None:  # at most 8 passes in flight: the slot's previous pass is read out first
-            prev.result()
+            prev._resolve()
         m, C_ = topo.total_experts(), int(candidates.shape[0])
         scores = self._scores(C_)
         cur = torch.cuda.current_stream(torch.device("cuda", self.device))

@@ -122,7 +122,11 @@ def test_run_async_matches_run(G, orc, shape):
     for p in pend:
         r = p.result()
         assert r.argmin == want.argmin and r.greedy == want.greedy and r.affinity.experts == want.affinity.experts
-    cands[C // 2, 3] = (int(cands[C // 2, 3]) + 1) % g
-    bad = hp.run_async(trace, cands)
+    bad_cands = cands.clone()
+    bad_cands[C // 2, 3] = (int(bad_cands[C // 2, 3]) + 1) % g
+    bad = hp.run_async(trace, bad_cands)
+    later = [hp.run_async(trace, cands) for _ in range(12)]  # the ninth call reads `bad` out
+    for p in later:  # the bad pass's error stays with it
+        assert p.result().argmin == want.argmin
     with pytest.raises(ValueError, match="infeasible"):
         bad.result()
