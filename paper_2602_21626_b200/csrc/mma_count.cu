@@ -30,7 +30,10 @@ namespace gimbal_gpu {
 
 namespace {
 
-constexpr int kTok = 128;                  // tokens per tile (MMA K, 4 instructions of 32)
+#ifndef GIMBAL_MMA_TOK
+#define GIMBAL_MMA_TOK 128
+#endif
+constexpr int kTok = GIMBAL_MMA_TOK;       // tokens per tile (MMA K, kTok / 32 instructions of 32)
 constexpr int kRows = 128;                 // experts per tile row block (MMA M, N <= 128)
 constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
 #ifndef GIMBAL_MMA_PAIRS
@@ -38,9 +41,15 @@ constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
 #endif
 constexpr int kMaxPairs = GIMBAL_MMA_PAIRS;  // accumulators: kMaxPairs x 128 TMEM columns
 constexpr int kTmemCols = kMaxPairs <= 2 ? 256 : 512;
-constexpr int kCtasPerSm = kMaxPairs <= 2 ? 2 : 1;  // two CTAs (TMEM halves) overlap barrier stalls
-constexpr int kStages = 2;
-constexpr int kThreads = (kMaxPairs + 1) * kTok;           // one token-layer row per thread
+#ifndef GIMBAL_MMA_CTAS
+#define GIMBAL_MMA_CTAS (GIMBAL_MMA_PAIRS <= 2 ? 2 : 1)
+#endif
+#ifndef GIMBAL_MMA_STAGES
+#define GIMBAL_MMA_STAGES 2
+#endif
+constexpr int kCtasPerSm = GIMBAL_MMA_CTAS;  // two CTAs (TMEM halves) overlap barrier stalls
+constexpr int kStages = GIMBAL_MMA_STAGES;
+constexpr int kThreads = (kMaxPairs + 1) * 128;            // one token-layer row per thread per 128 tokens
 constexpr int kIdSlots = 3;                                 // TMA ring of id word tiles
 constexpr int kIdCols = kMaxPairs + 2;                      // token-major box: 6 layers (16-B aligned start)
 constexpr int kIdSlotWords = kIdCols * kTok;                // >= 5 layers x 128 tokens (layer-major)
@@ -173,8 +182,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t use = fill_count - (uint32_t)min(2, n_tiles - 1 - it) - 1;  // fill index of tile it
       mbar_wait(&id_bars[use % kIdSlots], (use / kIdSlots) & 1);
       const unsigned long long* w_tile = ids + (use % kIdSlots) * kIdSlotWords;
-      const int s = it_global & 1;
-      if (it_global >= kStages) mbar_wait(&bars[s], ((it_global >> 1) - 1) & 1);
+      const int s = (int)(it_global % kStages);
+      if (it_global >= kStages) mbar_wait(&bars[s], ((it_global / kStages) - 1) & 1);
       uint8_t* stage = smem + s * kStageBytes;
       const int64_t t0 = t_begin + (int64_t)it * kTok;
       // one thread per token-layer row: zero its 128 expert bytes (8 chunks, SBO apart), then
@@ -246,8 +255,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   }
   if (TM && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(prm.flags, (uint32_t)kFlagIdOutOfRange);
   // drain: every commit on the stage barriers has been waited for except the last one per stage
-  if (it_global >= 1) mbar_wait(&bars[(it_global - 1) & 1], ((it_global - 1) >> 1) & 1);
-  if (it_global >= 2) mbar_wait(&bars[(it_global - 2) & 1], ((it_global - 2) >> 1) & 1);
+  for (uint32_t d = 1; d <= (uint32_t)kStages && d <= it_global; ++d) {
+    const uint32_t g = it_global - d;
+    mbar_wait(&bars[g % kStages], (g / kStages) & 1);
+  }
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
