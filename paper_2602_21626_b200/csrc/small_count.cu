@@ -189,6 +189,130 @@ __global__ void __launch_bounds__(THREADS)
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
 }
 
+// ---- Top-2 over 8 experts (Mixtral): one shared atomic per token-pair instead of four ----
+// A token-layer's two ids form an unordered multiset t = {lo, hi} of 8 experts: tri(t) =
+// hi (hi + 1) / 2 + lo, 36 values.  A token-pair (layers l, l+1) is one event (tri_l, tri_l+1) out of
+// 36 x 36 = 1296, counted in a u16 histogram per pair (red.shared.add on packed halves).  At the end
+//   E_l(j, k) = sum over the 8 multisets t containing j, the 8 t' containing k of
+//               H_l(t, t') * m(j, t) * m(k, t'),   m(x, t) = multiplicity of x in t (1 or 2),
+// exactly the reference's k x k pairing count with multiplicity (moe.cpp:179-188).  Rows with an
+// out-of-range id take small_count_row into a per-CTA E table instead (flagged there).
+constexpr int kEvThreads = 1024;
+constexpr int kEvTri = 36;
+constexpr int kEvBinWords = kEvTri * kEvTri / 2;  // 648 u32 words = 1296 u16 bins per layer pair
+constexpr int kEvMaxBlocks = 63;                   // <= 64512 tokens per CTA: u16 bins cannot overflow
+
+__device__ __forceinline__ uint32_t ev_tri(uint32_t a, uint32_t b) {
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  return ((hi * (hi + 1u)) >> 1) + lo;
+}
+
+__global__ void __launch_bounds__(kEvThreads, 1)
+    count_events8_kernel(int L, const uint8_t* __restrict__ trace, int64_t T, int row_bytes, int stride,
+                         unsigned long long* __restrict__ E, uint32_t* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int pairs = L - 1;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sm);  // [pairs][648]
+  uint32_t* tab = hist + pairs * kEvBinWords;        // [pairs][64] cells of rows with bad ids
+  uint8_t* rows = reinterpret_cast<uint8_t*>(tab + pairs * 64);
+  for (int i = threadIdx.x; i < pairs * (kEvBinWords + 64); i += kEvThreads) hist[i] = 0u;
+  // tri of a token-layer from its two 3-bit ids (a | b << 3): one shared load per layer
+  __shared__ uint8_t tri_tab[64];
+  if (threadIdx.x < 64) tri_tab[threadIdx.x] = (uint8_t)ev_tri(threadIdx.x & 7u, threadIdx.x >> 3);
+  bool bad = false;
+  const uint32_t hist_s = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
+  constexpr int kPf = 4;  // rows of <= 64 bytes (events8_applies)
+  const int q = row_bytes >> 4;
+  const int64_t step = (int64_t)gridDim.x * kEvThreads;
+  uint4 pre[kPf];
+  auto load = [&](int64_t t0) {
+    const int n = (int)min((int64_t)kEvThreads, T - t0);
+    const uint4* src = reinterpret_cast<const uint4*>(trace + t0 * row_bytes);
+#pragma unroll
+    for (int r = 0; r < kPf; ++r) {
+      const int i = threadIdx.x + r * kEvThreads;
+      if (i < n * q) pre[r] = __ldcs(src + i);
+    }
+  };
+  int64_t t0 = (int64_t)blockIdx.x * kEvThreads;
+  if (t0 < T) load(t0);
+  for (; t0 < T; t0 += step) {
+    const int n = (int)min((int64_t)kEvThreads, T - t0);
+    __syncthreads();  // the previous block's rows are consumed (and the tables are zeroed)
+#pragma unroll
+    for (int r = 0; r < kPf; ++r) {
+      const int i = threadIdx.x + r * kEvThreads;
+      if (i < n * q) {
+        const int rr = i / q, w = i - rr * q;
+        uint32_t* d = reinterpret_cast<uint32_t*>(rows + rr * stride + w * 16);
+        d[0] = pre[r].x;
+        d[1] = pre[r].y;
+        d[2] = pre[r].z;
+        d[3] = pre[r].w;
+      }
+    }
+    __syncthreads();
+    if (t0 + step < T) load(t0 + step);
+    if (threadIdx.x < n) {
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + threadIdx.x * stride);
+      uint32_t acc = 0;
+      for (int w = 0; w < L / 2; ++w) acc |= row[w];
+      if (acc & 0xf8f8f8f8u) {
+        bad |= small_count_row<2>(reinterpret_cast<const uint8_t*>(row), L, 8, tab);
+      } else {
+        // ids < 8 (checked above): a layer's index into tri_tab is (id0 & 7) | (id1 & 7) << 3
+        auto tri_lo = [&](uint32_t v) { return (uint32_t)tri_tab[(v & 7u) | ((v >> 5) & 0x38u)]; };
+        uint32_t w = row[0];
+        uint32_t tp = tri_lo(w) * kEvTri;  // this layer's tri x 36
+        uint32_t base = hist_s;
+        for (int lw = 0; lw < L / 2; ++lw) {
+          const uint32_t tn = tri_lo(w >> 16);  // layer 2 lw + 1
+          uint32_t bin = tp + tn;
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + (bin >> 1) * 4), "r"(1u << ((bin & 1u) << 4))
+                       : "memory");
+          base += kEvBinWords * 4;
+          if (lw + 1 == L / 2) break;
+          w = row[lw + 1];
+          const uint32_t tm = tri_lo(w);  // layer 2 lw + 2
+          bin = tn * kEvTri + tm;
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + (bin >> 1) * 4), "r"(1u << ((bin & 1u) << 4))
+                       : "memory");
+          base += kEvBinWords * 4;
+          tp = tm * kEvTri;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // expand the events into the pair's 8 x 8 cells (one thread per cell, no atomics), add to E
+  for (int cell = threadIdx.x; cell < pairs * 64; cell += kEvThreads) {
+    const int p = cell >> 6, j = (cell >> 3) & 7, kk = cell & 7;
+    const uint32_t* H = hist + p * kEvBinWords;
+    unsigned long long sum = tab[cell];
+    uint32_t tk[8];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) tk[y] = ev_tri((uint32_t)kk, (uint32_t)y);
+#pragma unroll 1
+    for (int x = 0; x < 8; ++x) {
+      const uint32_t tj = ev_tri((uint32_t)j, (uint32_t)x) * kEvTri;
+      uint32_t row_sum = 0;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const uint32_t bin = tj + tk[y];
+        const uint32_t c = (H[bin >> 1] >> ((bin & 1u) << 4)) & 0xffffu;
+        row_sum += y == kk ? 2u * c : c;
+      }
+      sum += (unsigned long long)(x == j ? 2u : 1u) * row_sum;
+    }
+    if (sum) atomicAdd(E + cell, sum);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
+}
+
+size_t events8_smem(int L) {
+  return (size_t)(L - 1) * (kEvBinWords + 64) * 4 + (size_t)kEvThreads * (L * 2 + 4);
+}
+
 size_t small_smem(int L, int ne, int k, int threads = kSmallThreads) {
   const size_t table = ((size_t)(L - 1) * ne * ne * 4 + 15) & ~(size_t)15;
   return table + (size_t)threads * ((size_t)L * k + 4);
@@ -217,6 +341,17 @@ bool small_count_supported(int L, int ne, int k, int id_bytes, int64_t T) {
 cudaError_t launch_count_small(int L, int ne, int k, int sms, const uint8_t* trace, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
+  if (ne == 8 && small2_applies(L, ne, k, trace) && L * k <= 64 && events8_smem(L) <= 200 * 1024 &&
+      !GIMBAL_KNOB("GIMBAL_SMALL_BYTEWISE") && !GIMBAL_KNOB("GIMBAL_SMALL_NO_EVENTS")) {
+    const int64_t blocks = (T + kEvThreads - 1) / kEvThreads;
+    int64_t grid = std::min<int64_t>(sms, blocks);
+    grid = std::max<int64_t>(grid, (blocks + kEvMaxBlocks - 1) / kEvMaxBlocks);  // u16 bins
+    const size_t smem = events8_smem(L);
+    cudaError_t e = cudaFuncSetAttribute(count_events8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    count_events8_kernel<<<(unsigned)grid, kEvThreads, smem, s>>>(L, trace, T, L * k, L * k + 4, E, flags);
+    return cudaGetLastError();
+  }
   if (small2_applies(L, ne, k, trace) && !GIMBAL_KNOB("GIMBAL_SMALL_BYTEWISE")) {
     const size_t smem = small_smem(L, ne, k, kSmall2Threads);
     int64_t grid = std::min<int64_t>(sms, (T + kSmall2Threads - 1) / kSmall2Threads);

@@ -63,6 +63,7 @@ def test_unfused_pass_for_small_shapes(L, ne, k, g, C):
     ({"GIMBAL_NO_DIRECT": "1"}, 26, 64, 6, 30001),
     ({"GIMBAL_NO_SMALL": "1"}, 32, 8, 2, 30001),
     ({"GIMBAL_SMALL_BYTEWISE": "1"}, 32, 8, 2, 30001),
+    ({"GIMBAL_SMALL_NO_EVENTS": "1"}, 32, 8, 2, 30001),
 ])
 def test_alternate_counters(knobs, L, ne, k, T):
     run_case(knobs, "count", L, ne, k, T)

@@ -191,6 +191,20 @@ def test_small2_count_layouts(G, orc, L, ne, T, offset, dup, bad):
     assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW)
 
 
+def test_events8_bin_bound(G, orc):
+    """Top-2 over 8 experts counts token-pair events in 16-bit bins: 10.5 Mi tokens of one repeated
+    id per layer put every token into the same bin of every pair, so the launcher must split the
+    trace over more CTAs than SMs (<= 63 blocks of 1024 tokens each); E_l(0, 0) = 4 T (the pair
+    (0, 0) counted with multiplicity 2 x 2)."""
+    L, ne, k, T = 32, 8, 2, 10_500_000
+    topo = G.MoeTopology(L, ne, k, 8)
+    s = G.RoutingStats(topo, 0)
+    s.add_tokens(torch.zeros((T, L, k), dtype=torch.uint8, device="cuda"))
+    A, E, W = s.read()
+    assert (E[:, 0, 0] == 4 * T).all() and E.sum() == (L - 1) * 4 * T
+    assert (A[:, 0] == 2 * T).all() and A.sum() == L * 2 * T
+
+
 @pytest.mark.parametrize("ne,bad", [(128, 128), (128, 255), (100, 100)])
 def test_mma_direct_out_of_range(G, ne, bad):
     L, k = 6, 8
