@@ -12,7 +12,8 @@
 //                        in the reference's double arithmetic and layer order, the lifetime
 //                        per-GPU activation totals (gpu_activation_total_), and the reset of the
 //                        per-iteration accumulators.
-// The copy, the kernels and the 16-byte read-back of {excess_sum, crossings} are one CUDA graph
+// The copy (large batches only; small ones are read zero-copy from pinned memory) and the kernels are
+// one CUDA graph, and the finish kernel writes {excess_sum, crossings} straight into pinned memory
 // (node parameters updated per launch for the batch size); the host turns them into seconds with
 // the reference's own expression.  Statistics stay device-resident: the window handle is the
 // caller's gimbal_stats_t (its E/A feed maybe_relocate's greedy on the GPU).
@@ -205,16 +206,17 @@ struct gimbal_online_s {
   unsigned int* d_hist = nullptr;
   unsigned long long* d_cross = nullptr;
   unsigned long long* d_totals = nullptr;
-  OnlineOut* d_out = nullptr;
-  OnlineOut* h_out = nullptr;  // pinned
+  OnlineOut* h_out = nullptr;      // pinned, written by online_finish_kernel through h_out_dev
+  OnlineOut* h_out_dev = nullptr;  // its device address
+  uint8_t* h_ids_dev = nullptr;    // device address of the pinned id staging (zero-copy reads)
   bool placed = false;
-  // the iteration as a graph: H2D ids -> count [+ pairs] -> finish -> D2H result; two variants
+  // the iteration as a graph: [H2D ids ->] count [+ pairs] -> finish (result into pinned memory); two variants
   // (mode 0: online_count_kernel counts E with global atomics -- small batches; mode 1: the
   // shared-memory pair tables of online_pairs_kernel -- large batches)
   struct Graph {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
-    cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_pairs = nullptr, n_finish = nullptr, n_d2h = nullptr;
+    cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_pairs = nullptr, n_finish = nullptr;
   } gr[2];
   int64_t iterations = 0;
 
@@ -228,6 +230,7 @@ struct gimbal_online_s {
     cudaFreeHost(h_ids);
     d_ids = nullptr;
     h_ids = nullptr;
+    h_ids_dev = nullptr;
     cap = 0;
   }
 };
@@ -241,7 +244,10 @@ int grow(gimbal_online_t o, int64_t n) {
   const int64_t cap = std::max<int64_t>(n, 4096);
   const size_t bytes = (size_t)cap * o->L * o->k;
   GIMBAL_CUDA_TRY(cudaMalloc(&o->d_ids, bytes));
-  GIMBAL_CUDA_TRY(cudaMallocHost(&o->h_ids, bytes));
+  GIMBAL_CUDA_TRY(cudaHostAlloc(&o->h_ids, bytes, cudaHostAllocMapped));
+  void* dev = nullptr;
+  GIMBAL_CUDA_TRY(cudaHostGetDevicePointer(&dev, o->h_ids, 0));
+  o->h_ids_dev = static_cast<uint8_t*>(dev);
   o->cap = cap;
   return GIMBAL_OK;
 }
@@ -288,7 +294,10 @@ void node_params(gimbal_online_t o, int mode, int64_t n, unsigned grid, NodeArgs
   a.with_pairs = mode == 1 ? 0 : 1;  // mode 1: online_pairs_kernel counts E and the crossings
   a.rows = pg.rows;
   a.parts = pg.parts;
-  a.ids = o->d_ids;
+  // mode 0 (small batches) reads the ids straight from the pinned staging buffer (zero-copy: no
+  // copy node); mode 1 copies them to the device first (its pair kernel reads each column once per
+  // row block)
+  a.ids = mode == 1 ? o->d_ids : o->h_ids_dev;
   a.place = o->d_place;
   a.E = o->si.dE;
   a.A = o->si.dA;
@@ -296,7 +305,7 @@ void node_params(gimbal_online_t o, int mode, int64_t n, unsigned grid, NodeArgs
   a.totals = o->d_totals;
   a.hist = o->d_hist;
   a.flags = o->si.dflags;
-  a.out = o->d_out;
+  a.out = o->h_out_dev;  // the 16-byte result straight into pinned host memory (no copy node)
   void* c[] = {(void*)&a.ids, &a.nn, &a.L, &a.ne, &a.k, &a.g, (void*)&a.place, &a.E, &a.A, &a.hist, &a.cross,
                &a.flags, &a.with_pairs};
   std::copy(c, c + 13, a.cargs);
@@ -329,27 +338,31 @@ int online_mode(const gimbal_online_s* o, int64_t n) {
   return o->L > 1 && n * (int64_t)o->k * o->k >= (int64_t)o->ne * o->ne / 4 && n >= 256 ? 1 : 0;
 }
 
-// H2D ids -> {histogram kernel, pair kernel} (mode 1) or the combined kernel (mode 0) -> finish
-// -> D2H result
+// mode 1: H2D ids -> {histogram kernel, pair kernel} -> finish; mode 0: the combined kernel reading the
+// pinned ids -> finish.  finish writes the result into pinned host memory.
 int build_graph(gimbal_online_t o, int mode, int64_t n, unsigned grid) {
   GIMBAL_CUDA_TRY(cudaFuncSetAttribute(online_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
   gimbal_online_s::Graph& x = o->gr[mode];
   GIMBAL_CUDA_TRY(cudaGraphCreate(&x.graph, 0));
-  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&x.n_h2d, x.graph, nullptr, 0, o->d_ids, o->h_ids,
-                                           (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
   NodeArgs a;
   cudaKernelNodeParams kp, pp, fp;
   node_params(o, mode, n, grid, a, kp, pp, fp);
-  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_count, x.graph, &x.n_h2d, 1, &kp));
+  const cudaGraphNode_t* first = nullptr;
+  size_t n_first = 0;
+  if (mode == 1) {
+    GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&x.n_h2d, x.graph, nullptr, 0, o->d_ids, o->h_ids,
+                                             (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
+    first = &x.n_h2d;
+    n_first = 1;
+  }
+  GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_count, x.graph, first, n_first, &kp));
   cudaGraphNode_t before_finish[2] = {x.n_count, nullptr};
   int n_before = 1;
   if (mode == 1) {
-    GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_pairs, x.graph, &x.n_h2d, 1, &pp));
+    GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_pairs, x.graph, first, n_first, &pp));
     before_finish[n_before++] = x.n_pairs;
   }
   GIMBAL_CUDA_TRY(cudaGraphAddKernelNode(&x.n_finish, x.graph, before_finish, n_before, &fp));
-  GIMBAL_CUDA_TRY(cudaGraphAddMemcpyNode1D(&x.n_d2h, x.graph, &x.n_finish, 1, o->h_out, o->d_out,
-                                           sizeof(OnlineOut), cudaMemcpyDeviceToHost));
   GIMBAL_CUDA_TRY(cudaGraphInstantiate(&x.exec, x.graph, 0));
   return GIMBAL_OK;
 }
@@ -357,8 +370,9 @@ int build_graph(gimbal_online_t o, int mode, int64_t n, unsigned grid) {
 // batch size n -> graph node parameters (copy size, kernel n and grid)
 int update_graph(gimbal_online_t o, int mode, int64_t n, unsigned grid) {
   gimbal_online_s::Graph& x = o->gr[mode];
-  GIMBAL_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(x.exec, x.n_h2d, o->d_ids, o->h_ids,
-                                                     (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
+  if (mode == 1)
+    GIMBAL_CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(x.exec, x.n_h2d, o->d_ids, o->h_ids,
+                                                       (size_t)n * o->L * o->k, cudaMemcpyHostToDevice));
   NodeArgs a;
   cudaKernelNodeParams kp, pp, fp;
   node_params(o, mode, n, grid, a, kp, pp, fp);
@@ -395,8 +409,8 @@ int gimbal_online_create(gimbal_stats_t window, gimbal_online_t* out) {
   if (cudaMalloc(&o->d_place, (size_t)o->m) != cudaSuccess ||
       cudaMalloc(&o->d_hist, (size_t)o->L * o->g * 4) != cudaSuccess ||
       cudaMalloc(&o->d_cross, 8) != cudaSuccess || cudaMalloc(&o->d_totals, (size_t)o->g * 8) != cudaSuccess ||
-      cudaMalloc(&o->d_out, sizeof(OnlineOut)) != cudaSuccess ||
-      cudaMallocHost(&o->h_out, sizeof(OnlineOut)) != cudaSuccess) {
+      cudaHostAlloc(&o->h_out, sizeof(OnlineOut), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&o->h_out_dev), o->h_out, 0) != cudaSuccess) {
     set_error("gimbal_online_create: allocation failed");
     return fail(GIMBAL_CUDA_ERROR);
   }
@@ -419,7 +433,6 @@ int gimbal_online_destroy(gimbal_online_t o) {
   cudaFree(o->d_hist);
   cudaFree(o->d_cross);
   cudaFree(o->d_totals);
-  cudaFree(o->d_out);
   cudaFreeHost(o->h_out);
   delete o;
   return GIMBAL_OK;
