@@ -122,9 +122,6 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 __device__ __forceinline__ uint64_t kdesc(uint32_t saddr) {
   uint64_t d = 0;

@@ -591,8 +591,7 @@ Lm8Plan make_lm8_plan(int L, int ne, int k, int sms, int max_smem_optin) {
     const int ng = (pairs + p.P - 1) / p.P;
     p.P = (pairs + ng - 1) / ng;
     p.n_groups = (pairs + p.P - 1) / p.P;
-  } else if (ne % 64 == 0 && ne * ne * 2 <= budget && !(GIMBAL_KNOB("GIMBAL_COUNT_PATH") &&
-                                                         std::string(GIMBAL_KNOB("GIMBAL_COUNT_PATH")) == "split")) {
+  } else if (ne % 64 == 0 && ne * ne * 2 <= budget && !knob_is(GIMBAL_KNOB("GIMBAL_COUNT_PATH"), "split")) {
     p.u15 = true;
     p.P = 1;
     p.R = ne;
@@ -698,8 +697,11 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   CUtensorMap tmap;
   if (encode_trace_map(&tmap, trace, T, plan.L, 2, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
-    static const bool u16 = !(GIMBAL_KNOB("GIMBAL_TMA_MODE") && std::string(GIMBAL_KNOB("GIMBAL_TMA_MODE")) == "u15");
-    static const int agg = GIMBAL_KNOB("GIMBAL_TMA_AGG") ? std::atoi(GIMBAL_KNOB("GIMBAL_TMA_AGG")) : 0;
+    static const bool u16 = !knob_is(GIMBAL_KNOB("GIMBAL_TMA_MODE"), "u15");
+    static const int agg = [] {
+      const char* e = GIMBAL_KNOB("GIMBAL_TMA_AGG");
+      return e ? std::atoi(e) : 0;
+    }();
     auto kern = !u16      ? count_tm_u15_tma_kernel<false>
                 : agg == 1 ? count_tm_u15_tma_kernel<true, 1>
                 : agg == 2 ? count_tm_u15_tma_kernel<true, 2>

@@ -85,6 +85,15 @@ int nccl_merge_argmin(const double* local, int64_t n_local, int64_t offset, doub
 #else
 #define GIMBAL_KNOB(name) (static_cast<const char*>(nullptr))
 #endif
+// true when knob `name` is set to exactly `value` (never in the shipped build)
+inline bool knob_is(const char* knob_value, const char* value) {
+  if (!knob_value) return false;
+  while (*knob_value && *knob_value == *value) {
+    ++knob_value;
+    ++value;
+  }
+  return *knob_value == *value;
+}
 
 inline int invalid(const std::string& msg) {
   set_error(msg);
