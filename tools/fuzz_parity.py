@@ -1,0 +1,96 @@
+#!/usr/bin/env python3
+"""Randomised parity sweep of the whole pass against the CPU oracle (not part of the test suite;
+run on a GPU box with a time budget).  Each case draws a topology (layers, experts, top-k, GPUs),
+a token count, a candidate count and pass arguments (threshold, top_e, anchor, alpha, beta), runs
+HotPath.run (graph path, eager and replayed) or HotPath.run_async, and compares counts, strong-pair
+set, greedy placement, every candidate's scores and the argmin with the oracle.
+
+  python tools/fuzz_parity.py [--seconds 600] [--seed 1]
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+import paper_2602_21626_b200 as G  # noqa: E402
+
+
+def draw(rng):
+    ne = int(rng.choice([4, 8, 8, 16, 16, 24, 32, 64, 64, 100, 128, 256]))
+    k = int(rng.integers(1, min(8, ne) + 1))
+    divisors = [d for d in (1, 2, 4, 8, 16) if ne % d == 0 and d <= ne]
+    g = int(rng.choice(divisors))
+    L = int(rng.integers(1, 60 if ne <= 64 else 20))
+    T = int(rng.choice([1, 7, 255, 1024, 4097, 20011, 70001]))
+    C = int(rng.choice([1, 2, 9, 33, 300, 1025]))
+    top_e = int(rng.choice([0, 1, 2, 4, 4, 6, 8]))
+    threshold = float(rng.choice([0.0, 0.0, 3.0, 50.0]))
+    anchor = int(rng.integers(0, g))
+    alpha, beta = float(rng.choice([1.0, 0.5, 2.0])), float(rng.choice([1.0, 0.25, 3.0]))
+    return L, ne, k, g, T, C, top_e, threshold, anchor, alpha, beta
+
+
+def one(orc, rng, case):
+    L, ne, k, g, T, C, top_e, threshold, anchor, alpha, beta = case
+    topo = G.MoeTopology(L, ne, k, g)
+    m = L * ne
+    ids = rng.integers(0, ne, size=(T, L, k), dtype=np.uint8)
+    if rng.random() < 0.3 and k > 1:  # repeated ids (counted with multiplicity)
+        step = int(rng.integers(2, 9))
+        ids[::step, :, 1] = ids[::step, :, 0]
+    trace = torch.from_numpy(ids).cuda()
+    cands = torch.from_numpy(G.shuffled_candidates(m, g, int(rng.integers(1, 1 << 30)), C)).cuda()
+    hp = G.HotPath(topo, 0, threshold=threshold, top_e=top_e, anchor_gpu=anchor, alpha=alpha, beta=beta)
+    mode = int(rng.integers(0, 3))
+    if mode == 0:
+        res = hp.run(trace, cands, graph=False)
+    elif mode == 1:
+        for _ in range(3):  # eager, recorded, replayed
+            res = hp.run(trace, cands)
+    else:
+        res = hp.run_async(trace, cands).result()
+    oA, oE, oW = orc.stats(L, ne, k, ids)
+    A, E, W = hp.stats.read()
+    assert np.array_equal(A, oA) and np.array_equal(E, oE) and np.array_equal(W, oW), "counts"
+    if L < 2:
+        M = []
+    else:
+        M = list(orc.affinity_set(L, ne, g, oE, threshold, top_e, m // g, anchor))
+    assert res.affinity.experts == M, ("strong pairs", res.affinity.experts, M)
+    greedy = orc.greedy_place(L, ne, g, oA, M, anchor)
+    assert res.greedy == list(greedy), "greedy"
+    want = cands.cpu().numpy()
+    D, cut, obj, am = orc.eval_costs(L, ne, g, oA, oE, want, alpha, beta)
+    sc = hp._out.cpu().numpy()
+    assert np.array_equal(sc[0], D) and np.array_equal(sc[1], cut) and np.array_equal(sc[2], obj), "scores"
+    assert res.argmin == am, ("argmin", res.argmin, am)
+    return mode
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=600)
+    ap.add_argument("--seed", type=int, default=1)
+    args = ap.parse_args()
+    rng = np.random.default_rng(args.seed)
+    orc = oracle.Oracle()
+    t0, n, fails = time.time(), 0, 0
+    while time.time() - t0 < args.seconds:
+        case = draw(rng)
+        try:
+            one(orc, rng, case)
+        except Exception as ex:  # report and go on
+            fails += 1
+            print("FAIL", case, repr(ex)[:300], flush=True)
+        n += 1
+    print(f"fuzz: {n} cases, {fails} failures, {time.time() - t0:.0f} s")
+
+
+if __name__ == "__main__":
+    main()
