@@ -73,23 +73,63 @@ def one(orc, rng, case):
     return mode
 
 
+def one_hook(ref, rng, case):
+    """The online hook (gimbal_online_iteration, both graph variants) against the reference's
+    per-token loop of MoeSubsystem::iteration_cost over random batch sizes and relocations."""
+    L, ne, k, g = case[:4]
+    if ne > 256:
+        return
+    topo = G.MoeTopology(L, ne, k, g)
+    window = G.RoutingStats(topo, 0)
+    hook = G.OnlineHook(window)
+    place = list(G.shuffled_candidates(L * ne, g, int(rng.integers(1, 1 << 30)), 1)[0])
+    hook.set_placement(place)
+    rh = ref.hook_create(L, ne, k, g, place)
+    try:
+        for i in range(int(rng.integers(1, 6))):
+            if rng.random() < 0.3:  # relocation: new placement, window closed and reset
+                place = list(G.shuffled_candidates(L * ne, g, int(rng.integers(1, 1 << 30)), 1)[0])
+                hook.set_placement(place)
+                ref.hook_set_placement(rh, place)
+                window.reset()
+                ref.hook_reset_window(rh)
+            n = int(rng.choice([1, 3, 64, 255, 256, 1000, 4096]))
+            ids = rng.integers(0, ne, size=(n, L, k), dtype=np.uint8)
+            if rng.random() < 0.3 and k > 1:
+                ids[::2, :, 1] = ids[::2, :, 0]
+            got = hook.iteration(ids.astype(np.int32) if rng.random() < 0.5 else ids)
+            want = ref.hook_iteration(rh, ids.astype(np.int32))
+            assert got[1] == want[1] and got[0] == want[0], ("iteration", i, got, want)
+        A, E, W = window.read()
+        rA, rE, rT = ref.hook_stats(rh, L, ne, g)
+        assert np.array_equal(A, rA.astype(np.uint64)) and np.array_equal(E, rE.astype(np.uint64)), "window stats"
+        assert np.array_equal(hook.gpu_totals(), rT), "gpu totals"
+    finally:
+        ref.hook_destroy(rh)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=600)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--what", default="pass", choices=["pass", "hook"])
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     orc = oracle.Oracle()
+    ref = oracle.Ref() if args.what == "hook" else None
     t0, n, fails = time.time(), 0, 0
     while time.time() - t0 < args.seconds:
         case = draw(rng)
         try:
-            one(orc, rng, case)
+            if args.what == "hook":
+                one_hook(ref, rng, case)
+            else:
+                one(orc, rng, case)
         except Exception as ex:  # report and go on
             fails += 1
             print("FAIL", case, repr(ex)[:300], flush=True)
         n += 1
-    print(f"fuzz: {n} cases, {fails} failures, {time.time() - t0:.0f} s")
+    print(f"fuzz {args.what}: {n} cases, {fails} failures, {time.time() - t0:.0f} s")
 
 
 if __name__ == "__main__":
