@@ -108,11 +108,44 @@ def one_hook(ref, rng, case):
         ref.hook_destroy(rh)
 
 
+def one_stream(orc, rng, case):
+    """Tumbling windows (HotPath.stream: two handles, queued per-window greedy / scores / argmin):
+    every window's greedy placement, scores, argmin and moved count against the oracle."""
+    L, ne, k, g, T, C = case[:6]
+    if L < 2 or ne > 256:
+        return
+    topo = G.MoeTopology(L, ne, k, g)
+    m = L * ne
+    calib = torch.from_numpy(rng.integers(0, ne, size=(int(rng.integers(1, 5000)), L, k), dtype=np.uint8)).cuda()
+    wins = [torch.from_numpy(rng.integers(0, ne, size=(int(rng.choice([1, 100, 4097, 20011])), L, k),
+                                          dtype=np.uint8)).cuda() for _ in range(int(rng.integers(1, 5)))]
+    cands = torch.from_numpy(G.shuffled_candidates(m, g, int(rng.integers(1, 1 << 30)), max(C, 2))).cuda()
+    hp = G.HotPath(topo, 0)
+    M = hp.calibrate(calib)
+    cA, cE, _ = orc.stats(L, ne, k, calib.cpu().numpy())
+    assert M.experts == list(orc.affinity_set(L, ne, g, cE, 0.0, 4, m // g, 0)), "calibration set"
+    out = hp.stream(wins, cands, M)
+    scores = hp._window_scores.cpu().numpy()
+    prev = None
+    for i, (w, (am, moved, gp)) in enumerate(zip(wins, out)):
+        oA, oE, _ = orc.stats(L, ne, k, w.cpu().numpy())
+        ogp = np.asarray(orc.greedy_place(L, ne, g, oA, M.experts, 0), np.int32)
+        assert np.array_equal(gp, ogp), ("window greedy", i)
+        hc = cands.cpu().numpy()
+        hc[0] = ogp.astype(np.uint8)
+        D, cut, obj, oam = orc.eval_costs(L, ne, g, oA, oE, hc)
+        assert am == oam, ("window argmin", i)
+        assert np.array_equal(scores[i][0], D) and np.array_equal(scores[i][1], cut), ("window scores", i)
+        assert np.array_equal(scores[i][2], obj), ("window objective", i)
+        assert moved == (len(ogp) if prev is None else int(np.count_nonzero(prev != ogp))), ("moved", i)
+        prev = ogp
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=600)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--what", default="pass", choices=["pass", "hook"])
+    ap.add_argument("--what", default="pass", choices=["pass", "hook", "stream"])
     args = ap.parse_args()
     rng = np.random.default_rng(args.seed)
     orc = oracle.Oracle()
@@ -123,6 +156,8 @@ def main():
         try:
             if args.what == "hook":
                 one_hook(ref, rng, case)
+            elif args.what == "stream":
+                one_stream(orc, rng, case)
             else:
                 one(orc, rng, case)
         except Exception as ex:  # report and go on
