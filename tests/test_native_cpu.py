@@ -150,3 +150,15 @@ def test_bench_entry_points_exist():
         n = bench.kernel_launches_per_step(G.MoeTopology(L, ne, k, g), 1, tokens=T)
         # Mixtral: counting + the fused small-shape pass; the others: the multi-kernel pass
         assert (n == 2) if cfg == "mixtral" else (8 <= n <= 40), (cfg, n)
+
+
+def test_c_host_builds_and_links():
+    """The plain-C host of the C ABI (tools/c_host_pass.c) is built with the library and loads it
+    (usage message without arguments; no GPU work)."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2602_21626_b200", "lib",
+                       "c_host_pass")
+    assert os.path.exists(exe)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+    assert out.returncode == 2 and "usage" in out.stderr
