@@ -130,3 +130,19 @@ def test_run_async_matches_run(G, orc, shape):
         assert p.result().argmin == want.argmin
     with pytest.raises(ValueError, match="infeasible"):
         bad.result()
+
+
+def test_run_async_on_the_handle_stream(G, orc):
+    """gimbal_pass_enqueue with the caller's stream = the handle's own stream (no joins): same answers."""
+    L, ne, k, g, C = 32, 8, 2, 8, 200
+    topo = G.MoeTopology(L, ne, k, g)
+    trace = G.generate_trace(topo, 5001, model_seed=8, stream_seed=1, device=0)
+    cands = torch.from_numpy(G.shuffled_candidates(L * ne, g, 12, C)).cuda()
+    hp = G.HotPath(topo, 0)
+    want = hp.run(trace, cands)
+    hs = torch.cuda.ExternalStream(hp.stats.device_buffers()[2], device=torch.device("cuda", 0))
+    with torch.cuda.stream(hs):
+        pend = [hp.run_async(trace, cands) for _ in range(20)]
+    for p in pend:
+        r = p.result()
+        assert r.argmin == want.argmin and r.greedy == want.greedy and r.affinity.experts == want.affinity.experts
