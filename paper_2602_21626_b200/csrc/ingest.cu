@@ -93,6 +93,7 @@ struct Lm8Params {
   int64_t chunk_tokens;
   int64_t T;       // tokens in X
   int64_t ld;      // row stride of X (tokens)
+  int sync_drain = 0;  // TMA u16 counter: drain every 32 blocks behind block barriers (AB: the old form)
 };
 
 __device__ __forceinline__ uint32_t id_of(unsigned long long w, int a) {
@@ -430,7 +431,31 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(i + kTmaStages, g + kTmaStages);
       }
-      if (U16 && (i + 1) % kDrainBlocks == 0 && i + 1 < nb) {
+      if (U16 && !prm.sync_drain) {
+        // rolling drain, no barrier: after each block a thread checks two words of one 16th of
+        // the table (every word once per 16 blocks); a half that reached 32768 gives 32768 to the
+        // u64 tensor by an atomic subtract, safe beside the other warps' increments.  Between
+        // two checks of a word its halves gain at most (16 + 3 stages of drift) x 1024 < 32768,
+        // so no half ever passes 65535
+        const int base = (int)(i & 15u) * (2 * kTmaBlock) + tid;
+#pragma unroll
+        for (int rep = 0; rep < 2; ++rep) {
+          const int w = base + rep * kTmaBlock;
+          const uint32_t v = cnt[w];
+          if (v & 0x80008000u) {
+            const int j = w / wpr;
+            const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+            if (v & 0x8000u) {
+              atomicSub(cnt + w, 0x8000u);
+              atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
+            }
+            if (v & 0x80000000u) {
+              atomicSub(cnt + w, 0x80000000u);
+              atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
+            }
+          }
+        }
+      } else if (U16 && (i + 1) % kDrainBlocks == 0 && i + 1 < nb) {
         __syncthreads();
         for (int w = tid; w < ne * wpr; w += kTmaBlock) {
           const uint32_t v = cnt[w];
@@ -698,6 +723,7 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   if (encode_trace_map(&tmap, trace, T, plan.L, 2, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
     static const bool u16 = !knob_is(GIMBAL_KNOB("GIMBAL_TMA_MODE"), "u15");
+    prm.sync_drain = GIMBAL_KNOB("GIMBAL_U15_SYNC_DRAIN") ? 1 : 0;
     static const int agg = [] {
       const char* e = GIMBAL_KNOB("GIMBAL_TMA_AGG");
       return e ? std::atoi(e) : 0;
