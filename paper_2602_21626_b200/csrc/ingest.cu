@@ -309,11 +309,13 @@ constexpr int kU15Bytes = 256 * 128 * 4;
 
 constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tokens
 
-// U16 = full 16-bit halves, increments without return values, and a drain every kDrainBlocks
-// blocks: a token whose ids are distinct within each layer adds at most 1 to any cell, so after
-// a drain leaves every half below 32768 the next 32768 tokens cannot carry out of a half.  Tokens
-// with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor instead.
-// Without the return-value dependency a warp issues its 64 increments back to back.
+// U16 = full 16-bit halves, increments without return values, and a rolling drain (each thread
+// checks one table word after every block, so every word is checked once per 32 blocks): a token
+// whose ids are distinct within each layer adds at most 1 to any cell, so a half drained below
+// 16384 cannot carry out within the next 35 blocks (32 + the 3-stage drift between warps).
+// Tokens with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor
+// instead.  Without the return-value dependency a warp issues its 64 increments back to back.
+// (AB knob GIMBAL_U15_SYNC_DRAIN: the earlier block-wide drain every kDrainBlocks blocks.)
 // !U16 = guarded 15-bit halves with per-increment overflow detection (u15_count_token).
 // AGG (issue-order experiments, U16 only; the AB build selects them with GIMBAL_TMA_AGG):
 //   0 = slot order as drawn (default);
@@ -432,27 +434,24 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
         issue(i + kTmaStages, g + kTmaStages);
       }
       if (U16 && !prm.sync_drain) {
-        // rolling drain, no barrier: after each block a thread checks two words of one 16th of
-        // the table (every word once per 16 blocks); a half that reached 32768 gives 32768 to the
-        // u64 tensor by an atomic subtract, safe beside the other warps' increments.  Between
-        // two checks of a word its halves gain at most (16 + 3 stages of drift) x 1024 < 32768,
-        // so no half ever passes 65535
-        const int base = (int)(i & 15u) * (2 * kTmaBlock) + tid;
-#pragma unroll
-        for (int rep = 0; rep < 2; ++rep) {
-          const int w = base + rep * kTmaBlock;
-          const uint32_t v = cnt[w];
-          if (v & 0x80008000u) {
-            const int j = w / wpr;
-            const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
-            if (v & 0x8000u) {
-              atomicSub(cnt + w, 0x8000u);
-              atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
-            }
-            if (v & 0x80000000u) {
-              atomicSub(cnt + w, 0x80000000u);
-              atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
-            }
+        // rolling drain, no barrier: after each 1024-token block a thread checks one word of one
+        // 32nd of the table (every word once per 32 blocks) and moves a half's top two bits
+        // (>= 16384) to the u64 tensor by an atomic subtract, safe beside the other warps'
+        // increments.  Between two checks a half gains at most (32 + 3 stages of drift) x 1024
+        // = 35840 from at most 16383, so it never passes 65535
+        const int w = (int)(i & 31u) * kTmaBlock + tid;
+        const uint32_t v = cnt[w];
+        if (v & 0xc000c000u) {
+          const int j = w / wpr;
+          const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+          const uint32_t lo = v & 0xc000u, hi = v & 0xc0000000u;
+          if (lo) {
+            atomicSub(cnt + w, lo);
+            atomicAdd(El + (int64_t)j * ne + k0, (unsigned long long)lo);
+          }
+          if (hi) {
+            atomicSub(cnt + w, hi);
+            atomicAdd(El + (int64_t)j * ne + k0 + 1, (unsigned long long)(hi >> 16));
           }
         }
       } else if (U16 && (i + 1) % kDrainBlocks == 0 && i + 1 < nb) {
