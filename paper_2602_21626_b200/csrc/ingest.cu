@@ -94,6 +94,8 @@ struct Lm8Params {
   int64_t T;       // tokens in X
   int64_t ld;      // row stride of X (tokens)
   int sync_drain = 0;  // TMA u16 counter: drain every 32 blocks behind block barriers (AB: the old form)
+  int drain_blocks = 32; // TMA u16 counter, block-wide drain: blocks between drains (<= 32)
+  int roll_sync = 0;   // TMA u16 counter, rolling drain: a block barrier every roll_sync blocks (AB)
 };
 
 __device__ __forceinline__ uint32_t id_of(unsigned long long w, int a) {
@@ -308,6 +310,13 @@ constexpr int kTmaCols = 4;      // u64 words per token in a stage (two 2-layer 
 constexpr int kU15Bytes = 256 * 128 * 4;
 
 constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tokens
+#ifdef GIMBAL_AB_KNOBS
+#define U15_ROLL_SYNC prm.roll_sync
+#define U15_DRAIN_BLOCKS prm.drain_blocks
+#else
+#define U15_ROLL_SYNC 0
+#define U15_DRAIN_BLOCKS kDrainBlocks
+#endif
 
 // U16 = full 16-bit halves, increments without return values, and a rolling drain (each thread
 // checks one table word after every block, so every word is checked once per 32 blocks): a token
@@ -316,6 +325,12 @@ constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tok
 // Tokens with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor
 // instead.  Without the return-value dependency a warp issues its 64 increments back to back.
 // (AB knob GIMBAL_U15_SYNC_DRAIN: the earlier block-wide drain every kDrainBlocks blocks.)
+// DRAM traffic: the 57 CTAs counting the pairs of one chunk read the same rows, and L2 serves the
+// later ones only while they stay within ~100 blocks of each other.  The block-wide drain's pauses
+// keep them close (53-73 GB per 64 Mi tokens); without them per-pair speed differences let them
+// drift apart (190-215 GB), yet the rolling drain is faster (103.1 vs 103.7-103.9 ms): DRAM runs
+// at 2 TB/s, far from binding, and re-aligning (a barrier every 8 blocks: 57 GB) costs 4 %.
+// profiles/r2c_dsv3_drain_traffic.md has the A/B.
 // !U16 = guarded 15-bit halves with per-increment overflow detection (u15_count_token).
 // AGG (issue-order experiments, U16 only; the AB build selects them with GIMBAL_TMA_AGG):
 //   0 = slot order as drawn (default);
@@ -454,16 +469,25 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
             atomicAdd(El + (int64_t)j * ne + k0 + 1, (unsigned long long)(hi >> 16));
           }
         }
-      } else if (U16 && (i + 1) % kDrainBlocks == 0 && i + 1 < nb) {
+        if (U15_ROLL_SYNC && (i + 1) % (uint32_t)U15_ROLL_SYNC == 0) __syncthreads();
+      } else if (U16 && (i + 1) % (uint32_t)U15_DRAIN_BLOCKS == 0 && i + 1 < nb) {
         __syncthreads();
-        for (int w = tid; w < ne * wpr; w += kTmaBlock) {
-          const uint32_t v = cnt[w];
-          if (v & 0x80008000u) {
-            const int j = w / wpr;
-            const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
-            if (v & 0x8000u) atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
-            if (v & 0x80000000u) atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
-            cnt[w] = v & 0x7fff7fffu;
+        for (int w4 = tid; w4 < ne * wpr / 4; w4 += kTmaBlock) {  // four words per 16-byte load
+          const uint4 q = reinterpret_cast<const uint4*>(cnt)[w4];
+          if ((q.x | q.y | q.z | q.w) & 0x80008000u) {
+            const uint32_t vs[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t v = vs[c];
+              if (v & 0x80008000u) {
+                const int w = 4 * w4 + c;
+                const int j = w / wpr;
+                const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+                if (v & 0x8000u) atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
+                if (v & 0x80000000u) atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
+                cnt[w] = v & 0x7fff7fffu;
+              }
+            }
           }
         }
         __syncthreads();
@@ -723,6 +747,8 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
     static const bool u16 = !knob_is(GIMBAL_KNOB("GIMBAL_TMA_MODE"), "u15");
     prm.sync_drain = GIMBAL_KNOB("GIMBAL_U15_SYNC_DRAIN") ? 1 : 0;
+    if (const char* e = GIMBAL_KNOB("GIMBAL_U15_DRAIN_BLOCKS")) prm.drain_blocks = std::min(32, std::max(1, std::atoi(e)));
+    if (const char* e = GIMBAL_KNOB("GIMBAL_U15_ROLL_SYNC")) prm.roll_sync = std::max(0, std::atoi(e));
     static const int agg = [] {
       const char* e = GIMBAL_KNOB("GIMBAL_TMA_AGG");
       return e ? std::atoi(e) : 0;
