@@ -93,8 +93,9 @@ struct Lm8Params {
   int64_t chunk_tokens;
   int64_t T;       // tokens in X
   int64_t ld;      // row stride of X (tokens)
-  int sync_drain = 0;  // TMA u16 counter: drain every 32 blocks behind block barriers (AB: the old form)
+  int rolling = 0;     // TMA u16 counter: rolling drain without barriers (AB)
   int drain_blocks = 32; // TMA u16 counter, block-wide drain: blocks between drains (<= 32)
+  int scalar_scan = 0;  // TMA u16 counter, block-wide drain: scan one word per load (AB)
   int roll_sync = 0;   // TMA u16 counter, rolling drain: a block barrier every roll_sync blocks (AB)
 };
 
@@ -313,24 +314,30 @@ constexpr int kDrainBlocks = 32;  // u16 mode: drain every 32 x 1024 = 32768 tok
 #ifdef GIMBAL_AB_KNOBS
 #define U15_ROLL_SYNC prm.roll_sync
 #define U15_DRAIN_BLOCKS prm.drain_blocks
+#define U15_SCALAR_SCAN prm.scalar_scan
+#define U15_ROLLING prm.rolling
 #else
+#define U15_ROLLING 0
+#define U15_SCALAR_SCAN 0
 #define U15_ROLL_SYNC 0
 #define U15_DRAIN_BLOCKS kDrainBlocks
 #endif
 
-// U16 = full 16-bit halves, increments without return values, and a rolling drain (each thread
-// checks one table word after every block, so every word is checked once per 32 blocks): a token
-// whose ids are distinct within each layer adds at most 1 to any cell, so a half drained below
-// 16384 cannot carry out within the next 35 blocks (32 + the 3-stage drift between warps).
-// Tokens with a repeated id (multiplicity up to 64 per cell) add straight to the u64 tensor
-// instead.  Without the return-value dependency a warp issues its 64 increments back to back.
-// (AB knob GIMBAL_U15_SYNC_DRAIN: the earlier block-wide drain every kDrainBlocks blocks.)
-// DRAM traffic: the 57 CTAs counting the pairs of one chunk read the same rows, and L2 serves the
-// later ones only while they stay within ~100 blocks of each other.  The block-wide drain's pauses
-// keep them close (53-73 GB per 64 Mi tokens); without them per-pair speed differences let them
-// drift apart (190-215 GB), yet the rolling drain is faster (103.1 vs 103.7-103.9 ms): DRAM runs
-// at 2 TB/s, far from binding, and re-aligning (a barrier every 8 blocks: 57 GB) costs 4 %.
-// profiles/r2c_dsv3_drain_traffic.md has the A/B.
+// U16 = full 16-bit halves and increments without return values (a warp issues its 64 increments
+// back to back), drained block-wide every 32 blocks: between two drains a token whose ids are
+// distinct within each layer adds at most 1 to any cell, so a half below 32768 stays below 65536.
+// The drain scans the table with 16-byte loads behind two block barriers and moves bit 15 of each
+// half to the u64 tensor.  Tokens with a repeated id (multiplicity up to 64 per cell) add straight
+// to the u64 tensor instead.
+// AB knob GIMBAL_U15_ROLLING: a rolling drain with no barrier (each thread checks one table word
+// after every block, every word once per 32 blocks, and moves a half's top two bits (>= 16384) out
+// by an atomic subtract; 35 blocks of growth from below 16384 cannot pass 65535).  It is 0.5 %
+// faster (103.1-103.3 vs 103.7-103.9 ms per 64 Mi DS-V3 tokens) but reads 3x the DRAM bytes
+// (190-215 vs 68-73 GB; 31 GB algorithmic): the 57 CTAs counting the pairs of one chunk read the
+// same rows, L2 serves the later ones only while they stay close, and the drain pauses keep them
+// close (a barrier alone every 32 blocks does not; every 8 blocks does, at 4 % time).  The pass
+// runs beside the serving engine that produces the trace, so HBM bandwidth left to it matters more
+// than 0.5 %: the block-wide drain ships.  profiles/r2c_dsv3_drain_traffic.md has the A/B.
 // !U16 = guarded 15-bit halves with per-increment overflow detection (u15_count_token).
 // AGG (issue-order experiments, U16 only; the AB build selects them with GIMBAL_TMA_AGG):
 //   0 = slot order as drawn (default);
@@ -448,9 +455,9 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(i + kTmaStages, g + kTmaStages);
       }
-      if (U16 && !prm.sync_drain) {
-        // rolling drain, no barrier: after each 1024-token block a thread checks one word of one
-        // 32nd of the table (every word once per 32 blocks) and moves a half's top two bits
+      if (U16 && U15_ROLLING) {
+        // (AB) rolling drain, no barrier: after each 1024-token block a thread checks one word of
+        // one 32nd of the table (every word once per 32 blocks) and moves a half's top two bits
         // (>= 16384) to the u64 tensor by an atomic subtract, safe beside the other warps'
         // increments.  Between two checks a half gains at most (32 + 3 stages of drift) x 1024
         // = 35840 from at most 16383, so it never passes 65535
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
         if (U15_ROLL_SYNC && (i + 1) % (uint32_t)U15_ROLL_SYNC == 0) __syncthreads();
       } else if (U16 && (i + 1) % (uint32_t)U15_DRAIN_BLOCKS == 0 && i + 1 < nb) {
         __syncthreads();
-        for (int w4 = tid; w4 < ne * wpr / 4; w4 += kTmaBlock) {  // four words per 16-byte load
+        for (int w4 = tid; w4 < (U15_SCALAR_SCAN ? 0 : ne * wpr / 4); w4 += kTmaBlock) {  // 16-byte loads
           const uint4 q = reinterpret_cast<const uint4*>(cnt)[w4];
           if ((q.x | q.y | q.z | q.w) & 0x80008000u) {
             const uint32_t vs[4] = {q.x, q.y, q.z, q.w};
@@ -488,6 +495,16 @@ __global__ void __launch_bounds__(kTmaBlock, 1)
                 cnt[w] = v & 0x7fff7fffu;
               }
             }
+          }
+        }
+        for (int w = tid; w < (U15_SCALAR_SCAN ? ne * wpr : 0); w += kTmaBlock) {  // AB: one word per load
+          const uint32_t v = cnt[w];
+          if (v & 0x80008000u) {
+            const int j = w / wpr;
+            const int k0 = 2 * ((w - j * wpr) ^ (j & 31));
+            if (v & 0x8000u) atomicAdd(El + (int64_t)j * ne + k0, 32768ull);
+            if (v & 0x80000000u) atomicAdd(El + (int64_t)j * ne + k0 + 1, 32768ull);
+            cnt[w] = v & 0x7fff7fffu;
           }
         }
         __syncthreads();
@@ -746,8 +763,9 @@ cudaError_t launch_count_direct_u15(const Lm8Plan& plan, const uint8_t* trace, i
   if (encode_trace_map(&tmap, trace, T, plan.L, 2, kTmaBox)) {
     const size_t smem = (size_t)kU15Bytes + (size_t)kTmaStages * kTmaBlock * kTmaCols * 8;
     static const bool u16 = !knob_is(GIMBAL_KNOB("GIMBAL_TMA_MODE"), "u15");
-    prm.sync_drain = GIMBAL_KNOB("GIMBAL_U15_SYNC_DRAIN") ? 1 : 0;
+    prm.rolling = GIMBAL_KNOB("GIMBAL_U15_ROLLING") ? 1 : 0;
     if (const char* e = GIMBAL_KNOB("GIMBAL_U15_DRAIN_BLOCKS")) prm.drain_blocks = std::min(32, std::max(1, std::atoi(e)));
+    prm.scalar_scan = GIMBAL_KNOB("GIMBAL_U15_SCALAR_SCAN") ? 1 : 0;
     if (const char* e = GIMBAL_KNOB("GIMBAL_U15_ROLL_SYNC")) prm.roll_sync = std::max(0, std::atoi(e));
     static const int agg = [] {
       const char* e = GIMBAL_KNOB("GIMBAL_TMA_AGG");

@@ -57,9 +57,10 @@ def test_unfused_pass_for_small_shapes(L, ne, k, g, C):
 
 @pytest.mark.parametrize("knobs,L,ne,k,T", [
     ({"GIMBAL_TMA_MODE": "u15"}, 58, 256, 8, 70001),
-    ({"GIMBAL_U15_SYNC_DRAIN": "1"}, 58, 256, 8, 70001),
-    ({"GIMBAL_U15_SYNC_DRAIN": "1", "GIMBAL_U15_DRAIN_BLOCKS": "16"}, 58, 256, 8, 300001),
-    ({"GIMBAL_U15_ROLL_SYNC": "8"}, 58, 256, 8, 300001),
+    ({"GIMBAL_U15_ROLLING": "1"}, 58, 256, 8, 300001),
+    ({"GIMBAL_U15_ROLLING": "1", "GIMBAL_U15_ROLL_SYNC": "8"}, 58, 256, 8, 300001),
+    ({"GIMBAL_U15_DRAIN_BLOCKS": "16"}, 58, 256, 8, 300001),
+    ({"GIMBAL_U15_SCALAR_SCAN": "1"}, 58, 256, 8, 300001),
     ({"GIMBAL_NO_TMA": "1"}, 58, 256, 8, 70001),
     ({"GIMBAL_COUNT_PATH": "split"}, 58, 256, 8, 30001),
     ({"GIMBAL_COUNT_PATH": "atomic"}, 48, 128, 8, 30001),
