@@ -270,6 +270,15 @@ int gimbal_online_gpu_totals(gimbal_online_t o, int64_t* out);
 int gimbal_eval_cost_dense(int32_t rows, int32_t m, const double* A, const double* W, int32_t g,
                            double alpha, double beta, const int32_t* assign, double* deviation,
                            double* cut, double* objective);
+/* exact_solve (placement.cpp:87-184, placement.hpp:49-51): the objective-minimal balanced placement
+ * of m <= 16 experts on g <= 4 GPUs, the lexicographically least (labels in first-use order) among
+ * ties, as the reference's branch and bound returns it; every placement is scored on the GPU.  The
+ * assignment (m int32) and eval_cost of it go to host memory.  A / W must be non-negative,
+ * integer-valued doubles below 2^40 (else GIMBAL_NOT_SUPPORTED); too large an instance returns
+ * GIMBAL_INVALID_ARGUMENT with the reference's message.  Replaces: placement::exact_solve. */
+int gimbal_exact_solve_dense(int32_t rows, int32_t m, const double* A, const double* W, int32_t g,
+                             double alpha, double beta, int32_t* assign_out, double* deviation,
+                             double* cut, double* objective);
 /* build_affinity_set from an explicit double tensor E [(n_blocks)][n_e][n_e] (host). */
 int gimbal_affinity_set_dense(const gimbal_topology* topo, const double* E, int32_t n_blocks,
                               double threshold, int32_t top_e, int32_t capacity,

@@ -220,6 +220,8 @@ class Ref:
         L.ref_comm_cost.argtypes = [C.c_int] * 4 + [C.c_void_p, C.c_int, _i64, _i32p, C.c_int, _i64p]
         L.ref_eval_cost.argtypes = [C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_double, C.c_double, _i32p,
                                     C.c_int, _dp, _dp, _dp]
+        L.ref_exact_solve.argtypes = [C.c_int, C.c_int, _f64p, _f64p, C.c_int, C.c_double, C.c_double, _i32p,
+                                      _dp, _dp, _dp]
         L.ref_build_affinity_set.argtypes = [C.c_int] * 4 + [_f64p, C.c_int, C.c_double, C.c_int, C.c_int,
                                                               C.c_int, _i32p, C.POINTER(C.c_int)]
         L.ref_greedy_place.argtypes = [C.c_int, C.c_int, _f64p, _i32p, C.c_int, C.c_int, C.c_int, _i32p]
@@ -284,6 +286,16 @@ class Ref:
         self._ok(self.lib.ref_eval_cost(A.shape[0], A.shape[1], A, W, g, alpha, beta, a, a.size, C.byref(D),
                                         C.byref(c), C.byref(o)))
         return D.value, c.value, o.value
+
+    def exact_solve(self, A, W, g, alpha=1.0, beta=1.0):
+        """placement::exact_solve -> (assign, (D, cut, objective))."""
+        A = np.ascontiguousarray(np.atleast_2d(A), np.float64)
+        W = np.ascontiguousarray(W, np.float64)
+        a = np.zeros(A.shape[1], np.int32)
+        D, c, o = C.c_double(), C.c_double(), C.c_double()
+        self._ok(self.lib.ref_exact_solve(A.shape[0], A.shape[1], A, W, g, alpha, beta, a, C.byref(D), C.byref(c),
+                                          C.byref(o)))
+        return a, (D.value, c.value, o.value)
 
     def build_affinity_set(self, L, ne, k, g, E, threshold=0.0, top_e=4, capacity=None, anchor=0):
         E = np.ascontiguousarray(E, np.float64).ravel()

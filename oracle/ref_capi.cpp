@@ -141,6 +141,24 @@ int ref_eval_cost(int rows, int m, const double* A, const double* W, int g, doub
   });
 }
 
+// exact_solve (placement.cpp:87-184): the reference's branch and bound, assignment + its cost.
+int ref_exact_solve(int rows, int m, const double* A, const double* W, int g, double alpha, double beta,
+                    std::int32_t* assign, double* D, double* cut, double* obj) {
+  return guarded([&] {
+    placement::PlacementProblem p;
+    p.A = from_rowmajor(A, rows, m);
+    p.W = from_rowmajor(W, m, m);
+    p.g = g;
+    p.alpha = alpha;
+    p.beta = beta;
+    auto [pl, c] = placement::exact_solve(p);
+    for (int j = 0; j < m; ++j) assign[j] = pl.assign[static_cast<std::size_t>(j)];
+    *D = c.deviation;
+    *cut = c.cut;
+    *obj = c.objective;
+  });
+}
+
 // build_affinity_set (placement.cpp:186-238) from E [(L-1)][ne][ne].
 int ref_build_affinity_set(int L, int ne, int k, int g, const double* E, int n_blocks,
                            double threshold, int top_e, int capacity, int anchor,

@@ -8,7 +8,7 @@ from . import _native
 from .moe import (AffinityTensor, MoeTopology, RoutedStream, RoutingParams, RoutingStats, comm_cost,
                   generate_trace, generator_tables, record_stats)
 from .placement import (AffinitySet, Placement, PlacementCost, PlacementProblem, Relocation, build_affinity_set,
-                        eval_cost, eval_costs, eval_excess, greedy_place, maybe_relocate, shuffled_candidates, static_placement)
+                        eval_cost, eval_costs, eval_excess, exact_solve, greedy_place, maybe_relocate, shuffled_candidates, static_placement)
 from .pipeline import HotPath
 from .hook import OnlineHook
 

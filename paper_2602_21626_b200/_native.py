@@ -76,6 +76,8 @@ SIGNATURES = [
     ("gimbal_online_set_placement", C.c_int, [_P, _P, _i64]),
     ("gimbal_online_iteration", C.c_int, [_P, _P, C.c_int, _i64, C.POINTER(_d), C.POINTER(_i64)]),
     ("gimbal_online_gpu_totals", C.c_int, [_P, _P]),
+    ("gimbal_exact_solve_dense", C.c_int, [_i32, _i32, _P, _P, _i32, _d, _d, _P, C.POINTER(_d), C.POINTER(_d),
+                                           C.POINTER(_d)]),
     ("gimbal_eval_cost_dense", C.c_int, [_i32, _i32, _P, _P, _i32, _d, _d, _P, C.POINTER(_d), C.POINTER(_d),
                                          C.POINTER(_d)]),
     ("gimbal_affinity_set_dense", C.c_int, [_TP, _P, _i32, _d, _i32, _i32, _i32, _P, C.POINTER(_i32)]),

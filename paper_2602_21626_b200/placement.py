@@ -86,6 +86,23 @@ def eval_cost(problem: PlacementProblem, placement: Placement) -> PlacementCost:
     return PlacementCost(D.value, c.value, o.value)
 
 
+def exact_solve(problem: PlacementProblem):  # placement.cpp:87-184
+    """placement::exact_solve: (Placement, PlacementCost) of the objective-minimal balanced placement
+    (m <= 16 experts, g <= 4 GPUs; the lexicographically least among ties), every placement scored
+    on the GPU.  A / W must be non-negative integer-valued (counts)."""
+    A = np.ascontiguousarray(np.atleast_2d(np.asarray(problem.A, np.float64)))
+    W = np.ascontiguousarray(np.asarray(problem.W, np.float64))
+    m = A.shape[1]
+    if W.shape != (m, m) and m >= 1 and problem.g >= 1 and m % problem.g == 0:
+        raise ValueError("PlacementProblem: W must be experts x experts")
+    a = np.zeros(max(m, 1), np.int32)
+    D, c, o = C.c_double(), C.c_double(), C.c_double()
+    N.check(N.lib().gimbal_exact_solve_dense(A.shape[0], m, A.ctypes.data, W.ctypes.data, problem.g, problem.alpha,
+                                             problem.beta, a.ctypes.data, C.byref(D), C.byref(c), C.byref(o)),
+            "exact_solve")
+    return Placement([int(x) for x in a[:m]]), PlacementCost(D.value, c.value, o.value)
+
+
 def eval_costs(stats: RoutingStats, candidates, alpha: float = 1.0, beta: float = 1.0, out=None):
     """Batch eval_cost of candidates [C][m] uint8 against the stats' flat A / W.
 

@@ -49,64 +49,21 @@ PlacementCost eval_cost(const PlacementProblem& problem, const Placement& placem
   return cost;
 }
 
-// Branch and bound over balanced partitions, GPU labels in first-use order so the first optimum
-// met is the lexicographically smallest; prune on lower bound >= incumbent (placement.cpp:87-184
-// semantics).  Host-only: it is the m <= 16 verification oracle, not part of the hot path.
+// Every balanced placement scored on the GPU (gimbal_exact_solve_dense, csrc/exact.cu): the
+// objective-minimal one, lexicographically least among ties -- what placement.cpp:87-184's branch
+// and bound returns -- and its eval_cost.
 std::pair<Placement, PlacementCost> exact_solve(const PlacementProblem& problem) {
   problem.validate();
-  if (problem.experts() > kExactMaxExperts || problem.g > kExactMaxGpus) {
-    throw std::invalid_argument("exact_solve: instance too large (max " + std::to_string(kExactMaxExperts) +
-                                " experts on " + std::to_string(kExactMaxGpus) + " GPUs); use greedy_place");
-  }
-  const int m = problem.experts(), g = problem.g, cap = m / g;
-  const Eigen::Index rows = problem.A.rows();
-  std::vector<double> ideal(static_cast<std::size_t>(rows));
-  for (Eigen::Index i = 0; i < rows; ++i) ideal[static_cast<std::size_t>(i)] = problem.A.row(i).sum() / g;
-  Eigen::MatrixXd load = Eigen::MatrixXd::Zero(rows, g);
-  std::vector<int> used(static_cast<std::size_t>(g), 0), cur(static_cast<std::size_t>(m), -1), best;
-  double best_obj = std::numeric_limits<double>::infinity(), cut = 0.0;
-  auto pw = [&](int j, int k) { return problem.W(j, k) + problem.W(k, j); };
-  auto bound = [&] {
-    double d = 0.0;  // overflow above ideal is permanent; shortfall only binds on full GPUs
-    for (Eigen::Index i = 0; i < rows; ++i)
-      for (int p = 0; p < g; ++p) {
-        d = std::max(d, load(i, p) - ideal[static_cast<std::size_t>(i)]);
-        if (used[static_cast<std::size_t>(p)] == cap) d = std::max(d, ideal[static_cast<std::size_t>(i)] - load(i, p));
-      }
-    return d;
-  };
-  auto rec = [&](auto&& self, int j, int labels) -> void {
-    if (problem.alpha * bound() + problem.beta * cut >= best_obj) return;
-    if (j == m) {
-      double d = 0.0;
-      for (Eigen::Index i = 0; i < rows; ++i)
-        for (int p = 0; p < g; ++p) d = std::max(d, std::abs(load(i, p) - ideal[static_cast<std::size_t>(i)]));
-      const double obj = problem.alpha * d + problem.beta * cut;
-      if (obj < best_obj) {
-        best_obj = obj;
-        best = cur;
-      }
-      return;
-    }
-    for (int p = 0; p <= std::min(g - 1, labels); ++p) {
-      if (used[static_cast<std::size_t>(p)] == cap) continue;
-      double add = 0.0;
-      for (int k = 0; k < j; ++k)
-        if (cur[static_cast<std::size_t>(k)] != p) add += pw(k, j);
-      cur[static_cast<std::size_t>(j)] = p;
-      used[static_cast<std::size_t>(p)] += 1;
-      load.col(p) += problem.A.col(j);
-      cut += add;
-      self(self, j + 1, std::max(labels, p + 1));
-      cut -= add;
-      load.col(p) -= problem.A.col(j);
-      used[static_cast<std::size_t>(p)] -= 1;
-      cur[static_cast<std::size_t>(j)] = -1;
-    }
-  };
-  rec(rec, 0, 0);
-  Placement pl{std::move(best)};
-  return {pl, eval_cost(problem, pl)};
+  const int m = problem.experts();
+  const auto A = rowmajor(problem.A);
+  const auto W = rowmajor(problem.W);
+  std::vector<std::int32_t> a(static_cast<std::size_t>(std::max(m, 1)));
+  PlacementCost cost;
+  check(gimbal_exact_solve_dense(static_cast<std::int32_t>(problem.A.rows()), m, A.data(), W.data(), problem.g,
+                                 problem.alpha, problem.beta, a.data(), &cost.deviation, &cost.cut, &cost.objective),
+        "exact_solve");
+  Placement pl{std::vector<int>(a.begin(), a.begin() + m)};
+  return {pl, cost};
 }
 
 AffinitySet build_affinity_set(const moe::AffinityTensor& affinity, const moe::MoeTopology& topo, double threshold,
