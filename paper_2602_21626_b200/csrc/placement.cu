@@ -306,6 +306,120 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---- deviation + feasibility: one CTA per candidate, one warp per layer at a time ----
+// Lane-private bins (g <= G <= 8): every lane adds its experts' activations into its own G bins in
+// shared memory, laid out [GPU][lane] so a warp's accesses fall on its lanes' banks whatever GPU ids
+// the lanes hold (no atomics, no bank conflicts); per-GPU counts ride in registers as 4-bit fields.
+// The warp then sums each GPU's 32 bins with a reduce-scatter of shuffles.  Integer sums: the same
+// loads as any order.
+template <int G>
+__global__ void __launch_bounds__(256)
+    eval_dev_bins_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
+                         const uint8_t* __restrict__ cands, int64_t m, double* __restrict__ D,
+                         uint32_t* __restrict__ flags, long long* __restrict__ bad_index, int64_t base) {
+  constexpr int kWarps = 8;
+  __shared__ unsigned long long bins[kWarps][G][32];
+  __shared__ uint32_t ctot[G];
+  __shared__ double dmax[kWarps];
+  __shared__ int bad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t c = blockIdx.x;
+  const uint8_t* P = cands + c * m;
+  if (threadIdx.x < G) ctot[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) bad = 0;
+#pragma unroll
+  for (int p = 0; p < G; ++p) bins[warp][p][lane] = 0ull;
+  __syncthreads();
+  double dev = 0.0;
+  uint32_t cnt_lo = 0u, cnt_hi = 0u;  // per-GPU expert counts, 8-bit fields (GPUs 0-3, 4-7)
+  bool my_bad = false;
+  for (int l = warp; l < L; l += kWarps) {
+    // n_e <= 256 (uint8 ids): at most 8 experts per lane, all loaded before the bin updates
+    unsigned long long av[8];
+    uint32_t pv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      av[i] = e < ne ? A[(int64_t)l * ne + e] : 0ull;
+      pv[i] = e < ne ? (uint32_t)P[(int64_t)l * ne + e] : 0xffffffffu;
+    }
+    unsigned long long rowsum = 0;
+    uint32_t nib = 0u;  // this layer's counts, 4-bit fields (<= 8 experts per lane)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (lane + 32 * i >= ne) break;
+      rowsum += av[i];
+      if (pv[i] >= (uint32_t)g) {
+        my_bad = true;
+        continue;
+      }
+      bins[warp][pv[i]][lane] += av[i];
+      nib += 1u << (4 * pv[i]);
+    }
+    cnt_lo += nib & 0x0f0f0f0fu;
+    cnt_hi += (nib >> 4) & 0x0f0f0f0fu;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rowsum += __shfl_xor_sync(0xffffffffu, rowsum, o);
+    // read back (and clear) this lane's bins, then sum each GPU over the 32 lanes
+    unsigned long long v[G];
+#pragma unroll
+    for (int p = 0; p < G; ++p) {
+      v[p] = bins[warp][p][lane];
+      bins[warp][p][lane] = 0ull;
+    }
+    // reduce-scatter: after the halving steps lane keeps GPU (lane % G)'s partial sum
+#pragma unroll
+    for (int h = G / 2; h >= 1; h >>= 1) {
+      const bool upper = (lane & h) != 0;
+#pragma unroll
+      for (int p = 0; p < h; ++p) {
+        const unsigned long long send = upper ? v[p] : v[p + h];
+        const unsigned long long keep = upper ? v[p + h] : v[p];
+        v[p] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+      }
+    }
+    unsigned long long load = v[0];
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) load += __shfl_xor_sync(0xffffffffu, load, o);
+    // ideal_l = A.row(l).sum() / g (placement.cpp:68); integer rowsum < 2^53 is exact in fp64
+    if (lane < g && lane < G) {
+      const double ideal = __ddiv_rn((double)rowsum, (double)g);
+      dev = fmax(dev, fabs(__dsub_rn((double)load, ideal)));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if (lane == 0) dmax[warp] = dev;
+  // counts: widen the 8-bit fields (<= 31 layers x 8 per lane: L <= 248) to 16 bits, sum the warp
+  uint32_t c16[4] = {cnt_lo & 0x00ff00ffu, (cnt_lo >> 8) & 0x00ff00ffu, cnt_hi & 0x00ff00ffu, (cnt_hi >> 8) & 0x00ff00ffu};
+#pragma unroll
+  for (int w = 0; w < 4; ++w)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c16[w] += __shfl_xor_sync(0xffffffffu, c16[w], o);
+  if (lane == 0) {
+    // 16-bit fields (low, high): c16[0] GPUs 0, 4; c16[1] 2, 6; c16[2] 1, 5; c16[3] 3, 7
+#pragma unroll
+    for (int p = 0; p < G; ++p) {
+      const uint32_t word = c16[(p & 1) * 2 + ((p >> 1) & 1)];
+      atomicAdd(&ctot[p], (word >> (16 * ((p >> 2) & 1))) & 0xffffu);
+    }
+  }
+  if (__any_sync(0xffffffffu, my_bad) && lane == 0) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double d = 0.0;
+    for (int w = 0; w < kWarps; ++w) d = fmax(d, dmax[w]);
+    D[c] = d;
+    const uint32_t cap = (uint32_t)(m / g);
+    int infeasible = bad;
+    for (int p = 0; p < g; ++p)
+      if (ctot[p] != cap) infeasible = 1;
+    if (infeasible) {
+      atomicOr(flags, (uint32_t)kFlagInfeasible);
+      atomicMin(bad_index, (long long)(base + c));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256)
     eval_dev_kernel(int L, int ne, int g, const unsigned long long* __restrict__ A,
                     const uint8_t* __restrict__ cands, int64_t m, double* __restrict__ D,
@@ -1224,7 +1338,16 @@ cudaError_t launch_eval_range(int L, int ne, int g, const unsigned long long* A,
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  {
+  if (g <= 8 && L <= 248 && !GIMBAL_KNOB("GIMBAL_EVAL_DEV_ATOMIC")) {
+    auto kern = g <= 1 ? eval_dev_bins_kernel<1> : g <= 2 ? eval_dev_bins_kernel<2> : g <= 4 ? eval_dev_bins_kernel<4>
+                : eval_dev_bins_kernel<8>;
+    // eight 16 KB CTAs per SM need a large shared-memory carveout
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)C, 256, 0, s>>>(L, ne, g, A, cands, m, D, flags, bad_index, base);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  } else {
     const int threads = 256;
     const size_t smem = (size_t)(threads / 32) * g * 8 + (size_t)g * 4 + 8;
     e = cudaFuncSetAttribute(eval_dev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
