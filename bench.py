@@ -50,8 +50,8 @@ ATOMS_RANDOM_PEAK = 2.553e12
 # capture (profiles/r2b/ncu_count_r2b_<config>.txt, tools/gpu_profile_r2b.sh), bytes / launch, with
 # the tokens of that launch; for the tensor-core counters also the tensor pipe's active cycles
 # (sm__pipe_tensor_cycles_active, % of elapsed) from the same capture.
-TRAFFIC = {"dsv3": {"bytes": 52.109266e9 + 1.385795e9, "tokens_in_launch": 67108864,
-                    "source": "profiles/r2d/ncu_count_r2d_dsv3.txt"},
+TRAFFIC = {"dsv3": {"bytes": 51.311285e9 + 1.495309e9, "tokens_in_launch": 67108864,
+                    "source": "profiles/r2e/ncu_count_r2e_dsv3.txt"},
            "qwen3": {"bytes": 60.180595e9 + 25.665280e6, "tokens_in_launch": 33554432,
                      "source": "profiles/r2b/ncu_count_r2b_qwen3.txt", "tensor_pipe_active_pct": 35.057135},
            "dsv2lite": {"bytes": 3.962039e9 + 6.150656e6, "tokens_in_launch": 16777216,

@@ -42,7 +42,8 @@ constexpr int kN = 64;         // MMA N: (candidate, gpu) columns per group
 constexpr int kPlanes = 4;     // byte planes of a cell < 2^27
 constexpr int kThreads = 288;  // warps 0-3 epilogue, warps 4-7 producers, warp 8 issuer
 constexpr int kBStages = 2;    // one-hot tiles = TMEM buffers
-constexpr int kIdSlots = 4;    // candidate-id ring, filled two groups ahead
+constexpr int kIdSlotsMax = 16;  // candidate-id ring: 4, 8 or 16 slots (what shared memory holds), filled
+                                 // slots - 2 groups ahead so the bulk copies' latency is hidden
 constexpr int kIssuerWarp = 8;
 
 struct EvalMmaParams {
@@ -50,6 +51,7 @@ struct EvalMmaParams {
   int n_jb, n_cr;  // row blocks per pair, candidate ranges
   int64_t C, m, range_cands, n_units;
   uint32_t idesc;
+  int id_shift;  // log2 of the id-ring slots
 };
 
 // K-major, no swizzle: core matrix = 8 rows x 16 bytes; K-adjacent core matrices LBO = 128 B apart,
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     unsigned long long* __restrict__ same, WidthGuard guard) {
   extern __shared__ __align__(1024) uint8_t smem[];
   if (width_skip(guard)) return;  // a cell >= 2^27: the generic evaluator runs instead
-  __shared__ uint64_t mma_done[kBStages], tmem_free[kBStages], b_full[kBStages], id_full[kIdSlots];
+  __shared__ uint64_t mma_done[kBStages], tmem_free[kBStages], b_full[kBStages], id_full[kIdSlotsMax];
   __shared__ uint32_t tmem_slot;
   // stacked (n_e = 64, ST): A rows [0, 64) = E_l, [64, 128) = E_l+1, each half of the N = 64
   // columns serves one pair, so a group holds 32 / G candidates
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // per candidate: P_c(l+1, 0..n_e) then P_c(l, j0..j0+128); stacked: P_c(l), P_c(l+1), P_c(l+2)
   const int ids_stride = ST ? 3 * ne : ne + kRowsBlk;
   const int ids_bytes = kCpg * ids_stride;
+  const int R = 1 << prm.id_shift;  // id-ring slots
   uint8_t* A = smem;
   uint8_t* Bst = smem + kPlanes * plane_bytes;
   uint8_t* idst = Bst + kBStages * b_bytes;
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_free[s], 4);  // one arrival per epilogue warp
       mbar_init(&b_full[s], 4);     // one arrival per producer warp
     }
-    for (int s = 0; s < kIdSlots; ++s) mbar_init(&id_full[s], 1);
+    for (int s = 0; s < kIdSlotsMax; ++s) mbar_init(&id_full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -186,6 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto fetch_ids = [&](uint32_t slot, int l, int j0, int64_t c0, int n_live) {
     uint8_t* dst = idst + slot * ids_bytes;
     const uint32_t bar = smem_u32(&id_full[slot]);
+    // the slot's previous readers (producers, epilogue) released it through b_full / tmem_free,
+    // which this warp acquired; order those generic-proxy reads before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (ST) {  // one copy per candidate: layers l .. min(l + 2, L - 1)
       const int bytes = min(3, prm.L - l) * ne;
       if (lane == 0)
@@ -217,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   // Both roles walk the same (unit, group) sequence; G_ counts this CTA's groups: B stage / TMEM
-  // buffer = G & 1 (barrier parity (G >> 1) & 1), id slot = G & 3 (parity (G >> 2) & 1).
+  // buffer = G & 1 (barrier parity (G >> 1) & 1), id slot = G mod R (parity (G / R) & 1), R = id-ring slots.
   uint32_t G_ = 0;
   for (int64_t unit = blockIdx.x; unit < prm.n_units; unit += gridDim.x) {
     const int cr = (int)(unit % prm.n_cr);
@@ -234,8 +240,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == kIssuerWarp) {
       // ---------------- issuer: id fetches + MMAs ----------------
-      fetch_ids(G_ & 3, l, j0, c_begin, live(0));
-      if (n_groups > 1) fetch_ids((G_ + 1) & 3, l, j0, c_begin + kCpg, live(1));
+      // groups up to G_ - 3 have finished their epilogues (tmem_free waits): their slots are free
+      for (int gi = 0; gi < min(R - 2, n_groups); ++gi)
+        fetch_ids((G_ + gi) & (R - 1), l, j0, c_begin + (int64_t)gi * kCpg, live(gi));
       for (int gi = 0; gi < n_groups; ++gi) {
         const uint32_t Gg = G_ + gi, s = Gg & 1;
         mbar_wait(&b_full[s], (Gg >> 1) & 1);                          // A (first group) and B(Gg) built
@@ -251,8 +258,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&mma_done[s]);
         }
         __syncwarp();
-        // the slot of group Gg + 2 last served group Gg - 2, whose epilogue has finished
-        if (gi + 2 < n_groups) fetch_ids((Gg + 2) & 3, l, j0, c_begin + (int64_t)(gi + 2) * kCpg, live(gi + 2));
+        // the slot of group Gg + R - 2 last served group Gg - 2, whose epilogue has finished
+        if (gi + R - 2 < n_groups)
+          fetch_ids((Gg + R - 2) & (R - 1), l, j0, c_begin + (int64_t)(gi + R - 2) * kCpg, live(gi + R - 2));
       }
     } else if (warp >= 4) {
       // ---------------- producers: A planes once per unit, a one-hot tile per group ----------------
@@ -301,9 +309,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int gi = 0; gi < n_groups; ++gi) {
         const uint32_t Gg = G_ + gi, s = Gg & 1;
         // one-hot tile: ids landed, and the stage's previous MMAs (group Gg - 2) are done
-        mbar_wait(&id_full[Gg & 3], (Gg >> 2) & 1);
+        mbar_wait(&id_full[Gg & (R - 1)], (Gg >> prm.id_shift) & 1);
         if (Gg >= 2) mbar_wait(&mma_done[s], ((Gg - 2) >> 1) & 1);
-        build_onehot<G, ST>(Bst + s * b_bytes, idst + (Gg & 3) * ids_bytes, ids_stride, ne, live(gi), sbo, pwarp,
+        build_onehot<G, ST>(Bst + s * b_bytes, idst + (Gg & (R - 1)) * ids_bytes, ids_stride, ne, live(gi), sbo, pwarp,
                             lane, halves_live);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -319,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&mma_done[s], (Gg >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         // row jr's assignment P_c(l, j0 + jr); stacked: P_c(l + jr / 64, jr % 64)
-        const uint8_t* ids = idst + (Gg & 3) * ids_bytes + (ST ? (jr >> 6) * ne + (jr & 63) : ne + jr);
+        const uint8_t* ids = idst + (Gg & (R - 1)) * ids_bytes + (ST ? (jr >> 6) * ne + (jr & 63) : ne + jr);
         unsigned long long acc[kCpg];
         uint32_t pj[kCpg];
 #pragma unroll
@@ -383,20 +391,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-size_t eval_mma_smem(int ne, int g);
+size_t eval_mma_smem(int ne, int g, int slots = 4);
 
 bool eval_mma_supported(int L, int ne, int g, const uint8_t* cands, int64_t C) {
   if (GIMBAL_KNOB("GIMBAL_EVAL_ALU")) return false;
   if (!(L > 1 && C > 0 && (ne == 64 || ne == 128 || ne == 256) && (g == 4 || g == 8 || g == 16) &&
         (reinterpret_cast<uintptr_t>(cands) & 15) == 0))  // 16-B aligned bulk copies
     return false;
-  return eval_mma_smem(ne, g) <= 227 * 1024;
+  return eval_mma_smem(ne, g, 4) <= 227 * 1024;
 }
 
-size_t eval_mma_smem(int ne, int g) {
+size_t eval_mma_smem(int ne, int g, int slots) {
   if (ne == 64)  // stacked pairs: 32 / g candidates per group, three id rows each
-    return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)kIdSlots * (kN / 2 / g) * (3 * ne);
-  return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)kIdSlots * (kN / g) * (ne + kRowsBlk);
+    return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)slots * (kN / 2 / g) * (3 * ne);
+  return (size_t)kPlanes * kRowsBlk * ne + (size_t)kBStages * kN * ne + (size_t)slots * (kN / g) * (ne + kRowsBlk);
 }
 
 // same[c] += sum over pairs of the same-GPU weight (same[] zeroed by the caller); E cells < 2^27.
@@ -423,7 +431,11 @@ cudaError_t launch_eval_mma(int L, int ne, int g, const unsigned long long* E, c
   prm.n_units = base * prm.n_cr;
   // c = s32, a = b = u8, both K-major, N >> 3 at bit 17, M >> 4 at bit 24
   prm.idesc = (2u << 4) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kRowsBlk >> 4) << 24);
-  const size_t smem = eval_mma_smem(ne, g);
+  int slots = kIdSlotsMax;
+  if (const char* e = GIMBAL_KNOB("GIMBAL_EVAL_ID_SLOTS")) slots = std::atoi(e);
+  while (slots > 4 && eval_mma_smem(ne, g, slots) > 227 * 1024) slots >>= 1;
+  prm.id_shift = slots == 16 ? 4 : slots == 8 ? 3 : 2;
+  const size_t smem = eval_mma_smem(ne, g, 1 << prm.id_shift);
   // one SM stays free: the greedy walk (one CTA, up to 200 KB of shared memory) of the same pass
   // runs beside the scoring of the other candidates (capi.cu gimbal_pass_async)
   const int grid = (int)std::min<int64_t>(prm.n_units, std::max(1, sms - 1));
