@@ -52,8 +52,8 @@ ATOMS_RANDOM_PEAK = 2.553e12
 # (sm__pipe_tensor_cycles_active, % of elapsed) from the same capture.
 TRAFFIC = {"dsv3": {"bytes": 51.311285e9 + 1.495309e9, "tokens_in_launch": 67108864,
                     "source": "profiles/r2e/ncu_count_r2e_dsv3.txt"},
-           "qwen3": {"bytes": 60.180595e9 + 25.665280e6, "tokens_in_launch": 33554432,
-                     "source": "profiles/r2b/ncu_count_r2b_qwen3.txt", "tensor_pipe_active_pct": 35.057135},
+           "qwen3": {"bytes": 25.095350e9 + 10.015744e6, "tokens_in_launch": 33554432,
+                     "source": "profiles/r2e/ncu_count_r2e_qwen3.txt", "tensor_pipe_active_pct": 35.530166},
            "dsv2lite": {"bytes": 3.962039e9 + 6.150656e6, "tokens_in_launch": 16777216,
                         "source": "profiles/r2b/ncu_count_r2b_dsv2lite.txt", "tensor_pipe_active_pct": 15.320577},
            "mixtral": {"bytes": 67.141888e6 + 429.056e3, "tokens_in_launch": 1048576,

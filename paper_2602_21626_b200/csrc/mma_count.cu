@@ -37,7 +37,9 @@ constexpr int kTok = GIMBAL_MMA_TOK;       // tokens per tile (MMA K, kTok / 32 
 constexpr int kRows = 128;                 // experts per tile row block (MMA M, N <= 128)
 constexpr int kTileBytes = kTok * kRows;   // 16 KB u8 operand tile
 #ifndef GIMBAL_MMA_PAIRS
-#define GIMBAL_MMA_PAIRS 2  // 2 pairs x 128 TMEM columns, 2 CTAs per SM: 29.1 vs 30.1 ms at Qwen3 (4 pairs, 1 CTA)
+// 4 pairs x 128 TMEM columns, 1 CTA per SM: at Qwen3 count 31.70 vs 32.13 ms and 27.1 vs 59.4 GB of DRAM
+// reads for 2 pairs x 2 CTAs per SM (half the groups re-read each trace row; profiles/r2e_qwen3_geometry.txt)
+#define GIMBAL_MMA_PAIRS 4
 #endif
 constexpr int kMaxPairs = GIMBAL_MMA_PAIRS;  // accumulators: kMaxPairs x 128 TMEM columns
 constexpr int kTmemCols = kMaxPairs <= 2 ? 256 : 512;
