@@ -165,24 +165,37 @@ __global__ void online_finish_kernel(long long n, int L, int k, int g, unsigned 
   // gpu_activation_total_[p] += every activation placed on p this iteration
   for (int p = threadIdx.x; p < g; p += blockDim.x) {
     unsigned long long s = 0;
+#pragma unroll 8
     for (int l = 0; l < L; ++l) s += hist[l * g + p];
     gpu_totals[p] += s;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     // sim.cpp:132-144, operation by operation: per_layer = double(n * k); for each layer in order
-    // excess_sum += max(0.0, peak * n_gpus / per_layer - 1.0)  (IEEE, no contraction)
+    // excess_sum += max(0.0, peak * n_gpus / per_layer - 1.0)  (IEEE, no contraction).  Lane i
+    // finds the peaks of layers i, i + 32, ... (independent loads); lane 0 adds the terms in layer
+    // order (a single thread walking all L x g cells cost 15 us at the DS-V3 shape)
+    const int lane = threadIdx.x;
     const double per_layer = (double)(n * (long long)k);
     double sum = 0.0;
-    for (int l = 0; l < L; ++l) {
-      unsigned int peak = 0;
-      for (int p = 0; p < g; ++p) peak = max(peak, hist[l * g + p]);
-      const double x = __dsub_rn(__ddiv_rn(__dmul_rn((double)peak, (double)g), per_layer), 1.0);
-      sum = __dadd_rn(sum, 0.0 < x ? x : 0.0);  // std::max(0.0, x)
+    for (int l0 = 0; l0 < L; l0 += 32) {
+      double x = 0.0;
+      if (l0 + lane < L) {
+        const unsigned int* h = hist + (l0 + lane) * g;
+        unsigned int peak = 0;
+        for (int p = 0; p < g; ++p) peak = max(peak, h[p]);
+        x = __dsub_rn(__ddiv_rn(__dmul_rn((double)peak, (double)g), per_layer), 1.0);
+      }
+      const int cnt = min(32, L - l0);
+      for (int i = 0; i < cnt; ++i) {
+        const double xi = __shfl_sync(0xffffffffu, x, i);
+        sum = __dadd_rn(sum, 0.0 < xi ? xi : 0.0);  // std::max(0.0, x)
+      }
     }
-    out->excess_sum = sum;
-    out->crossings = (long long)*crossings;
-    *crossings = 0;
+    if (lane == 0) {
+      out->excess_sum = sum;
+      out->crossings = (long long)*crossings;
+      *crossings = 0;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < L * g; i += blockDim.x) hist[i] = 0u;

@@ -207,31 +207,45 @@ __device__ __forceinline__ uint32_t ev_tri(uint32_t a, uint32_t b) {
   return ((hi * (hi + 1u)) >> 1) + lo;
 }
 
+// tri of the layer whose two ids are bytes `sh` / 8 and `sh` / 8 + 1 of `w` (ids < 8): the
+// triangular number hi (hi + 1) / 2 comes from a byte permute of the 8-entry table {0, 1, 3, 6, 10,
+// 15, 21, 28} held in two constants (no shared-memory lookup)
+__device__ __forceinline__ uint32_t ev_tri_word(uint32_t w, int sh) {
+  const uint32_t a = (w >> sh) & 7u, b = (w >> (sh + 8)) & 7u;
+  const uint32_t lo = min(a, b), hi = max(a, b);
+  return (__byte_perm(0x06030100u, 0x1c150f0au, hi) & 0xffu) + lo;
+}
+
+__device__ __forceinline__ void ev_add(uint32_t hist_s, uint32_t bin) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hist_s + (bin >> 1) * 4), "r"(1u << ((bin & 1u) << 4))
+               : "memory");
+}
+
+// Q = 16-byte chunks per row (L = 8 Q layers of two ids).  Rows are staged with 16-byte stores at a
+// stride of an odd number of chunks and read back with 16-byte loads (conflict-free per quarter
+// warp); each thread then holds its token's whole row in registers.
+template <int Q>
 __global__ void __launch_bounds__(kEvThreads, 1)
-    count_events8_kernel(int L, const uint8_t* __restrict__ trace, int64_t T, int row_bytes, int stride,
-                         unsigned long long* __restrict__ E, uint32_t* __restrict__ flags) {
+    count_events8_kernel(const uint8_t* __restrict__ trace, int64_t T, unsigned long long* __restrict__ E,
+                         uint32_t* __restrict__ flags) {
+  constexpr int L = 8 * Q, pairs = L - 1, kRowBytes = 16 * Q;
+  constexpr int kStride16 = (Q & 1) ? Q + 2 : Q + 1;  // odd
   extern __shared__ __align__(16) uint8_t sm[];
-  const int pairs = L - 1;
   uint32_t* hist = reinterpret_cast<uint32_t*>(sm);  // [pairs][648]
   uint32_t* tab = hist + pairs * kEvBinWords;        // [pairs][64] cells of rows with bad ids
-  uint8_t* rows = reinterpret_cast<uint8_t*>(tab + pairs * 64);
+  uint4* rows = reinterpret_cast<uint4*>(tab + pairs * 64);
   for (int i = threadIdx.x; i < pairs * (kEvBinWords + 64); i += kEvThreads) hist[i] = 0u;
-  // tri of a token-layer from its two 3-bit ids (a | b << 3): one shared load per layer
-  __shared__ uint8_t tri_tab[64];
-  if (threadIdx.x < 64) tri_tab[threadIdx.x] = (uint8_t)ev_tri(threadIdx.x & 7u, threadIdx.x >> 3);
   bool bad = false;
   const uint32_t hist_s = static_cast<uint32_t>(__cvta_generic_to_shared(hist));
-  constexpr int kPf = 4;  // rows of <= 64 bytes (events8_applies)
-  const int q = row_bytes >> 4;
   const int64_t step = (int64_t)gridDim.x * kEvThreads;
-  uint4 pre[kPf];
+  uint4 pre[Q];
   auto load = [&](int64_t t0) {
     const int n = (int)min((int64_t)kEvThreads, T - t0);
-    const uint4* src = reinterpret_cast<const uint4*>(trace + t0 * row_bytes);
+    const uint4* src = reinterpret_cast<const uint4*>(trace + t0 * kRowBytes);
 #pragma unroll
-    for (int r = 0; r < kPf; ++r) {
+    for (int r = 0; r < Q; ++r) {
       const int i = threadIdx.x + r * kEvThreads;
-      if (i < n * q) pre[r] = __ldcs(src + i);
+      if (i < n * Q) pre[r] = __ldcs(src + i);
     }
   };
   int64_t t0 = (int64_t)blockIdx.x * kEvThreads;
@@ -240,45 +254,44 @@ __global__ void __launch_bounds__(kEvThreads, 1)
     const int n = (int)min((int64_t)kEvThreads, T - t0);
     __syncthreads();  // the previous block's rows are consumed (and the tables are zeroed)
 #pragma unroll
-    for (int r = 0; r < kPf; ++r) {
+    for (int r = 0; r < Q; ++r) {
       const int i = threadIdx.x + r * kEvThreads;
-      if (i < n * q) {
-        const int rr = i / q, w = i - rr * q;
-        uint32_t* d = reinterpret_cast<uint32_t*>(rows + rr * stride + w * 16);
-        d[0] = pre[r].x;
-        d[1] = pre[r].y;
-        d[2] = pre[r].z;
-        d[3] = pre[r].w;
+      if (i < n * Q) {
+        const int rr = i / Q, c = i - rr * Q;
+        rows[rr * kStride16 + c] = pre[r];
       }
     }
     __syncthreads();
     if (t0 + step < T) load(t0 + step);
     if (threadIdx.x < n) {
-      const uint32_t* row = reinterpret_cast<const uint32_t*>(rows + threadIdx.x * stride);
+      uint32_t w[4 * Q];
+#pragma unroll
+      for (int c = 0; c < Q; ++c) {
+        const uint4 v = rows[threadIdx.x * kStride16 + c];
+        w[4 * c] = v.x;
+        w[4 * c + 1] = v.y;
+        w[4 * c + 2] = v.z;
+        w[4 * c + 3] = v.w;
+      }
       uint32_t acc = 0;
-      for (int w = 0; w < L / 2; ++w) acc |= row[w];
+#pragma unroll
+      for (int i = 0; i < 4 * Q; ++i) acc |= w[i];
       if (acc & 0xf8f8f8f8u) {
-        bad |= small_count_row<2>(reinterpret_cast<const uint8_t*>(row), L, 8, tab);
+        bad |= small_count_row<2>(reinterpret_cast<const uint8_t*>(rows + threadIdx.x * kStride16), L, 8, tab);
       } else {
-        // ids < 8 (checked above): a layer's index into tri_tab is (id0 & 7) | (id1 & 7) << 3
-        auto tri_lo = [&](uint32_t v) { return (uint32_t)tri_tab[(v & 7u) | ((v >> 5) & 0x38u)]; };
-        uint32_t w = row[0];
-        uint32_t tp = tri_lo(w) * kEvTri;  // this layer's tri x 36
         uint32_t base = hist_s;
-        for (int lw = 0; lw < L / 2; ++lw) {
-          const uint32_t tn = tri_lo(w >> 16);  // layer 2 lw + 1
-          uint32_t bin = tp + tn;
-          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + (bin >> 1) * 4), "r"(1u << ((bin & 1u) << 4))
-                       : "memory");
+        uint32_t tp = ev_tri_word(w[0], 0) * kEvTri;  // layer 0's tri x 36
+#pragma unroll
+        for (int lw = 0; lw < 4 * Q; ++lw) {
+          const uint32_t tn = ev_tri_word(w[lw], 16);  // layer 2 lw + 1
+          ev_add(base, tp + tn);
           base += kEvBinWords * 4;
-          if (lw + 1 == L / 2) break;
-          w = row[lw + 1];
-          const uint32_t tm = tri_lo(w);  // layer 2 lw + 2
-          bin = tn * kEvTri + tm;
-          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(base + (bin >> 1) * 4), "r"(1u << ((bin & 1u) << 4))
-                       : "memory");
-          base += kEvBinWords * 4;
-          tp = tm * kEvTri;
+          if (lw + 1 < 4 * Q) {
+            const uint32_t tm = ev_tri_word(w[lw + 1], 0);  // layer 2 lw + 2
+            ev_add(base, tn * kEvTri + tm);
+            base += kEvBinWords * 4;
+            tp = tm * kEvTri;
+          }
         }
       }
     }
@@ -310,7 +323,9 @@ __global__ void __launch_bounds__(kEvThreads, 1)
 }
 
 size_t events8_smem(int L) {
-  return (size_t)(L - 1) * (kEvBinWords + 64) * 4 + (size_t)kEvThreads * (L * 2 + 4);
+  const int q = L / 8;
+  const int stride16 = (q & 1) ? q + 2 : q + 1;
+  return (size_t)(L - 1) * (kEvBinWords + 64) * 4 + (size_t)kEvThreads * stride16 * 16;
 }
 
 size_t small_smem(int L, int ne, int k, int threads = kSmallThreads) {
@@ -341,16 +356,24 @@ bool small_count_supported(int L, int ne, int k, int id_bytes, int64_t T) {
 cudaError_t launch_count_small(int L, int ne, int k, int sms, const uint8_t* trace, int64_t T,
                                unsigned long long* E, uint32_t* flags, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  if (ne == 8 && small2_applies(L, ne, k, trace) && L * k <= 64 && events8_smem(L) <= 200 * 1024 &&
+  if (ne == 8 && small2_applies(L, ne, k, trace) && L % 8 == 0 && L * k <= 64 && events8_smem(L) <= 200 * 1024 &&
       !GIMBAL_KNOB("GIMBAL_SMALL_BYTEWISE") && !GIMBAL_KNOB("GIMBAL_SMALL_NO_EVENTS")) {
     const int64_t blocks = (T + kEvThreads - 1) / kEvThreads;
     int64_t grid = std::min<int64_t>(sms, blocks);
     grid = std::max<int64_t>(grid, (blocks + kEvMaxBlocks - 1) / kEvMaxBlocks);  // u16 bins
     const size_t smem = events8_smem(L);
-    cudaError_t e = cudaFuncSetAttribute(count_events8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    count_events8_kernel<<<(unsigned)grid, kEvThreads, smem, s>>>(L, trace, T, L * k, L * k + 4, E, flags);
-    return cudaGetLastError();
+    auto go = [&](auto kern) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<(unsigned)grid, kEvThreads, smem, s>>>(trace, T, E, flags);
+      return cudaGetLastError();
+    };
+    switch (L / 8) {
+      case 1: return go(count_events8_kernel<1>);
+      case 2: return go(count_events8_kernel<2>);
+      case 3: return go(count_events8_kernel<3>);
+      default: return go(count_events8_kernel<4>);
+    }
   }
   if (small2_applies(L, ne, k, trace) && !GIMBAL_KNOB("GIMBAL_SMALL_BYTEWISE")) {
     const size_t smem = small_smem(L, ne, k, kSmall2Threads);
