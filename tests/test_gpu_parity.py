@@ -163,7 +163,12 @@ def test_mma_stack_out_of_range(G, bad):
                                                   (32, 8, 5000, 0, True, None), (16, 16, 9001, 0, True, None),
                                                   (32, 8, 3000, 0, False, (2999, 31, 1, 8)),
                                                   (32, 16, 3000, 0, False, (5, 0, 0, 200)),
-                                                  (32, 8, 3000, 8, False, None), (30, 8, 3000, 0, False, None)])
+                                                  (32, 8, 3000, 8, False, None), (30, 8, 3000, 0, False, None),
+                                                  # the event-histogram counter's other row widths (L = 8, 16, 24)
+                                                  (8, 8, 4099, 0, True, None), (8, 8, 1, 0, False, None),
+                                                  (16, 8, 70001, 0, False, None), (24, 8, 3000, 0, True, None),
+                                                  (24, 8, 3000, 0, False, (1234, 23, 1, 9)),
+                                                  (16, 8, 2000, 0, False, (0, 0, 0, 255))])
 def test_small2_count_layouts(G, orc, L, ne, T, offset, dup, bad):
     """Top-2 traces of 8 / 16 experts are counted word-wise (small_count.cu small_count_row2):
     ragged blocks, one token, repeated ids, an out-of-range id (that row falls back to the
