@@ -20,9 +20,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "internal.cuh"
@@ -207,6 +211,69 @@ __global__ void online_finish_kernel(long long n, int L, int k, int g, unsigned 
 
 using namespace gimbal_gpu;
 
+namespace {
+
+// A few persistent host threads that stage large batches of routed ids into the pinned buffer
+// together (a 4096-token DS-V3 batch is 1.9 MB of uint8 or 7.6 MB of int32 ids; one core narrows
+// int32 at ~8 GB/s).  run(f) calls f(part) for every part, part 0 on the caller, and returns when
+// all have finished.  Created on the first large batch of a handle.
+class HostPool {
+ public:
+  explicit HostPool(int parts) : parts_(parts) {
+    for (int i = 1; i < parts; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (std::thread& t : th_) t.join();
+  }
+  int parts() const { return parts_; }
+  void run(const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      remaining_ = parts_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return remaining_ == 0; });
+  }
+
+ private:
+  void loop(int part) {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      const std::function<void(int)>* f = job_;
+      lk.unlock();
+      (*f)(part);
+      lk.lock();
+      if (--remaining_ == 0) done_.notify_one();
+    }
+  }
+  const int parts_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int remaining_ = 0;
+  bool stop_ = false;
+};
+
+constexpr size_t kPoolMinBytes = 1u << 20;  // int32 input bytes from which narrowing is split over threads
+
+}  // namespace
+
 struct gimbal_online_s {
   gimbal_stats_t window = nullptr;
   StatsInternals si;
@@ -232,6 +299,7 @@ struct gimbal_online_s {
     cudaGraphNode_t n_h2d = nullptr, n_count = nullptr, n_pairs = nullptr, n_finish = nullptr;
   } gr[2];
   int64_t iterations = 0;
+  std::unique_ptr<HostPool> pool;  // host staging threads (created on the first large batch)
 
   void release() {
     for (Graph& x : gr) {
@@ -484,22 +552,43 @@ int gimbal_online_iteration(gimbal_online_t o, const void* ids, int id_bytes, in
   GIMBAL_TRY(stats_resolve_tokens(o->window));
   GIMBAL_TRY(grow(o, n));
   const size_t cnt = (size_t)n * o->L * o->k;
-  if (id_bytes == 1) {
-    std::memcpy(o->h_ids, ids, cnt);
-  } else {  // int32 (RoutedStream::choices) -> uint8 (n_e <= 256); the reference leaves bad ids UB
-    // branch-free (vectorisable) conversion with one range verdict for the whole batch
+  // int32 (RoutedStream::choices) -> uint8 (n_e <= 256; the reference leaves bad ids UB): a
+  // branch-free (vectorisable) conversion with one range verdict per part
+  const uint32_t ne = (uint32_t)o->ne;
+  auto stage = [&](size_t b, size_t e) -> uint32_t {
+    if (id_bytes == 1) {
+      std::memcpy(o->h_ids + b, static_cast<const uint8_t*>(ids) + b, e - b);
+      return 0u;
+    }
     const int32_t* s = static_cast<const int32_t*>(ids);
-    const uint32_t ne = (uint32_t)o->ne;
     uint32_t bad = 0;
-    for (size_t i = 0; i < cnt; ++i) {
+    for (size_t i = b; i < e; ++i) {
       const uint32_t v = (uint32_t)s[i];  // negative ids wrap above n_e
       bad |= v >= ne ? 1u : 0u;
       o->h_ids[i] = (uint8_t)v;
     }
-    if (bad) {
-      set_error("add_token: expert id out of range [0, n_experts)");
-      return GIMBAL_OUT_OF_RANGE;
+    return bad;
+  };
+  uint32_t bad = 0;
+  if (id_bytes == 4 && cnt * 4 >= kPoolMinBytes) {  // (a uint8 memcpy is faster alone than woken threads)
+    if (!o->pool) {
+      const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+      o->pool.reset(new HostPool((int)std::min(8u, hw / 2)));
     }
+    const int parts = o->pool->parts();
+    std::vector<uint32_t> bads((size_t)parts, 0u);
+    const size_t per = ((cnt + parts - 1) / parts + 63) & ~(size_t)63;
+    o->pool->run([&](int p) {
+      const size_t b = std::min(cnt, (size_t)p * per), e = std::min(cnt, b + per);
+      bads[(size_t)p] = stage(b, e);
+    });
+    for (uint32_t x : bads) bad |= x;
+  } else {
+    bad = stage(0, cnt);
+  }
+  if (bad) {
+    set_error("add_token: expert id out of range [0, n_experts)");
+    return GIMBAL_OUT_OF_RANGE;
   }
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(4 * 148, (n * o->L + kOnlineThreads - 1) / kOnlineThreads));

@@ -84,6 +84,15 @@ int main(int argc, char** argv) {
         }
       printf("{\"what\": \"gimbal_online_iteration\", \"shape\": \"%s\", \"tokens\": %d, \"us\": %.2f}\n", sh.name, n,
              (now_us() - t0) / iters);
+      std::vector<int32_t> ids32(ids.begin(), ids.end());  // RoutedStream::choices as the engine passes them
+      t0 = now_us();
+      for (int i = 0; i < iters; ++i)
+        if (gimbal_online_iteration(o, ids32.data(), 4, n, &ex, &cr)) {
+          printf("iteration failed: %s\n", gimbal_last_error());
+          return 1;
+        }
+      printf("{\"what\": \"gimbal_online_iteration, int32 ids\", \"shape\": \"%s\", \"tokens\": %d, \"us\": %.2f}\n",
+             sh.name, n, (now_us() - t0) / iters);
       gimbal_online_destroy(o);
       gimbal_stats_destroy(w);
     }
