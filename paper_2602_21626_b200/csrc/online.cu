@@ -220,17 +220,14 @@ namespace {
 class HostPool {
  public:
   explicit HostPool(int parts) : parts_(parts) {
-    for (int i = 1; i < parts; ++i) th_.emplace_back([this, i] { loop(i); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-      ++gen_;
+    try {
+      for (int i = 1; i < parts; ++i) th_.emplace_back([this, i] { loop(i); });
+    } catch (...) {  // the threads already started are stopped and joined before rethrowing
+      shutdown();
+      throw;
     }
-    cv_.notify_all();
-    for (std::thread& t : th_) t.join();
   }
+  ~HostPool() { shutdown(); }
   int parts() const { return parts_; }
   void run(const std::function<void(int)>& f) {
     {
@@ -246,6 +243,16 @@ class HostPool {
   }
 
  private:
+  void shutdown() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (std::thread& t : th_) t.join();
+    th_.clear();
+  }
   void loop(int part) {
     uint64_t seen = 0;
     std::unique_lock<std::mutex> lk(mu_);
@@ -300,6 +307,7 @@ struct gimbal_online_s {
   } gr[2];
   int64_t iterations = 0;
   std::unique_ptr<HostPool> pool;  // host staging threads (created on the first large batch)
+  bool pool_failed = false;        // thread creation failed once: stage on the calling thread
 
   void release() {
     for (Graph& x : gr) {
@@ -570,11 +578,17 @@ int gimbal_online_iteration(gimbal_online_t o, const void* ids, int id_bytes, in
     return bad;
   };
   uint32_t bad = 0;
-  if (id_bytes == 4 && cnt * 4 >= kPoolMinBytes) {  // (a uint8 memcpy is faster alone than woken threads)
+  if (id_bytes == 4 && cnt * 4 >= kPoolMinBytes && !o->pool_failed) {  // (uint8: one memcpy beats woken threads)
     if (!o->pool) {
       const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
-      o->pool.reset(new HostPool((int)std::min(8u, hw / 2)));
+      try {
+        o->pool.reset(new HostPool((int)std::min(8u, hw / 2)));
+      } catch (const std::exception&) {  // no threads to be had: stage on the calling thread
+        o->pool_failed = true;
+      }
     }
+  }
+  if (o->pool && id_bytes == 4 && cnt * 4 >= kPoolMinBytes) {
     const int parts = o->pool->parts();
     std::vector<uint32_t> bads((size_t)parts, 0u);
     const size_t per = ((cnt + parts - 1) / parts + 63) & ~(size_t)63;
