@@ -207,13 +207,15 @@ __device__ __forceinline__ uint32_t ev_tri(uint32_t a, uint32_t b) {
   return ((hi * (hi + 1u)) >> 1) + lo;
 }
 
-// tri of the layer whose two ids are bytes `sh` / 8 and `sh` / 8 + 1 of `w` (ids < 8): the
-// triangular number hi (hi + 1) / 2 comes from a byte permute of the 8-entry table {0, 1, 3, 6, 10,
-// 15, 21, 28} held in two constants (no shared-memory lookup)
-__device__ __forceinline__ uint32_t ev_tri_word(uint32_t w, int sh) {
-  const uint32_t a = (w >> sh) & 7u, b = (w >> (sh + 8)) & 7u;
-  const uint32_t lo = min(a, b), hi = max(a, b);
-  return (__byte_perm(0x06030100u, 0x1c150f0au, hi) & 0xffu) + lo;
+// Both layers of a row word at once (bytes a0 b0 a1 b1, ids < 8): the two ids of each layer go to
+// 16-bit lanes, min / max per lane (min.u16x2 / max.u16x2), one byte permute of the triangular-number
+// table for both his: tri of layer 0 in the low half, of layer 1 in the high half.
+__device__ __forceinline__ uint32_t ev_tri2(uint32_t w) {
+  const uint32_t a = __byte_perm(w, 0u, 0x4240), b = __byte_perm(w, 0u, 0x4341);
+  uint32_t lo, hi;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(lo) : "r"(a), "r"(b));
+  asm("max.u16x2 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(b));
+  return __byte_perm(0x06030100u, 0x1c150f0au, hi | (hi >> 8)) + lo;
 }
 
 __device__ __forceinline__ void ev_add(uint32_t hist_s, uint32_t bin) {
@@ -280,17 +282,16 @@ __global__ void __launch_bounds__(kEvThreads, 1)
         bad |= small_count_row<2>(reinterpret_cast<const uint8_t*>(rows + threadIdx.x * kStride16), L, 8, tab);
       } else {
         uint32_t base = hist_s;
-        uint32_t tp = ev_tri_word(w[0], 0) * kEvTri;  // layer 0's tri x 36
+        uint32_t t2 = ev_tri2(w[0]);
 #pragma unroll
         for (int lw = 0; lw < 4 * Q; ++lw) {
-          const uint32_t tn = ev_tri_word(w[lw], 16);  // layer 2 lw + 1
-          ev_add(base, tp + tn);
+          const uint32_t tp = t2 & 0xffffu, tn = t2 >> 16;  // layers 2 lw, 2 lw + 1
+          ev_add(base, tp * kEvTri + tn);
           base += kEvBinWords * 4;
           if (lw + 1 < 4 * Q) {
-            const uint32_t tm = ev_tri_word(w[lw + 1], 0);  // layer 2 lw + 2
-            ev_add(base, tn * kEvTri + tm);
+            t2 = ev_tri2(w[lw + 1]);
+            ev_add(base, tn * kEvTri + (t2 & 0xffffu));  // layers 2 lw + 1, 2 lw + 2
             base += kEvBinWords * 4;
-            tp = tm * kEvTri;
           }
         }
       }
