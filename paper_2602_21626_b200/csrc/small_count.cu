@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(kEvThreads, 1)
                          uint32_t* __restrict__ flags) {
   constexpr int L = 8 * Q, pairs = L - 1, kRowBytes = 16 * Q;
   constexpr int kStride16 = (Q & 1) ? Q + 2 : Q + 1;  // odd
+  static_assert(pairs * kEvTri * 8 * 4 <= kEvThreads * kStride16 * 16, "the expansion's G fits the row staging");
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* hist = reinterpret_cast<uint32_t*>(sm);  // [pairs][648]
   uint32_t* tab = hist + pairs * kEvBinWords;        // [pairs][64] cells of rows with bad ids
@@ -298,26 +299,32 @@ __global__ void __launch_bounds__(kEvThreads, 1)
     }
   }
   __syncthreads();
-  // expand the events into the pair's 8 x 8 cells (one thread per cell, no atomics), add to E
+  // expand the events into the pair's 8 x 8 cells in two steps (no atomics; the row staging area
+  // holds the intermediate):
+  //   G_l(t, k) = sum over the 8 multisets t' containing k of H_l(t, t') m(k, t')   (36 x 8 per pair)
+  //   E_l(j, k) = sum over the 8 multisets t containing j of m(j, t) G_l(t, k)
+  // 72 bin reads per cell instead of 64 per cell of the one-step sum, 31 % fewer in all
+  uint32_t* Gt = reinterpret_cast<uint32_t*>(rows);  // [pairs][36][8]
+  for (int idx = threadIdx.x; idx < pairs * kEvTri * 8; idx += kEvThreads) {
+    const int p = idx / (kEvTri * 8), r = idx - p * (kEvTri * 8), t = r >> 3, kk = r & 7;
+    const uint32_t* H = hist + p * kEvBinWords;
+    uint32_t g = 0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const uint32_t bin = (uint32_t)t * kEvTri + ev_tri((uint32_t)kk, (uint32_t)y);
+      const uint32_t c = (H[bin >> 1] >> ((bin & 1u) << 4)) & 0xffffu;
+      g += y == kk ? 2u * c : c;
+    }
+    Gt[idx] = g;
+  }
+  __syncthreads();
   for (int cell = threadIdx.x; cell < pairs * 64; cell += kEvThreads) {
     const int p = cell >> 6, j = (cell >> 3) & 7, kk = cell & 7;
-    const uint32_t* H = hist + p * kEvBinWords;
+    const uint32_t* Gp = Gt + p * (kEvTri * 8);
     unsigned long long sum = tab[cell];
-    uint32_t tk[8];
 #pragma unroll
-    for (int y = 0; y < 8; ++y) tk[y] = ev_tri((uint32_t)kk, (uint32_t)y);
-#pragma unroll 1
-    for (int x = 0; x < 8; ++x) {
-      const uint32_t tj = ev_tri((uint32_t)j, (uint32_t)x) * kEvTri;
-      uint32_t row_sum = 0;
-#pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const uint32_t bin = tj + tk[y];
-        const uint32_t c = (H[bin >> 1] >> ((bin & 1u) << 4)) & 0xffffu;
-        row_sum += y == kk ? 2u * c : c;
-      }
-      sum += (unsigned long long)(x == j ? 2u : 1u) * row_sum;
-    }
+    for (int x = 0; x < 8; ++x)
+      sum += (unsigned long long)(x == j ? 2u : 1u) * Gp[ev_tri((uint32_t)j, (uint32_t)x) * 8 + kk];
     if (sum) atomicAdd(E + cell, sum);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, (uint32_t)kFlagIdOutOfRange);
