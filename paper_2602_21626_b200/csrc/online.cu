@@ -62,6 +62,51 @@ __global__ void __launch_bounds__(kOnlineThreads)
     const int l = (int)(u - t * L);
     const uint8_t* row = ids + (t * L + l) * k;
     const uint8_t* pl = place + (long long)l * ne;
+    if (k <= 8) {
+      // top-k <= 8: the unit's ids and the next layer's, loaded up front into two registers (the
+      // small-batch graph reads them zero-copy from pinned host memory: one round trip, not one per
+      // dependent id)
+      const bool pairs = with_pairs && l + 1 < L;
+      unsigned long long cw = 0, nw = 0;
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (a < k) {
+          cw |= (unsigned long long)row[a] << (8 * a);
+          if (pairs) nw |= (unsigned long long)row[k + a] << (8 * a);
+        }
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        if (a >= k) break;
+        const uint32_t e = (uint32_t)(cw >> (8 * a)) & 0xffu;
+        if (e >= (uint32_t)ne) {
+          bad = true;
+          continue;
+        }
+        atomicAdd(&sh_hist[l * g + pl[e]], 1u);
+        if (L == 1) atomicAdd(A + e, 1ull);
+      }
+      if (pairs) {
+        const uint8_t* pn = pl + ne;
+        unsigned long long* El = E + (long long)l * nE;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          if (a >= k) break;
+          const uint32_t j = (uint32_t)(cw >> (8 * a)) & 0xffu;
+          if (j >= (uint32_t)ne) continue;
+          const uint32_t pj = pl[j];
+          unsigned long long* Erow = El + (long long)j * ne;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (b >= k) break;
+            const uint32_t kk = (uint32_t)(nw >> (8 * b)) & 0xffu;
+            if (kk >= (uint32_t)ne) continue;
+            atomicAdd(Erow + kk, 1ull);
+            cross += (pj != pn[kk]) ? 1u : 0u;
+          }
+        }
+      }
+      continue;
+    }
     for (int a = 0; a < k; ++a) {  // layer_gpu_tokens_(l, P(f(l, e))) += 1 (sim.cpp:117-126)
       const uint32_t e = row[a];
       if (e >= (uint32_t)ne) {
